@@ -1,0 +1,207 @@
+/*
+ * dmath_b200 -- C ABI of the B200-native distributed fp32 GEMM path.
+ *
+ * Drop-in boundary for the reference's distributed-matrix/GEMM API
+ * (arxiv 1604.01416 "dMath", code under /root/reference/proj/include/gridgemm).
+ * Every entry point names the reference interface it replaces (file:line,
+ * relative to /root/reference/proj/include/gridgemm/).  Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary.
+ *
+ * All functions return a dm_status (0 = ok).  On error, dm_last_error()
+ * returns the message of the failing call on this thread; the code maps 1:1
+ * onto the reference's exception classes (common.hpp:22-78).
+ */
+#ifndef DMATH_B200_H_
+#define DMATH_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DMATH_B200_ABI_VERSION 1
+
+/* ---- status codes: reference exception classes (common.hpp:22-78) ---- */
+enum dm_status {
+  DM_OK = 0,
+  DM_ERR_USAGE = 1,       /* UsageError      common.hpp:28-32 */
+  DM_ERR_CONFIG = 2,      /* ConfigError     common.hpp:34-38 */
+  DM_ERR_SHAPE = 3,       /* ShapeError      common.hpp:40-44 */
+  DM_ERR_PROTOCOL = 4,    /* ProtocolError   common.hpp:46-51 */
+  DM_ERR_DEADLOCK = 5,    /* DeadlockError   common.hpp:53-57 */
+  DM_ERR_INTEGRITY = 6,   /* IntegrityError  common.hpp:59-63 */
+  DM_ERR_PLAN = 7,        /* PlanError       common.hpp:65-70 */
+  DM_ERR_CACHE_MISS = 8,  /* CacheMissError  common.hpp:72-78 */
+  DM_ERR_CUDA = 9,        /* device runtime failure (no reference equivalent) */
+  DM_ERR_NCCL = 10,       /* NCCL failure (no reference equivalent) */
+  DM_ERR_UNSUPPORTED = 11 /* outside the fp32 hot path (Half16/Double64 storage) */
+};
+
+/* ---- enums mirroring the reference ---- */
+enum dm_layout_kind { /* layout.hpp:69-75 */
+  DM_ROW_BLOCKS_1D = 0,
+  DM_COL_BLOCKS_1D = 1,
+  DM_ROW_CYCLIC_1D = 2,
+  DM_CHECKERBOARD_2D = 3,
+  DM_CUSTOM = 4
+};
+enum dm_precision { DM_HALF16 = 0, DM_SINGLE32 = 1, DM_DOUBLE64 = 2 }; /* precision.hpp:14 */
+enum dm_fill { DM_FILL_ZEROS = 0, DM_FILL_SEEDED = 1, DM_FILL_FROM_HOST = 2 }; /* runtime_types.hpp:68 */
+enum dm_mode {
+  DM_MODE_LOCAL = 0, /* one process drives every worker (reference Session, session.hpp:64-76) */
+  DM_MODE_SPMD = 1   /* one process per GPU; every rank makes the same calls (torchrun) */
+};
+
+/* LayoutSpec (layout.hpp:116-142): block grid + kind + worker count.
+ * `custom` is the row-major n_block_rows x n_block_cols owner table (Custom only). */
+typedef struct dm_layout {
+  int32_t kind;
+  int32_t worker_count;
+  int64_t global_rows, global_cols;
+  int64_t block_rows, block_cols;
+  const int32_t* custom;
+  int64_t custom_len;
+} dm_layout;
+
+/* Pool::Stats (pool.hpp:63-69), per worker device pool. */
+typedef struct dm_pool_stats {
+  uint64_t fresh_allocations;
+  uint64_t reuses;
+  uint64_t bytes_live;
+  uint64_t bytes_pooled;
+  uint64_t high_water;
+} dm_pool_stats;
+
+/* Data-movement and kernel counters of one worker (cumulative). */
+typedef struct dm_worker_stats {
+  uint64_t peer_bytes_read;   /* operand bytes pulled from other workers' blocks */
+  uint64_t local_bytes_read;  /* operand bytes read from own owned/cached blocks */
+  uint64_t gemm_launches;     /* tcgen05 GEMM kernel launches */
+  uint64_t split_launches;    /* split/pull kernel launches */
+  double gemm_flops;          /* algorithmic 2*m*n*k of those launches */
+  double gemm_ms;             /* CUDA-event time of the GEMM launches (timing enabled) */
+} dm_worker_stats;
+
+/* MatrixDescriptor (layout.hpp:224-236). */
+typedef struct dm_descriptor {
+  uint64_t matrix_id;
+  int32_t precision;
+  int32_t replicated;
+  uint64_t version;
+  uint64_t replica_version;
+  uint64_t seed;
+  dm_layout layout; /* layout.custom points into session-owned storage */
+} dm_descriptor;
+
+typedef struct dm_session_config {
+  int32_t worker_count;     /* P (Config::worker_count, session.hpp:56) */
+  int32_t mode;             /* dm_mode */
+  int32_t rank;             /* SPMD: this process's worker id */
+  int32_t coherence_checks; /* Config::coherence_checks (session.hpp:61) */
+  uint64_t root_seed;       /* Config::root_seed (session.hpp:59) */
+  const int32_t* devices;   /* LOCAL: device of each worker (NULL = w % device_count) */
+  const void* nccl_id;      /* SPMD: 128-byte ncclUniqueId from rank 0 (dm_nccl_unique_id) */
+} dm_session_config;
+
+typedef struct dm_session dm_session;
+typedef uint64_t dm_matrix_id;
+
+/* ---- diagnostics ---- */
+const char* dm_last_error(void);
+/* CacheMissError::missing_coords of the last failure: fills up to cap (row,col)
+ * pairs into coords[2*i], returns the total count. */
+int dm_last_error_missing(int32_t* coords, int cap);
+int dm_abi_version(void);
+
+/* ---- host-only geometry (no GPU needed) ---- */
+/* detail::checkerboard_dims (layout.hpp:100-105) */
+int dm_checkerboard_dims(int workers, int* pr, int* pc);
+/* LayoutSpec::owner (layout.hpp:122-139) */
+int dm_layout_owner(const dm_layout* layout, int row, int col, int* owner);
+/* BlockGrid::n_block_rows/cols (layout.hpp:34-40), clamped flag (make_grid, layout.hpp:49-59) */
+int dm_layout_grid(const dm_layout* layout, int* n_block_rows, int* n_block_cols, int* clamped);
+/* block_extent (layout.hpp:62-67) */
+int dm_block_extent(const dm_layout* layout, int row, int col, int64_t* rows, int64_t* cols);
+/* layout_to_string (layout.hpp:174-187); returns needed length incl. NUL */
+int dm_layout_to_string(const dm_layout* layout, char* buf, int cap);
+/* Pool::size_class (pool.hpp:121-125) */
+uint64_t dm_pool_size_class(uint64_t bytes);
+/* GEMM data-movement plan of worker `w` for general_gemm on these layouts:
+ * counts the distinct peer blocks w must read (GeneralGemmExec::add_needed,
+ * ops.hpp:503-524) and their bytes.  Pure host logic. */
+int dm_plan_general_gemm(const dm_layout* a, int trans_a, const dm_layout* b, int trans_b,
+                         const dm_layout* c, int worker, int64_t* peer_blocks,
+                         int64_t* peer_bytes);
+
+/* ---- session (Session, session.hpp:53-485) ---- */
+/* Session::Session (session.hpp:64-76).  SPMD: collective over all ranks. */
+int dm_session_create(const dm_session_config* cfg, dm_session** out);
+/* Session::~Session / shutdown (session.hpp:467-481). Idempotent. */
+int dm_session_destroy(dm_session* s);
+int dm_session_shutdown(dm_session* s);
+int dm_nccl_unique_id(void* out128);
+
+/* create_matrix (session.hpp:129-150); host used for DM_FILL_FROM_HOST
+ * (row-major global_rows x global_cols fp32). */
+int dm_create_matrix(dm_session* s, const dm_layout* layout, int precision, int fill,
+                     const void* host, dm_matrix_id* out);
+/* destroy_matrix (session.hpp:152-160) */
+int dm_destroy_matrix(dm_session* s, dm_matrix_id id);
+/* scatter (session.hpp:164-175): host row-major rows x cols, bit-exact. */
+int dm_scatter(dm_session* s, dm_matrix_id id, const void* host, int64_t rows, int64_t cols);
+/* gather (session.hpp:179-201): owned blocks only, bit-exact.  root >= 0:
+ * the full matrix lands in `host` of worker `root`'s process (SPMD) --
+ * LOCAL sessions always fill the whole matrix; root = -1 (SPMD): every rank
+ * writes only the blocks it owns into its own `host`. */
+int dm_gather(dm_session* s, dm_matrix_id id, void* host, int64_t rows, int64_t cols, int root);
+/* general_gemm (session.hpp:244-250): C <- alpha op(A) op(B) + beta C */
+int dm_general_gemm(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b, double beta,
+                    dm_matrix_id c, int trans_a, int trans_b);
+/* cyclic_gemm (session.hpp:226-234): ring-plan preconditions (ops.hpp:84-169) */
+int dm_cyclic_gemm(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b, double beta,
+                   dm_matrix_id c, int trans_a, int trans_b, int cache_a);
+/* broadcast_gemm_reference (session.hpp:236-242) */
+int dm_broadcast_gemm_reference(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b,
+                                double beta, dm_matrix_id c, int trans_a, int trans_b);
+/* cached_backward_gemm (session.hpp:254-264): dX <- W dY, zero transfers */
+int dm_cached_backward_gemm(dm_session* s, dm_matrix_id w, dm_matrix_id dy, dm_matrix_id dx);
+
+/* ---- introspection ---- */
+int dm_worker_count(dm_session* s, int* out);
+int dm_local_workers(dm_session* s, int32_t* ids, int cap); /* returns count */
+int dm_descriptor_get(dm_session* s, dm_matrix_id id, dm_descriptor* out); /* session.hpp:93-97 */
+int dm_pool_stats_get(dm_session* s, int worker, dm_pool_stats* out);     /* session.hpp:102 */
+int dm_pool_trim(dm_session* s, int worker, uint64_t* freed);             /* pool.hpp:110-115 */
+int dm_worker_stats_get(dm_session* s, int worker, dm_worker_stats* out);
+int dm_worker_stats_reset(dm_session* s);
+/* Record CUDA events around every GEMM launch (fills gemm_ms). */
+int dm_set_gemm_timing(dm_session* s, int enable);
+int dm_worker_seed(dm_session* s, int worker, uint64_t* out); /* session.hpp:103 */
+int dm_descriptor_digest(dm_session* s, uint64_t* master, uint64_t* workers, int cap);
+/* device pointer of an owned block (for tests / zero-copy interop) */
+int dm_block_device_ptr(dm_session* s, dm_matrix_id id, int row, int col, void** ptr,
+                        int* device);
+int dm_barrier(dm_session* s);
+
+/* ---- the per-worker BLAS seam: local_gemm (kernels.hpp:81-89) on device
+ * memory.  op(A) is m x k (A stored k x m when trans_a), op(B) is k x n (B
+ * stored n x k when trans_b), row pitches in elements.  Stream-ordered on
+ * `stream` (cudaStream_t, NULL = legacy default). ---- */
+int dm_local_gemm_f32(double alpha, const float* a, int64_t lda, int trans_a, const float* b,
+                      int64_t ldb, int trans_b, double beta, float* c, int64_t ldc, int64_t m,
+                      int64_t n, int64_t k, void* stream);
+/* Same, forcing the tile shape: cta_group 1 (128x128 tiles) or 2 (256x256 CTA-pair tiles). */
+int dm_local_gemm_f32_ex(double alpha, const float* a, int64_t lda, int trans_a, const float* b,
+                         int64_t ldb, int trans_b, double beta, float* c, int64_t ldc, int64_t m,
+                         int64_t n, int64_t k, int cta_group, void* stream);
+/* WorkerContext::fill_seeded (runtime_types.hpp:208-218) for one block. */
+int dm_fill_seeded_f32(float* dst, int64_t count, uint64_t matrix_seed, int block_row,
+                       int block_col, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DMATH_B200_H_ */

@@ -1,0 +1,395 @@
+// extern "C" boundary (include/dmath_b200.h).  Every entry point converts
+// exceptions into dm_status codes 1:1 with the reference's exception classes
+// (gridgemm/common.hpp:22-78) and records the message for dm_last_error().
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <set>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "../../include/dmath_b200.h"
+#include "kernels/tf32x3_gemm.h"
+#include "runtime/layout.hpp"
+#include "runtime/pool.hpp"
+#include "runtime/session.hpp"
+
+struct dm_session {
+  std::unique_ptr<dm::Session> impl;
+  std::map<dm::MatrixId, std::vector<int32_t>> custom_tables;  // backing for dm_descriptor
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local std::vector<std::pair<int, int>> g_last_missing;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    g_last_missing.clear();
+    return DM_OK;
+  } catch (const dm::CacheMissError& e) {
+    g_last_error = e.what();
+    g_last_missing = e.missing_coords;
+    return e.code();
+  } catch (const dm::Error& e) {
+    g_last_error = e.what();
+    g_last_missing.clear();
+    return e.code();
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return DM_ERR_USAGE;
+  }
+}
+
+dm::Session& S(dm_session* s) {
+  if (s == nullptr || !s->impl) throw dm::UsageError("null session");
+  return *s->impl;
+}
+
+// Scratch for the stateless local_gemm seam: one pool per device.
+dm::DevicePool& seam_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<dm::DevicePool>> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& p = pools[dev];
+  if (!p) p = std::make_unique<dm::DevicePool>(dev);
+  return *p;
+}
+
+int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const float* b, int64_t ldb,
+                    int tb, double beta, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
+                    int cta_group, void* stream) {
+  return guarded([&] {
+    if (m < 0 || n < 0 || k < 0) throw dm::ShapeError("local_gemm: negative dimension");
+    if ((m > 0 && n > 0) && c == nullptr) throw dm::UsageError("local_gemm: null C");
+    if (k > 0 && (a == nullptr || b == nullptr)) throw dm::UsageError("local_gemm: null operand");
+    if (ldc < n) throw dm::ShapeError("local_gemm: ldc < n");
+    if (lda < (ta ? m : k) || ldb < (tb ? k : n)) throw dm::ShapeError("local_gemm: bad pitch");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int dev = 0;
+    dm::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    dm::DevicePool& pool = seam_pool(dev);
+    const int64_t kp = std::max<int64_t>(4, (k + 3) / 4 * 4);
+    dm::DeviceBuffer ah, al, bh, bl;
+    if (k > 0 && m > 0 && n > 0) {
+      ah = pool.acquire(static_cast<size_t>(m * kp) * 4);
+      al = pool.acquire(static_cast<size_t>(m * kp) * 4);
+      bh = pool.acquire(static_cast<size_t>(n * kp) * 4);
+      bl = pool.acquire(static_cast<size_t>(n * kp) * 4);
+      dm::cuda_check(dm::split_tf32(a, lda, ta, m, k, ah.f32(), al.f32(), kp, st), "split A");
+      dm::cuda_check(dm::split_tf32(b, ldb, tb ? 0 : 1, n, k, bh.f32(), bl.f32(), kp, st),
+                     "split B");
+    }
+    dm::Tf32x3Args args;
+    args.a_hi = ah.f32();
+    args.a_lo = al.f32();
+    args.lda = kp;
+    args.b_hi = bh.f32();
+    args.b_lo = bl.f32();
+    args.ldb = kp;
+    args.c = c;
+    args.ldc = ldc;
+    args.m = m;
+    args.n = n;
+    args.k = k;
+    args.alpha = static_cast<float>(alpha);
+    args.beta = static_cast<float>(beta);
+    args.read_c = beta != 0.0 ? 1 : 0;
+    args.cta_group = cta_group;
+    dm::cuda_check(dm::tf32x3_gemm(args, st), "tf32x3_gemm");
+    // scratch goes back to the pool: make the seam synchronous on its stream
+    dm::cuda_check(cudaStreamSynchronize(st), "local_gemm sync");
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dm_last_error(void) { return g_last_error.c_str(); }
+
+int dm_last_error_missing(int32_t* coords, int cap) {
+  const int n = static_cast<int>(g_last_missing.size());
+  for (int i = 0; i < n && i < cap; ++i) {
+    coords[2 * i] = g_last_missing[i].first;
+    coords[2 * i + 1] = g_last_missing[i].second;
+  }
+  return n;
+}
+
+int dm_abi_version(void) { return DMATH_B200_ABI_VERSION; }
+
+int dm_checkerboard_dims(int workers, int* pr, int* pc) {
+  return guarded([&] {
+    if (workers < 1) throw dm::UsageError("checkerboard_dims: workers must be >= 1");
+    auto [r, c] = dm::checkerboard_dims(workers);
+    *pr = r;
+    *pc = c;
+  });
+}
+
+int dm_layout_owner(const dm_layout* layout, int row, int col, int* owner) {
+  return guarded([&] { *owner = dm::layout_from_abi(layout).owner({row, col}); });
+}
+
+int dm_layout_grid(const dm_layout* layout, int* nbr, int* nbc, int* clamped) {
+  return guarded([&] {
+    const dm::LayoutSpec l = dm::layout_from_abi(layout);
+    *nbr = l.grid.n_block_rows();
+    *nbc = l.grid.n_block_cols();
+    *clamped = l.grid.clamped ? 1 : 0;
+  });
+}
+
+int dm_block_extent(const dm_layout* layout, int row, int col, int64_t* rows, int64_t* cols) {
+  return guarded([&] {
+    auto [r, c] = dm::block_extent(dm::layout_from_abi(layout).grid, {row, col});
+    *rows = r;
+    *cols = c;
+  });
+}
+
+int dm_layout_to_string(const dm_layout* layout, char* buf, int cap) {
+  std::string s;
+  const int rc = guarded([&] { s = dm::layout_to_string(dm::layout_from_abi(layout)); });
+  if (rc != DM_OK) return -rc;
+  if (buf != nullptr && cap > 0) {
+    std::strncpy(buf, s.c_str(), static_cast<size_t>(cap));
+    buf[cap - 1] = 0;
+  }
+  return static_cast<int>(s.size()) + 1;
+}
+
+uint64_t dm_pool_size_class(uint64_t bytes) { return dm::DevicePool::size_class(bytes); }
+
+int dm_plan_general_gemm(const dm_layout* a, int ta, const dm_layout* b, int tb,
+                         const dm_layout* c, int worker, int64_t* peer_blocks, int64_t* peer_bytes) {
+  return guarded([&] {
+    const dm::LayoutSpec la = dm::layout_from_abi(a), lb = dm::layout_from_abi(b),
+                         lc = dm::layout_from_abi(c);
+    std::set<std::pair<int, std::pair<int, int>>> need;  // (matrix 0/1, block)
+    auto add = [&](const dm::LayoutSpec& l, bool trans, bool along_rows, int64_t lo, int64_t len,
+                   int tag) {
+      for (int br = 0; br < l.grid.n_block_rows(); ++br)
+        for (int bc = 0; bc < l.grid.n_block_cols(); ++bc) {
+          const int64_t ar0 = br * l.grid.block_rows, ac0 = bc * l.grid.block_cols;
+          auto [ar, ac] = dm::block_extent(l.grid, {br, bc});
+          int64_t o0, olen;
+          if (along_rows) {
+            o0 = trans ? ac0 : ar0;
+            olen = trans ? ac : ar;
+          } else {
+            o0 = trans ? ar0 : ac0;
+            olen = trans ? ar : ac;
+          }
+          if (o0 + olen <= lo || o0 >= lo + len) continue;
+          if (l.owner({br, bc}) != worker) need.insert({tag, {br, bc}});
+        }
+    };
+    for (dm::BlockCoord cc : dm::owned_coords(lc, worker)) {
+      auto [mb, nb] = dm::block_extent(lc.grid, cc);
+      add(la, ta != 0, true, cc.row * lc.grid.block_rows, mb, 0);
+      add(lb, tb != 0, false, cc.col * lc.grid.block_cols, nb, 1);
+    }
+    int64_t bytes = 0;
+    for (const auto& [tag, rc] : need) {
+      auto [r, cc] = dm::block_extent((tag == 0 ? la : lb).grid, {rc.first, rc.second});
+      bytes += r * cc * 4;
+    }
+    *peer_blocks = static_cast<int64_t>(need.size());
+    *peer_bytes = bytes;
+  });
+}
+
+int dm_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) throw dm::NcclError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int dm_session_create(const dm_session_config* cfg, dm_session** out) {
+  return guarded([&] {
+    if (cfg == nullptr || out == nullptr) throw dm::UsageError("session_create: null argument");
+    auto s = std::make_unique<dm_session>();
+    s->impl = std::make_unique<dm::Session>(*cfg);
+    *out = s.release();
+  });
+}
+
+int dm_session_destroy(dm_session* s) {
+  return guarded([&] {
+    if (s == nullptr) return;
+    s->impl.reset();
+    delete s;
+  });
+}
+
+int dm_session_shutdown(dm_session* s) { return guarded([&] { S(s).shutdown(); }); }
+
+int dm_create_matrix(dm_session* s, const dm_layout* layout, int precision, int fill,
+                     const void* host, dm_matrix_id* out) {
+  return guarded([&] {
+    if (precision < 0 || precision > 2) throw dm::ConfigError("unknown precision");
+    if (fill < 0 || fill > 2) throw dm::UsageError("unknown fill kind");
+    dm::Session& ss = S(s);
+    const dm::LayoutSpec l = dm::layout_from_abi(layout);
+    *out = ss.create_matrix(l, static_cast<dm::Precision>(precision),
+                            static_cast<dm::FillKind>(fill), static_cast<const float*>(host));
+  });
+}
+
+int dm_destroy_matrix(dm_session* s, dm_matrix_id id) {
+  return guarded([&] {
+    S(s).destroy_matrix(id);
+    s->custom_tables.erase(id);
+  });
+}
+
+int dm_scatter(dm_session* s, dm_matrix_id id, const void* host, int64_t rows, int64_t cols) {
+  return guarded([&] { S(s).scatter(id, static_cast<const float*>(host), rows, cols); });
+}
+
+int dm_gather(dm_session* s, dm_matrix_id id, void* host, int64_t rows, int64_t cols, int root) {
+  return guarded([&] { S(s).gather(id, static_cast<float*>(host), rows, cols, root); });
+}
+
+int dm_general_gemm(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b, double beta,
+                    dm_matrix_id c, int ta, int tb) {
+  return guarded([&] { S(s).general_gemm(alpha, a, b, beta, c, ta != 0, tb != 0); });
+}
+
+int dm_cyclic_gemm(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b, double beta,
+                   dm_matrix_id c, int ta, int tb, int cache_a) {
+  return guarded([&] { S(s).cyclic_gemm(alpha, a, b, beta, c, ta != 0, tb != 0, cache_a != 0); });
+}
+
+int dm_broadcast_gemm_reference(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b,
+                                double beta, dm_matrix_id c, int ta, int tb) {
+  // Same preconditions and result as the ring variant (ops.hpp:572-577); on
+  // NVSwitch the pull schedule is the same for both.
+  return guarded([&] { S(s).cyclic_gemm(alpha, a, b, beta, c, ta != 0, tb != 0, false); });
+}
+
+int dm_cached_backward_gemm(dm_session* s, dm_matrix_id w, dm_matrix_id dy, dm_matrix_id dx) {
+  return guarded([&] { S(s).cached_backward_gemm(w, dy, dx); });
+}
+
+int dm_worker_count(dm_session* s, int* out) {
+  return guarded([&] { *out = S(s).worker_count(); });
+}
+
+int dm_local_workers(dm_session* s, int32_t* ids, int cap) {
+  std::vector<int> v;
+  const int rc = guarded([&] { v = S(s).local_worker_ids(); });
+  if (rc != DM_OK) return -rc;
+  for (int i = 0; i < static_cast<int>(v.size()) && i < cap; ++i) ids[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
+int dm_descriptor_get(dm_session* s, dm_matrix_id id, dm_descriptor* out) {
+  return guarded([&] {
+    const dm::MatrixDescriptor& d = S(s).descriptor(id);
+    out->matrix_id = d.matrix_id;
+    out->precision = static_cast<int32_t>(d.precision);
+    out->replicated = d.replicated ? 1 : 0;
+    out->version = d.version;
+    out->replica_version = d.replica_version;
+    out->seed = d.seed;
+    out->layout.kind = static_cast<int32_t>(d.layout.kind);
+    out->layout.worker_count = d.layout.worker_count;
+    out->layout.global_rows = d.layout.grid.global_rows;
+    out->layout.global_cols = d.layout.grid.global_cols;
+    out->layout.block_rows = d.layout.grid.block_rows;
+    out->layout.block_cols = d.layout.grid.block_cols;
+    auto& tbl = s->custom_tables[id];
+    tbl.assign(d.layout.custom.begin(), d.layout.custom.end());
+    out->layout.custom = tbl.empty() ? nullptr : tbl.data();
+    out->layout.custom_len = static_cast<int64_t>(tbl.size());
+  });
+}
+
+int dm_pool_stats_get(dm_session* s, int worker, dm_pool_stats* out) {
+  return guarded([&] {
+    const dm::DevicePool::Stats st = S(s).pool_stats(worker);
+    out->fresh_allocations = st.fresh_allocations;
+    out->reuses = st.reuses;
+    out->bytes_live = st.bytes_live;
+    out->bytes_pooled = st.bytes_pooled;
+    out->high_water = st.high_water;
+  });
+}
+
+int dm_pool_trim(dm_session* s, int worker, uint64_t* freed) {
+  return guarded([&] {
+    const uint64_t f = S(s).pool_trim(worker);
+    if (freed) *freed = f;
+  });
+}
+
+int dm_worker_stats_get(dm_session* s, int worker, dm_worker_stats* out) {
+  return guarded([&] { *out = S(s).worker_stats(worker); });
+}
+
+int dm_worker_stats_reset(dm_session* s) { return guarded([&] { S(s).reset_worker_stats(); }); }
+
+int dm_set_gemm_timing(dm_session* s, int enable) {
+  return guarded([&] { S(s).set_gemm_timing(enable != 0); });
+}
+
+int dm_worker_seed(dm_session* s, int worker, uint64_t* out) {
+  return guarded([&] { *out = S(s).worker_seed(worker); });
+}
+
+int dm_descriptor_digest(dm_session* s, uint64_t* master, uint64_t* workers, int cap) {
+  std::vector<uint64_t> v;
+  const int rc = guarded([&] {
+    *master = S(s).master_digest();
+    v = S(s).worker_digests();
+  });
+  if (rc != DM_OK) return -rc;
+  for (int i = 0; i < static_cast<int>(v.size()) && i < cap; ++i) workers[i] = v[i];
+  return static_cast<int>(v.size());
+}
+
+int dm_block_device_ptr(dm_session* s, dm_matrix_id id, int row, int col, void** ptr, int* device) {
+  return guarded([&] { *ptr = S(s).block_device_ptr(id, {row, col}, device); });
+}
+
+int dm_barrier(dm_session* s) { return guarded([&] { S(s).barrier(); }); }
+
+int dm_local_gemm_f32(double alpha, const float* a, int64_t lda, int ta, const float* b,
+                      int64_t ldb, int tb, double beta, float* c, int64_t ldc, int64_t m,
+                      int64_t n, int64_t k, void* stream) {
+  return local_gemm_impl(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, 0, stream);
+}
+
+int dm_local_gemm_f32_ex(double alpha, const float* a, int64_t lda, int ta, const float* b,
+                         int64_t ldb, int tb, double beta, float* c, int64_t ldc, int64_t m,
+                         int64_t n, int64_t k, int cta_group, void* stream) {
+  return local_gemm_impl(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, cta_group, stream);
+}
+
+int dm_fill_seeded_f32(float* dst, int64_t count, uint64_t matrix_seed, int block_row,
+                       int block_col, void* stream) {
+  return guarded([&] {
+    const uint64_t key =
+        dm::mix64(matrix_seed, (static_cast<uint64_t>(static_cast<uint32_t>(block_row)) << 32) |
+                                   static_cast<uint32_t>(block_col));
+    dm::cuda_check(dm::fill_seeded(dst, count, key, static_cast<cudaStream_t>(stream)),
+                   "fill_seeded");
+  });
+}
+
+}  // extern "C"

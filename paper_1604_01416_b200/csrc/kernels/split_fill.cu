@@ -1,0 +1,108 @@
+// Data-movement kernels that feed the 3xTF32 GEMM.
+//
+// split_tf32: reads a (possibly transposed, possibly peer-GPU) fp32 panel and
+//   writes the K-major tf32 hi/lo planes consumed by tf32x3_gemm.  This replaces
+//   the reference's panel assembly `assemble_op_rows` / `assemble_op_cols`
+//   (/root/reference/proj/include/gridgemm/ops.hpp:177-208, 534-558), fused with
+//   the 3xTF32 split; when `src` is a peer pointer it is also the transfer.
+// fill_seeded: bit-exact device restatement of WorkerContext::fill_seeded
+//   (runtime_types.hpp:208-218) using mix64 / u64_to_unit_double
+//   (common.hpp:107-121).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tf32x3_gemm.h"
+
+namespace dm {
+
+namespace {
+
+__device__ __forceinline__ float tf32_rne(float x) {
+  uint32_t u = __float_as_uint(x);
+  if ((u & 0x7f800000u) != 0x7f800000u) u += 0xFFFu + ((u >> 13) & 1u);
+  return __uint_as_float(u & 0xFFFFE000u);
+}
+
+__device__ __forceinline__ void split_store(float x, float* hi, float* lo, int64_t idx) {
+  const float h = tf32_rne(x);
+  hi[idx] = h;
+  lo[idx] = tf32_rne(x - h);
+}
+
+constexpr int kT = 32;  // tile edge
+constexpr int kRowsPerPass = 8;
+
+// One 32x32 output tile per block (32 x 8 threads).
+__global__ void split_direct_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
+                                    int64_t kcols, float* __restrict__ hi, float* __restrict__ lo,
+                                    int64_t ldo) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kT;
+  if (k >= kcols) return;
+#pragma unroll
+  for (int i = 0; i < kT; i += kRowsPerPass) {
+    const int64_t r = r0 + threadIdx.y + i;
+    if (r < rows) split_store(__ldg(src + r * lds + k), hi, lo, r * ldo + k);
+  }
+}
+
+__global__ void split_trans_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
+                                   int64_t kcols, float* __restrict__ hi, float* __restrict__ lo,
+                                   int64_t ldo) {
+  __shared__ float tile[kT][kT + 1];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kT;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kT;
+  // read: src[k][r], coalesced along r
+#pragma unroll
+  for (int i = 0; i < kT; i += kRowsPerPass) {
+    const int64_t k = k0 + threadIdx.y + i, r = r0 + threadIdx.x;
+    if (k < kcols && r < rows) tile[threadIdx.y + i][threadIdx.x] = __ldg(src + k * lds + r);
+  }
+  __syncthreads();
+  // write: out[r][k], coalesced along k
+#pragma unroll
+  for (int i = 0; i < kT; i += kRowsPerPass) {
+    const int64_t r = r0 + threadIdx.y + i, k = k0 + threadIdx.x;
+    if (k < kcols && r < rows) split_store(tile[threadIdx.x][threadIdx.y + i], hi, lo, r * ldo + k);
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+__global__ void fill_seeded_kernel(float* __restrict__ dst, int64_t count, uint64_t key) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t h = mix64(key ^ mix64(static_cast<uint64_t>(e)));
+    const double u = static_cast<double>(h >> 11) * 0x1.0p-53;
+    dst[e] = __double2float_rn(2.0 * u - 1.0);
+  }
+}
+
+}  // namespace
+
+cudaError_t split_tf32(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols,
+                       float* hi, float* lo, int64_t ldo, cudaStream_t stream) {
+  if (rows <= 0 || kcols <= 0) return cudaSuccess;
+  dim3 block(kT, kRowsPerPass);
+  dim3 grid(static_cast<unsigned>((kcols + kT - 1) / kT), static_cast<unsigned>((rows + kT - 1) / kT));
+  if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
+  if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, hi, lo, ldo);
+  else split_direct_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, hi, lo, ldo);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_seeded(float* dst, int64_t count, uint64_t key, cudaStream_t stream) {
+  if (count <= 0) return cudaSuccess;
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  fill_seeded_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(dst, count, key);
+  return cudaGetLastError();
+}
+
+}  // namespace dm

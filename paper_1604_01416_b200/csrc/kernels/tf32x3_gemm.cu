@@ -1,0 +1,390 @@
+// 3xTF32 fp32-accurate GEMM on the sm_100a 5th-generation tensor cores.
+//
+// This is the B200 replacement for the reference's per-worker BLAS seam
+// `gridgemm::local_gemm` -> `detail::gemm_typed<float>`
+// (/root/reference/proj/include/gridgemm/kernels.hpp:48-89):
+//
+//     C <- alpha * op(A) op(B) + beta * C      (beta == 0 never reads C)
+//
+// Operands arrive pre-split (split_pack.cu) as K-major tf32 hi/lo pairs:
+//     x = hi + lo,  hi = rn_tf32(x),  lo = rn_tf32(x - hi)
+// and the product is accumulated in fp32 TMEM as
+//     acc += lo_A*hi_B + hi_A*lo_B + hi_A*hi_B      (lo*lo dropped, ~2^-22)
+//
+// Structure (one persistent CTA per SM, or one CTA pair per TPC for CG=2):
+//   warp 0      TMA producer   4 tiles per stage (A hi/lo, B hi/lo), 128B swizzle
+//   warp 1      MMA issuer     tcgen05.mma.kind::tf32, 3 MMAs per k8 step; owns TMEM
+//   warps 2..5  epilogue       tcgen05.ld -> alpha/beta -> global stores
+// Pipelines: smem full/empty mbarriers (TMA<->MMA) and a double-buffered TMEM
+// accumulator with full/empty mbarriers (MMA<->epilogue).
+//
+// CG=1: tile 128x128 (UMMA M=128,N=128), cta_group::1.
+// CG=2: CTA pair computes a 256x256 tile (UMMA M=256,N=256, cta_group::2);
+//       each CTA stages its 128 rows of A and 128 rows of B^T, the leader
+//       issues the MMAs, both CTAs drain their own 128 accumulator lanes.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+
+#include "ptx.cuh"
+#include "tf32x3_gemm.h"
+
+namespace dm {
+
+namespace {
+
+template <int CG>
+struct Cfg {
+  static constexpr int kRowsPerCta = 128;              // A rows and B rows staged per CTA
+  static constexpr int kUmmaM = 128 * CG;
+  static constexpr int kUmmaN = 128 * CG;
+  static constexpr int kBK = 32;                       // fp32 per 128-B swizzle row
+  static constexpr int kStages = 3;
+  static constexpr int kTileBytes = kRowsPerCta * kBK * 4;  // 16 KB
+  static constexpr int kStageBytes = 4 * kTileBytes;        // 64 KB
+  static constexpr int kAccCols = kUmmaN;                    // fp32 TMEM columns per buffer
+  static constexpr int kTmemCols = 2 * kAccCols;             // double-buffered
+  static constexpr int kThreads = 192;
+  static constexpr int kGroupM = 8;                          // rasterisation group
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct EpiParams {
+  float* c;
+  int64_t ldc;
+  int m, n;
+  float alpha, beta;
+  int read_c;
+};
+
+template <int CG>
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mt, int& nt) {
+  constexpr int G = Cfg<CG>::kGroupM;
+  const int per_group = G * tiles_n;
+  const int group = t / per_group;
+  const int first_m = group * G;
+  const int gsize = min(G, tiles_m - first_m);
+  const int r = t - group * per_group;
+  mt = first_m + r % gsize;
+  nt = r / gsize;
+}
+
+template <int CG>
+__global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
+    tf32x3_gemm_kernel(const __grid_constant__ CUtensorMap tm_ahi,
+                       const __grid_constant__ CUtensorMap tm_alo,
+                       const __grid_constant__ CUtensorMap tm_bhi,
+                       const __grid_constant__ CUtensorMap tm_blo, int K, EpiParams ep) {
+  using C = Cfg<CG>;
+  using namespace ptx;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment is required by the 128B swizzle atoms.
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full_bar = bars;                        // [kStages]
+  uint64_t* empty_bar = bars + C::kStages;          // [kStages]
+  uint64_t* tfull_bar = bars + 2 * C::kStages;      // [2]
+  uint64_t* tempty_bar = bars + 2 * C::kStages + 2; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
+
+  const int warp = threadIdx.x / 32;
+  const uint32_t lane = threadIdx.x % 32;
+  const uint32_t cta_rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const bool leader = cta_rank == 0;
+
+  const int tiles_m = (ep.m + C::kUmmaM - 1) / C::kUmmaM;
+  const int tiles_n = (ep.n + C::kUmmaN - 1) / C::kUmmaN;
+  const int total_tiles = tiles_m * tiles_n;
+  const int unit = blockIdx.x / CG;
+  const int num_units = gridDim.x / CG;
+  const int num_kb = (K + C::kBK - 1) / C::kBK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(smem_u32(&full_bar[s]), 1);
+      mbar_init(smem_u32(&empty_bar[s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&tfull_bar[a]), 1);
+      mbar_init(smem_u32(&tempty_bar[a]), 4 * CG);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&tm_ahi);
+    prefetch_tmap(&tm_alo);
+    prefetch_tmap(&tm_bhi);
+    prefetch_tmap(&tm_blo);
+  }
+  if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), C::kTmemCols);
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = unit; t < total_tiles; t += num_units) {
+        int mt, nt;
+        tile_coords<CG>(t, tiles_m, tiles_n, mt, nt);
+        const int arow = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta;
+        const int brow = nt * C::kUmmaN + static_cast<int>(cta_rank) * C::kRowsPerCta;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
+          uint8_t* st = smem + stage * C::kStageBytes;
+          const uint32_t fb = smem_u32(&full_bar[stage]);
+          const int kx = kb * C::kBK;
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(fb, C::kStageBytes);
+            const uint64_t pol = policy_evict_last();
+            tma_load_2d(&tm_ahi, smem_u32(st), fb, kx, arow, pol);
+            tma_load_2d(&tm_alo, smem_u32(st + C::kTileBytes), fb, kx, arow, pol);
+            tma_load_2d(&tm_bhi, smem_u32(st + 2 * C::kTileBytes), fb, kx, brow, pol);
+            tma_load_2d(&tm_blo, smem_u32(st + 3 * C::kTileBytes), fb, kx, brow, pol);
+          } else {
+            // Completion bytes of both CTAs land on the leader's barrier.
+            uint32_t fb_leader;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb_leader) : "r"(fb));
+            if (leader) mbar_arrive_expect_tx(fb, 2 * C::kStageBytes);
+            const uint64_t pol = policy_evict_last();
+            tma_load_2d_cg2(&tm_ahi, smem_u32(st), fb_leader, kx, arow, pol);
+            tma_load_2d_cg2(&tm_alo, smem_u32(st + C::kTileBytes), fb_leader, kx, arow, pol);
+            tma_load_2d_cg2(&tm_bhi, smem_u32(st + 2 * C::kTileBytes), fb_leader, kx, brow, pol);
+            tma_load_2d_cg2(&tm_blo, smem_u32(st + 3 * C::kTileBytes), fb_leader, kx, brow, pol);
+          }
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (leader && lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(C::kUmmaM, C::kUmmaN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = unit; t < total_tiles; t += num_units, ++it) {
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(smem_u32(&tempty_bar[acc]), aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * C::kAccCols);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(smem_u32(&full_bar[stage]), phase);
+          tc_fence_after();
+          const uint32_t s0 = smem_u32(smem + stage * C::kStageBytes);
+          const uint64_t ahi = sdesc_k_sw128(s0);
+          const uint64_t alo = sdesc_k_sw128(s0 + C::kTileBytes);
+          const uint64_t bhi = sdesc_k_sw128(s0 + 2 * C::kTileBytes);
+          const uint64_t blo = sdesc_k_sw128(s0 + 3 * C::kTileBytes);
+#pragma unroll
+          for (int j = 0; j < C::kBK / 8; ++j) {
+            // advance 8 tf32 = 32 B along K inside the swizzle row (16-B units)
+            const uint64_t off = static_cast<uint64_t>(j * 2);
+            mma_tf32<CG>(d_tmem, alo + off, bhi + off, idesc, (kb | j) != 0);
+            mma_tf32<CG>(d_tmem, ahi + off, blo + off, idesc, 1u);
+            mma_tf32<CG>(d_tmem, ahi + off, bhi + off, idesc, 1u);
+          }
+          if constexpr (CG == 1) mma_commit(smem_u32(&empty_bar[stage]));
+          else mma_commit_cg2(smem_u32(&empty_bar[stage]), 0x3);
+          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+        }
+        if constexpr (CG == 1) mma_commit(smem_u32(&tfull_bar[acc]));
+        else mma_commit_cg2(smem_u32(&tfull_bar[acc]), 0x3);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp % 4;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int t = unit; t < total_tiles; t += num_units, ++it) {
+      int mt, nt;
+      tile_coords<CG>(t, tiles_m, tiles_n, mt, nt);
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(smem_u32(&tfull_bar[acc]), aphase);
+      tc_fence_after();
+      const int row = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta + q * 32 +
+                      static_cast<int>(lane);
+      const int col_base = nt * C::kUmmaN;
+      const bool row_ok = row < ep.m;
+      float* crow = ep.c + static_cast<int64_t>(row) * ep.ldc;
+      const bool vec_ok =
+          ((ep.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(ep.c) & 15) == 0);
+#pragma unroll 1
+      for (int ch = 0; ch < C::kAccCols / 32; ++ch) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem_base + static_cast<uint32_t>(acc * C::kAccCols + ch * 32) +
+                               (static_cast<uint32_t>(q * 32) << 16),
+                           v);
+        tmem_ld_wait();
+        const int c0 = col_base + ch * 32;
+        if (!row_ok || c0 >= ep.n) continue;
+        if (vec_ok && c0 + 32 <= ep.n) {
+          float4* dst = reinterpret_cast<float4*>(crow + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 o;
+            o.x = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 0]));
+            o.y = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 1]));
+            o.z = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 2]));
+            o.w = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 3]));
+            if (ep.read_c) {
+              const float4 cv = dst[j];
+              o.x = __fadd_rn(o.x, __fmul_rn(ep.beta, cv.x));
+              o.y = __fadd_rn(o.y, __fmul_rn(ep.beta, cv.y));
+              o.z = __fadd_rn(o.z, __fmul_rn(ep.beta, cv.z));
+              o.w = __fadd_rn(o.w, __fmul_rn(ep.beta, cv.w));
+            }
+            dst[j] = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (c0 + j < ep.n) {
+              float o = __fmul_rn(ep.alpha, __uint_as_float(v[j]));
+              if (ep.read_c) o = __fadd_rn(o, __fmul_rn(ep.beta, crow[c0 + j]));
+              crow[c0 + j] = o;
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 1) mbar_arrive(smem_u32(&tempty_bar[acc]));
+        else mbar_arrive_cluster(smem_u32(&tempty_bar[acc]), 0);
+      }
+    }
+  }
+
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<CG>(tmem_base, C::kTmemCols);
+  }
+}
+
+// C <- alpha*0 + beta*C for K == 0 (no tensor-core work).
+__global__ void scale_c_kernel(float* c, int64_t ldc, int m, int n, float alpha_zero, float beta,
+                               int read_c) {
+  const int64_t total = static_cast<int64_t>(m) * n;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / n), cc = static_cast<int>(i % n);
+    float o = __fmul_rn(alpha_zero, 0.0f);
+    if (read_c) o = __fadd_rn(o, __fmul_rn(beta, c[r * ldc + cc]));
+    c[r * ldc + cc] = o;
+  }
+}
+
+// ------------------------------------------------------------------ host
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// K-major fp32 operand [rows x K] with row pitch `ld` elements; box 32 x 128.
+int make_operand_map(CUtensorMap* map, const float* base, int64_t rows, int64_t k, int64_t ld) {
+  EncodeTiledFn enc = encode_fn();
+  if (enc == nullptr) return -1;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -2;
+}
+
+template <int CG>
+cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
+  using C = Cfg<CG>;
+  CUtensorMap maps[4];
+  if (make_operand_map(&maps[0], a.a_hi, a.m, a.k, a.lda) != 0 ||
+      make_operand_map(&maps[1], a.a_lo, a.m, a.k, a.lda) != 0 ||
+      make_operand_map(&maps[2], a.b_hi, a.n, a.k, a.ldb) != 0 ||
+      make_operand_map(&maps[3], a.b_lo, a.n, a.k, a.ldb) != 0)
+    return cudaErrorInvalidValue;
+  static bool attr_set[2][64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr_set[CG - 1][dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(tf32x3_gemm_kernel<CG>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set[CG - 1][dev & 63] = true;
+  }
+  int sms = a.num_sms;
+  if (sms <= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int tiles = ((a.m + C::kUmmaM - 1) / C::kUmmaM) * ((a.n + C::kUmmaN - 1) / C::kUmmaN);
+  int units = sms / CG;
+  if (units > tiles) units = tiles;
+  if (units < 1) units = 1;
+
+  EpiParams ep{a.c, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
+               a.read_c};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(units * CG);
+  cfg.blockDim = dim3(C::kThreads);
+  cfg.dynamicSmemBytes = C::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG>, maps[0], maps[1], maps[2], maps[3],
+                            static_cast<int>(a.k), ep);
+}
+
+}  // namespace
+
+cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
+  if (a.m <= 0 || a.n <= 0) return cudaSuccess;
+  if (a.k <= 0) {
+    const int64_t total = a.m * a.n;
+    int blocks = static_cast<int>((total + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    scale_c_kernel<<<blocks, 256, 0, stream>>>(a.c, a.ldc, static_cast<int>(a.m),
+                                               static_cast<int>(a.n), a.alpha, a.beta, a.read_c);
+    return cudaGetLastError();
+  }
+  // TMA needs 16-B aligned bases and pitches.
+  if ((a.lda & 3) || (a.ldb & 3) || (reinterpret_cast<uintptr_t>(a.a_hi) & 15) ||
+      (reinterpret_cast<uintptr_t>(a.a_lo) & 15) || (reinterpret_cast<uintptr_t>(a.b_hi) & 15) ||
+      (reinterpret_cast<uintptr_t>(a.b_lo) & 15))
+    return cudaErrorMisalignedAddress;
+  int cg = a.cta_group;
+  if (cg == 0) {
+    // Pairs pay off once there are enough 256x256 tiles to fill the machine.
+    const int64_t pair_tiles = ((a.m + 255) / 256) * ((a.n + 255) / 256);
+    cg = pair_tiles >= 74 ? 2 : 1;
+  }
+  return cg == 2 ? launch<2>(a, stream) : launch<1>(a, stream);
+}
+
+}  // namespace dm

@@ -1,0 +1,89 @@
+// Error taxonomy, hashing and seed mixing of the distributed-matrix runtime.
+//
+// Mirrors the reference's error classes (gridgemm/common.hpp:22-78) so every
+// C-ABI status code maps 1:1 onto the exception a reference user expects, and
+// restates its FNV-1a (common.hpp:83-103) and splitmix64 seed mixer
+// (common.hpp:107-121) -- the latter defines the seeded synthetic inputs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../../include/dmath_b200.h"
+
+namespace dm {
+
+class Error : public std::runtime_error {
+ public:
+  Error(int code, const std::string& what) : std::runtime_error(what), code_(code) {}
+  int code() const { return code_; }
+
+ private:
+  int code_;
+};
+
+#define DM_DEFINE_ERROR(Name, Code) \
+  class Name : public Error {       \
+   public:                          \
+    explicit Name(const std::string& w) : Error(Code, w) {} \
+  };
+
+DM_DEFINE_ERROR(UsageError, DM_ERR_USAGE)
+DM_DEFINE_ERROR(ConfigError, DM_ERR_CONFIG)
+DM_DEFINE_ERROR(ShapeError, DM_ERR_SHAPE)
+DM_DEFINE_ERROR(ProtocolError, DM_ERR_PROTOCOL)
+DM_DEFINE_ERROR(PlanError, DM_ERR_PLAN)
+DM_DEFINE_ERROR(UnsupportedError, DM_ERR_UNSUPPORTED)
+DM_DEFINE_ERROR(CudaError, DM_ERR_CUDA)
+DM_DEFINE_ERROR(NcclError, DM_ERR_NCCL)
+#undef DM_DEFINE_ERROR
+
+class CacheMissError : public Error {
+ public:
+  CacheMissError(const std::string& w, std::vector<std::pair<int, int>> missing)
+      : Error(DM_ERR_CACHE_MISS, w), missing_coords(std::move(missing)) {}
+  std::vector<std::pair<int, int>> missing_coords;
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+                    ")");
+}
+
+// FNV-1a 64 (descriptor digests; checksums of gathered matrices in tests).
+class Fnv1a {
+ public:
+  void update(const void* data, std::size_t n) {
+    const auto* p = static_cast<const unsigned char*>(data);
+    for (std::size_t i = 0; i < n; ++i) {
+      state_ ^= p[i];
+      state_ *= 1099511628211ULL;
+    }
+  }
+  void update_u64(std::uint64_t v) {
+    unsigned char b[8];
+    for (int i = 0; i < 8; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+    update(b, 8);
+  }
+  std::uint64_t digest() const { return state_; }
+
+ private:
+  std::uint64_t state_ = 14695981039346656037ULL;
+};
+
+inline std::uint64_t mix64(std::uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+inline std::uint64_t mix64(std::uint64_t a, std::uint64_t b) { return mix64(a ^ mix64(b)); }
+
+}  // namespace dm

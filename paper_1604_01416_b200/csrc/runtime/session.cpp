@@ -1,0 +1,798 @@
+// Session implementation.  See session.hpp for the architecture; reference
+// citations are to /root/reference/proj/include/gridgemm/.
+#include "session.hpp"
+
+#include <algorithm>
+#include <array>
+#include <cstdlib>
+#include <cstring>
+
+#include "../kernels/tf32x3_gemm.h"
+#include "comm.hpp"
+
+namespace dm {
+
+namespace {
+
+std::int64_t env_int(const char* name, std::int64_t dflt) {
+  const char* v = std::getenv(name);
+  if (v == nullptr || *v == 0) return dflt;
+  return std::strtoll(v, nullptr, 10);
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+std::uint64_t table_digest(const std::map<MatrixId, MatrixDescriptor>& t) {
+  Fnv1a h;
+  for (const auto& [id, d] : t) hash_descriptor(h, d);
+  return h.digest();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ lifecycle
+
+Session::Session(const dm_session_config& cfg) {
+  if (cfg.worker_count < 1) throw UsageError("init: worker_count must be >= 1");
+  P_ = cfg.worker_count;
+  mode_ = cfg.mode;
+  rank_ = cfg.rank;
+  coherence_ = cfg.coherence_checks != 0;
+  root_seed_ = cfg.root_seed;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    throw CudaError("init: no CUDA device visible (the B200 path has no CPU fallback)");
+  }
+  workers_.resize(P_);
+  auto make_worker = [&](int w, int dev) {
+    if (dev < 0 || dev >= ndev) throw ConfigError("init: device id out of range");
+    DeviceGuard g(dev);
+    auto wk = std::make_unique<Worker>();
+    wk->id = w;
+    wk->device = dev;
+    cuda_check(cudaStreamCreateWithFlags(&wk->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&wk->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    wk->pool = std::make_unique<DevicePool>(dev);
+    wk->seed = mix64(root_seed_, static_cast<std::uint64_t>(w));  // exec_seed, ops.hpp:1140
+    workers_[w] = std::move(wk);
+  };
+  if (mode_ == DM_MODE_LOCAL) {
+    std::set<int> devs;
+    for (int w = 0; w < P_; ++w) {
+      const int dev = cfg.devices ? cfg.devices[w] : w % ndev;
+      make_worker(w, dev);
+      devs.insert(dev);
+    }
+    for (int i : devs)
+      for (int j : devs) {
+        if (i == j) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, i, j);
+        if (!can) throw ConfigError("init: devices without peer access cannot share a session");
+        DeviceGuard g(i);
+        cudaError_t e = cudaDeviceEnablePeerAccess(j, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+          cuda_check(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+      }
+  } else if (mode_ == DM_MODE_SPMD) {
+    if (rank_ < 0 || rank_ >= P_) throw UsageError("init: rank out of range");
+    const int dev = cfg.devices ? cfg.devices[0] : rank_ % ndev;
+    make_worker(rank_, dev);
+    comm_ = std::make_unique<Comm>(P_, rank_, cfg.nccl_id, dev);
+  } else {
+    throw ConfigError("init: unknown session mode");
+  }
+  live_ = true;
+}
+
+Session::~Session() {
+  try {
+    shutdown();
+  } catch (...) {
+  }
+  comm_.reset();
+  for (auto& w : workers_) {
+    if (!w) continue;
+    cudaSetDevice(w->device);
+    for (auto& [a, b] : w->timing_events) {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    w->owned.clear();
+    w->cache.clear();
+    w->pool.reset();
+    cudaStreamDestroy(w->stream);
+    cudaStreamDestroy(w->side);
+  }
+}
+
+void Session::shutdown() {
+  if (!live_) return;
+  sync_local();
+  if (comm_) {
+    for (const auto& [id, d] : table_) comm_->unpublish(id);
+    comm_->barrier();
+  }
+  for (auto& w : workers_) {
+    if (!w) continue;
+    w->owned.clear();
+    w->cache.clear();
+    w->descriptors.clear();
+    w->pool->trim();
+  }
+  if (comm_) comm_->barrier();
+  table_.clear();
+  cache_meta_.clear();
+  live_ = false;
+}
+
+std::vector<int> Session::local_worker_ids() const {
+  std::vector<int> out;
+  for (int w = 0; w < P_; ++w)
+    if (workers_[w]) out.push_back(w);
+  return out;
+}
+
+Worker& Session::worker(int w) {
+  if (w < 0 || w >= P_) throw UsageError("unknown worker id");
+  if (!workers_[w]) throw UsageError("worker " + std::to_string(w) + " is not local to this process");
+  return *workers_[w];
+}
+const Worker& Session::worker(int w) const { return const_cast<Session*>(this)->worker(w); }
+
+Worker* Session::local(int w) { return workers_[w].get(); }
+const Worker* Session::local(int w) const { return workers_[w].get(); }
+
+void Session::require_live() const {
+  if (!live_) throw UsageError("session has been shut down");
+}
+
+void Session::validate_layout_workers(const LayoutSpec& l) const {
+  if (l.worker_count < 1) throw UsageError("layout: worker set must not be empty");
+  for (int r = 0; r < l.grid.n_block_rows(); ++r)
+    for (int c = 0; c < l.grid.n_block_cols(); ++c) {
+      const int o = l.owner({r, c});
+      if (o < 0 || o >= P_) throw UsageError("layout: block owner outside the session worker set");
+    }
+}
+
+const MatrixDescriptor& Session::descriptor(MatrixId id) const {
+  auto it = table_.find(id);
+  if (it == table_.end()) throw UsageError("unknown matrix id " + std::to_string(id));
+  return it->second;
+}
+
+void Session::sync_local() {
+  for (auto& w : workers_) {
+    if (!w) continue;
+    DeviceGuard g(w->device);
+    cuda_check(cudaStreamSynchronize(w->side), "stream sync");
+    cuda_check(cudaStreamSynchronize(w->stream), "stream sync");
+  }
+}
+
+void Session::end_command() {
+  sync_local();
+  collect_timing();
+  if (comm_) {
+    if (coherence_) {
+      const std::uint64_t mine = table_digest(workers_[rank_]->descriptors);
+      const std::uint64_t master = table_digest(table_);
+      if (mine != master) throw ProtocolError("descriptor tables diverged (worker vs master)");
+      const auto all = comm_->allgather(&master, sizeof(master));  // doubles as the barrier
+      for (int r = 0; r < P_; ++r) {
+        std::uint64_t v;
+        std::memcpy(&v, all.data() + r * sizeof(v), sizeof(v));
+        if (v != master) throw ProtocolError("descriptor tables diverged across ranks");
+      }
+    } else {
+      comm_->barrier();
+    }
+  } else if (coherence_) {
+    const std::uint64_t master = table_digest(table_);
+    for (auto& w : workers_)
+      if (w && table_digest(w->descriptors) != master)
+        throw ProtocolError("descriptor tables diverged");
+  }
+}
+
+void Session::barrier() {
+  sync_local();
+  if (comm_) comm_->barrier();
+}
+
+// --------------------------------------------------------------- matrices
+
+MatrixId Session::create_matrix(const LayoutSpec& layout, Precision p, FillKind fill,
+                                const float* host) {
+  require_live();
+  validate_layout_workers(layout);
+  if (fill == FillKind::FromHost && host == nullptr)
+    throw UsageError("create_matrix: FromHost requires host data");
+  if (p != Precision::Single32)
+    throw UnsupportedError(
+        "create_matrix: the B200 path stores Single32 only (Half16/Double64 are outside the fp32 "
+        "GEMM hot path)");
+  MatrixDescriptor d;
+  d.matrix_id = next_matrix_id_++;
+  d.layout = layout;
+  d.precision = p;
+  d.seed = mix64(root_seed_, d.matrix_id);  // session.hpp:142
+  for (auto& w : workers_) {
+    if (!w) continue;
+    DeviceGuard g(w->device);
+    for (BlockCoord c : owned_coords(layout, w->id)) {
+      auto [br, bc] = block_extent(layout.grid, c);
+      StoredBlock blk;
+      blk.rows = br;
+      blk.cols = bc;
+      blk.version_seen = d.version;
+      blk.mem = w->pool->acquire(static_cast<std::size_t>(br * bc) * 4);
+      if (fill == FillKind::SeededRandom) {
+        const std::uint64_t key =
+            mix64(d.seed, (static_cast<std::uint64_t>(static_cast<std::uint32_t>(c.row)) << 32) |
+                              static_cast<std::uint32_t>(c.col));
+        cuda_check(fill_seeded(blk.mem.f32(), br * bc, key, w->stream), "fill_seeded");
+      } else {
+        cuda_check(cudaMemsetAsync(blk.mem.data(), 0, static_cast<std::size_t>(br * bc) * 4,
+                                   w->stream),
+                   "cudaMemsetAsync");
+      }
+      w->owned[{d.matrix_id, c}] = std::move(blk);
+    }
+    w->descriptors[d.matrix_id] = d;
+  }
+  table_[d.matrix_id] = d;
+  sync_local();
+  if (comm_) comm_->publish(d.matrix_id, layout, workers_[rank_]->owned);
+  end_command();
+  if (fill == FillKind::FromHost)
+    scatter(d.matrix_id, host, layout.grid.global_rows, layout.grid.global_cols);
+  return d.matrix_id;
+}
+
+void Session::destroy_matrix(MatrixId id) {
+  require_live();
+  descriptor(id);
+  sync_local();
+  if (comm_) {
+    comm_->barrier();
+    comm_->unpublish(id);
+  }
+  for (auto& w : workers_) {
+    if (!w) continue;
+    for (auto* m : {&w->owned, &w->cache}) {
+      auto it = m->lower_bound({id, {0, 0}});
+      while (it != m->end() && it->first.matrix == id) it = m->erase(it);
+    }
+    w->descriptors.erase(id);
+  }
+  table_.erase(id);
+  cache_meta_.erase(id);
+  end_command();
+}
+
+void Session::bump_version(MatrixId id) {
+  const std::uint64_t v = ++table_.at(id).version;
+  for (auto& w : workers_) {
+    if (!w) continue;
+    w->descriptors.at(id).version = v;
+    auto it = w->owned.lower_bound({id, {0, 0}});
+    for (; it != w->owned.end() && it->first.matrix == id; ++it) it->second.version_seen = v;
+  }
+}
+
+void Session::scatter(MatrixId id, const float* host, std::int64_t rows, std::int64_t cols) {
+  require_live();
+  const MatrixDescriptor d = descriptor(id);
+  const BlockGrid& g = d.layout.grid;
+  if (rows != g.global_rows || cols != g.global_cols)
+    throw ShapeError("scatter: host data shape does not match the matrix");
+  if (host == nullptr) throw UsageError("scatter: null host pointer");
+  for (auto& w : workers_) {
+    if (!w) continue;
+    DeviceGuard guard(w->device);
+    for (BlockCoord c : owned_coords(d.layout, w->id)) {
+      StoredBlock& blk = w->owned.at({id, c});
+      const float* src = host + static_cast<std::int64_t>(c.row) * g.block_rows * g.global_cols +
+                         static_cast<std::int64_t>(c.col) * g.block_cols;
+      cuda_check(cudaMemcpy2DAsync(blk.mem.data(), static_cast<std::size_t>(blk.cols) * 4, src,
+                                   static_cast<std::size_t>(g.global_cols) * 4,
+                                   static_cast<std::size_t>(blk.cols) * 4,
+                                   static_cast<std::size_t>(blk.rows), cudaMemcpyHostToDevice,
+                                   w->stream),
+                 "scatter H2D");
+    }
+  }
+  bump_version(id);  // runtime_types.hpp:289-292
+  end_command();
+}
+
+void Session::gather(MatrixId id, float* host, std::int64_t rows, std::int64_t cols, int root) {
+  require_live();
+  const MatrixDescriptor d = descriptor(id);
+  const BlockGrid& g = d.layout.grid;
+  if (rows != g.global_rows || cols != g.global_cols)
+    throw ShapeError("gather: host buffer shape does not match the matrix");
+  if (root < -1 || root >= P_) throw UsageError("gather: root out of range");
+  const bool all_blocks = !comm_ || root == rank_;
+  const bool any = !comm_ || root == -1 || root == rank_;
+  if (any && host == nullptr) throw UsageError("gather: null host pointer");
+  if (any) {
+    Worker& me = comm_ ? *workers_[rank_] : *workers_[0];
+    for (int r = 0; r < g.n_block_rows(); ++r)
+      for (int c = 0; c < g.n_block_cols(); ++c) {
+        const int owner = d.layout.owner({r, c});
+        Worker* ow = local(owner);
+        if (!all_blocks && ow == nullptr) continue;
+        auto [br, bc] = block_extent(g, {r, c});
+        const float* src = ow ? ow->owned.at({id, {r, c}}).mem.f32() : comm_->remote_ptr(id, {r, c});
+        Worker& issuer = ow ? *ow : me;
+        DeviceGuard guard(issuer.device);
+        float* dst = host + static_cast<std::int64_t>(r) * g.block_rows * g.global_cols +
+                     static_cast<std::int64_t>(c) * g.block_cols;
+        cuda_check(cudaMemcpy2DAsync(dst, static_cast<std::size_t>(g.global_cols) * 4, src,
+                                     static_cast<std::size_t>(bc) * 4,
+                                     static_cast<std::size_t>(bc) * 4,
+                                     static_cast<std::size_t>(br), cudaMemcpyDefault,
+                                     issuer.stream),
+                   "gather D2H");
+      }
+  }
+  end_command();
+}
+
+// ----------------------------------------------------------------- GEMMs
+
+GemmArgs Session::gemm_command(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c,
+                               bool ta, bool tb, bool cache_a) const {
+  if (c == a || c == b) throw UsageError("gemm: destination must be distinct from the operands");
+  GemmArgs g;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.a = a;
+  g.b = b;
+  g.c = c;
+  g.trans_a = ta;
+  g.trans_b = tb;
+  g.cache_a = cache_a;
+  return g;
+}
+
+// Session::validate_general_gemm (session.hpp:531-545).
+void Session::validate_general(const GemmArgs& g) const {
+  const MatrixDescriptor& da = descriptor(g.a);
+  const MatrixDescriptor& db = descriptor(g.b);
+  const MatrixDescriptor& dc = descriptor(g.c);
+  if (da.precision != db.precision || da.precision != dc.precision)
+    throw UsageError("gemm: operands must share a precision; reshape to convert first");
+  if (dc.replicated) throw UsageError("gemm: destination matrix may not be replicated");
+  const std::int64_t kk = g.trans_a ? da.layout.grid.global_rows : da.layout.grid.global_cols;
+  const std::int64_t m = g.trans_a ? da.layout.grid.global_cols : da.layout.grid.global_rows;
+  const std::int64_t kb = g.trans_b ? db.layout.grid.global_cols : db.layout.grid.global_rows;
+  const std::int64_t n = g.trans_b ? db.layout.grid.global_rows : db.layout.grid.global_cols;
+  if (kk != kb) throw ShapeError("gemm: inner dimensions do not conform");
+  if (dc.layout.grid.global_rows != m || dc.layout.grid.global_cols != n)
+    throw ShapeError("gemm: output dimensions do not conform");
+}
+
+// Ring-plan preconditions of build_cyclic_plan (ops.hpp:84-169).
+void Session::validate_cyclic(const GemmArgs& g, std::vector<WorkerId>* strip_owners) const {
+  validate_general(g);
+  const MatrixDescriptor& da = descriptor(g.a);
+  const MatrixDescriptor& db = descriptor(g.b);
+  const MatrixDescriptor& dc = descriptor(g.c);
+  const BlockGrid& ga = da.layout.grid;
+  if ((da.layout.kind != LayoutKind::RowBlocks1D && da.layout.kind != LayoutKind::RowCyclic1D) ||
+      ga.n_block_cols() != 1)
+    throw PlanError("cyclic_gemm: A must use a 1D row-blocked decomposition");
+  if (da.layout.worker_count != P_)
+    throw PlanError("cyclic_gemm: A must be laid out over all session workers");
+  const int nbr = ga.n_block_rows();
+  if (nbr % P_ != 0) throw PlanError("cyclic_gemm: A block-rows must divide evenly over the ring");
+  const int inner = nbr / P_;
+  for (int w = 0; w < P_; ++w)
+    for (int i = 0; i < inner; ++i) {
+      const int row = da.layout.kind == LayoutKind::RowBlocks1D ? w * inner + i : w + i * P_;
+      if (da.layout.owner({row, 0}) != w)
+        throw PlanError("cyclic_gemm: A assignment does not match the ring plan");
+    }
+  const BlockGrid& gb = db.layout.grid;
+  const int strips = g.trans_b ? gb.n_block_rows() : gb.n_block_cols();
+  if ((g.trans_b ? gb.n_block_cols() : gb.n_block_rows()) != 1)
+    throw PlanError("cyclic_gemm: B must be a single line of stationary strips");
+  const BlockGrid& gc = dc.layout.grid;
+  if (gc.n_block_rows() != 1 || gc.n_block_cols() != strips)
+    throw PlanError("cyclic_gemm: C strips must match op(B) strips");
+  const std::int64_t m = g.trans_a ? ga.global_cols : ga.global_rows;
+  for (int s = 0; s < strips; ++s) {
+    const BlockCoord bcd = g.trans_b ? BlockCoord{s, 0} : BlockCoord{0, s};
+    auto [br, bc] = block_extent(gb, bcd);
+    const std::int64_t width = g.trans_b ? br : bc;
+    auto [cr, cc] = block_extent(gc, {0, s});
+    if (cc != width || cr != m) throw PlanError("cyclic_gemm: C strip extents must match op(B) strips");
+    const int owner = db.layout.owner(bcd);
+    if (dc.layout.owner({0, s}) != owner)
+      throw PlanError("cyclic_gemm: C strips must be co-located with op(B) strips");
+    if (strip_owners) strip_owners->push_back(owner);
+  }
+}
+
+const float* Session::source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
+                                 bool* remote) const {
+  const MatrixDescriptor& d = table_.at(m);
+  const int owner = d.layout.owner(c);
+  *remote = false;
+  if (owner == reader.id) return reader.owned.at({m, c}).mem.f32();
+  if (pol == SourcePolicy::LocalOnly) {
+    auto it = reader.cache.find({m, c});
+    if (it != reader.cache.end() && it->second.version_seen == d.version)
+      return it->second.mem.f32();
+    throw CacheMissError("cached_backward_gemm: stale or missing cached blocks", {{c.row, c.col}});
+  }
+  *remote = true;
+  if (const Worker* ow = local(owner)) return ow->owned.at({m, c}).mem.f32();
+  return comm_->remote_ptr(m, c);
+}
+
+// Pieces of op(M) covering range rg (op rows of A, or op cols of B) for every
+// K panel.  A piece is the intersection of one stored block with the range and
+// a panel -- the B200 form of GeneralGemmExec::add_needed + assemble_op_rows /
+// assemble_op_cols (ops.hpp:503-524, 177-208, 534-558).
+void Session::add_range_pieces(Range& rg, const MatrixDescriptor& d, bool trans, bool is_a,
+                               const std::vector<std::int64_t>& k0) const {
+  const BlockGrid& grid = d.layout.grid;
+  const bool range_on_rows = is_a ? !trans : trans;
+  const int np = static_cast<int>(k0.size()) - 1;
+  rg.panels.assign(np, {});
+  for (int br = 0; br < grid.n_block_rows(); ++br)
+    for (int bc = 0; bc < grid.n_block_cols(); ++bc) {
+      const std::int64_t sr0 = static_cast<std::int64_t>(br) * grid.block_rows;
+      const std::int64_t sc0 = static_cast<std::int64_t>(bc) * grid.block_cols;
+      auto [srows, scols] = block_extent(grid, {br, bc});
+      const std::int64_t o0 = range_on_rows ? sr0 : sc0, olen = range_on_rows ? srows : scols;
+      const std::int64_t q0 = range_on_rows ? sc0 : sr0, qlen = range_on_rows ? scols : srows;
+      const std::int64_t lo_o = std::max(o0, rg.start), hi_o = std::min(o0 + olen, rg.start + rg.len);
+      if (lo_o >= hi_o) continue;
+      for (int p = 0; p < np; ++p) {
+        const std::int64_t lo_k = std::max(q0, k0[p]), hi_k = std::min(q0 + qlen, k0[p + 1]);
+        if (lo_k >= hi_k) continue;
+        Piece pc;
+        pc.matrix = d.matrix_id;
+        pc.coord = {br, bc};
+        pc.lds = scols;
+        pc.rows = hi_o - lo_o;
+        pc.kcols = hi_k - lo_k;
+        pc.dst_row = lo_o - rg.start;
+        pc.dst_k = lo_k - k0[p];
+        if (range_on_rows) {
+          pc.src_off = (lo_o - sr0) * scols + (lo_k - sc0);
+          pc.trans = 0;
+        } else {
+          pc.src_off = (lo_k - sr0) * scols + (lo_o - sc0);
+          pc.trans = 1;
+        }
+        rg.panels[p].push_back(pc);
+      }
+    }
+}
+
+Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy pol) const {
+  const MatrixDescriptor& da = table_.at(g.a);
+  const MatrixDescriptor& db = table_.at(g.b);
+  const MatrixDescriptor& dc = table_.at(g.c);
+  const std::int64_t K = g.trans_a ? da.layout.grid.global_rows : da.layout.grid.global_cols;
+  WorkerPlan plan;
+  const BlockGrid& gc = dc.layout.grid;
+  std::map<int, int> row_idx, col_idx;
+  for (BlockCoord c : owned_coords(dc.layout, w)) {
+    auto [mb, nb] = block_extent(gc, c);
+    if (!row_idx.count(c.row)) {
+      row_idx[c.row] = static_cast<int>(plan.ar.size());
+      Range r;
+      r.start = static_cast<std::int64_t>(c.row) * gc.block_rows;
+      r.len = mb;
+      plan.ar.push_back(std::move(r));
+    }
+    if (!col_idx.count(c.col)) {
+      col_idx[c.col] = static_cast<int>(plan.br.size());
+      Range r;
+      r.start = static_cast<std::int64_t>(c.col) * gc.block_cols;
+      r.len = nb;
+      plan.br.push_back(std::move(r));
+    }
+    plan.tasks.push_back({c, row_idx[c.row], col_idx[c.col]});
+  }
+  if (plan.tasks.empty()) return plan;
+
+  // Single panel first; pipeline K only when some piece has to cross a link.
+  plan.k0 = {0, K};
+  for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
+  for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
+  if (pol == SourcePolicy::Peer) {
+    for (const auto* ranges : {&plan.ar, &plan.br})
+      for (const Range& r : *ranges)
+        for (const Piece& pc : r.panels[0])
+          if (table_.at(pc.matrix).layout.owner(pc.coord) != w) plan.has_remote = true;
+  }
+  const std::int64_t target = env_int("DM_PANEL_K", 8192);
+  if (plan.has_remote && K > 2 * 256 && target > 0) {
+    std::int64_t np = std::max<std::int64_t>(2, (K + target - 1) / target);
+    np = std::min<std::int64_t>(np, K / 256);
+    std::int64_t width = (K + np - 1) / np;
+    width = (width + 31) / 32 * 32;
+    plan.k0.clear();
+    for (std::int64_t k = 0; k < K; k += width) plan.k0.push_back(k);
+    plan.k0.push_back(K);
+    for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
+    for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
+  }
+  return plan;
+}
+
+void Session::record_timing(Worker& w, bool start) {
+  if (!timing_) return;
+  if (start) {
+    if (w.timing_used == w.timing_events.size()) {
+      cudaEvent_t a, b;
+      cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+      cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+      w.timing_events.push_back({a, b});
+    }
+    cuda_check(cudaEventRecord(w.timing_events[w.timing_used].first, w.stream), "cudaEventRecord");
+  } else {
+    cuda_check(cudaEventRecord(w.timing_events[w.timing_used].second, w.stream), "cudaEventRecord");
+    ++w.timing_used;
+  }
+}
+
+void Session::collect_timing() {
+  for (auto& w : workers_) {
+    if (!w) continue;
+    for (std::size_t i = 0; i < w->timing_used; ++i) {
+      float ms = 0;
+      cuda_check(cudaEventElapsedTime(&ms, w->timing_events[i].first, w->timing_events[i].second),
+                 "cudaEventElapsedTime");
+      w->stats.gemm_ms += ms;
+    }
+    w->timing_used = 0;
+  }
+}
+
+void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
+  struct Live {
+    std::vector<DeviceBuffer> bufs;
+    std::vector<cudaEvent_t> events;
+  };
+  std::vector<Live> live(P_);
+  const float alpha = static_cast<float>(g.alpha);
+  const float beta = static_cast<float>(g.beta);
+  const bool read_c0 = g.beta != 0.0;  // kernels.hpp:69-71: beta == 0 never reads C
+  const int cta_group = static_cast<int>(env_int("DM_CTA_GROUP", 0));
+
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    Worker& w = *wp;
+    DeviceGuard guard(w.device);
+    WorkerPlan plan = plan_worker(g, w.id, pol);
+    if (plan.tasks.empty()) continue;
+    Live& lv = live[w.id];
+    const int np = static_cast<int>(plan.k0.size()) - 1;
+    std::int64_t kmax = 0;
+    for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
+    const std::int64_t kpitch = std::max<std::int64_t>(4, (kmax + 3) / 4 * 4);
+    const int nbuf = np > 1 ? 2 : 1;
+    // panel buffers: [range][buf] -> (hi, lo)
+    auto alloc_planes = [&](const std::vector<Range>& rs, std::vector<std::array<float*, 4>>& out) {
+      out.resize(rs.size());
+      for (std::size_t i = 0; i < rs.size(); ++i)
+        for (int b = 0; b < nbuf; ++b)
+          for (int h = 0; h < 2; ++h) {
+            lv.bufs.push_back(
+                w.pool->acquire(static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1) * kpitch) * 4));
+            out[i][b * 2 + h] = lv.bufs.back().f32();
+          }
+    };
+    std::vector<std::array<float*, 4>> pa, pb;
+    alloc_planes(plan.ar, pa);
+    alloc_planes(plan.br, pb);
+    cudaEvent_t split_done[2], gemm_done[2];
+    for (int b = 0; b < 2; ++b) {
+      cuda_check(cudaEventCreateWithFlags(&split_done[b], cudaEventDisableTiming), "event");
+      cuda_check(cudaEventCreateWithFlags(&gemm_done[b], cudaEventDisableTiming), "event");
+      lv.events.push_back(split_done[b]);
+      lv.events.push_back(gemm_done[b]);
+    }
+    // operands of this worker's GEMMs were written by earlier commands on
+    // its own streams; order the side stream after the compute stream.
+    cuda_check(cudaEventRecord(gemm_done[1], w.stream), "event");
+    cuda_check(cudaStreamWaitEvent(w.side, gemm_done[1], 0), "wait");
+
+    for (int p = 0; p < np; ++p) {
+      const int buf = p % nbuf;
+      if (p >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_done[buf], 0), "wait");
+      auto issue = [&](const std::vector<Range>& rs, const std::vector<std::array<float*, 4>>& planes) {
+        for (std::size_t i = 0; i < rs.size(); ++i)
+          for (const Piece& pc : rs[i].panels[p]) {
+            bool remote = false;
+            const float* src = source_ptr(w, pc.matrix, pc.coord, pol, &remote) + pc.src_off;
+            float* hi = planes[i][buf * 2] + pc.dst_row * kpitch + pc.dst_k;
+            float* lo = planes[i][buf * 2 + 1] + pc.dst_row * kpitch + pc.dst_k;
+            cuda_check(split_tf32(src, pc.lds, pc.trans, pc.rows, pc.kcols, hi, lo, kpitch, w.side),
+                       "split_tf32");
+            w.stats.split_launches += 1;
+            (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes();
+          }
+      };
+      issue(plan.ar, pa);
+      issue(plan.br, pb);
+      cuda_check(cudaEventRecord(split_done[buf], w.side), "event");
+      cuda_check(cudaStreamWaitEvent(w.stream, split_done[buf], 0), "wait");
+      const std::int64_t kw = plan.k0[p + 1] - plan.k0[p];
+      for (const Task& t : plan.tasks) {
+        StoredBlock& cb = w.owned.at({g.c, t.c});
+        Tf32x3Args a;
+        a.a_hi = pa[t.ra][buf * 2];
+        a.a_lo = pa[t.ra][buf * 2 + 1];
+        a.lda = kpitch;
+        a.b_hi = pb[t.rb][buf * 2];
+        a.b_lo = pb[t.rb][buf * 2 + 1];
+        a.ldb = kpitch;
+        a.c = cb.mem.f32();
+        a.ldc = cb.cols;
+        a.m = cb.rows;
+        a.n = cb.cols;
+        a.k = kw;
+        a.alpha = alpha;
+        a.beta = p == 0 ? beta : 1.0f;
+        a.read_c = p == 0 ? (read_c0 ? 1 : 0) : 1;
+        a.cta_group = cta_group;
+        record_timing(w, true);
+        cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");
+        record_timing(w, false);
+        w.stats.gemm_launches += 1;
+        w.stats.gemm_flops += 2.0 * static_cast<double>(a.m) * a.n * a.k;
+      }
+      cuda_check(cudaEventRecord(gemm_done[buf], w.stream), "event");
+    }
+  }
+  sync_local();
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    DeviceGuard guard(wp->device);
+    for (cudaEvent_t e : live[wp->id].events) cudaEventDestroy(e);
+    live[wp->id].bufs.clear();
+  }
+}
+
+void Session::cache_foreign_a(const GemmArgs& g) {
+  const MatrixDescriptor& da = table_.at(g.a);
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    Worker& w = *wp;
+    DeviceGuard guard(w.device);
+    for (int r = 0; r < da.layout.grid.n_block_rows(); ++r) {
+      if (da.layout.owner({r, 0}) == w.id) continue;
+      auto [br, bc] = block_extent(da.layout.grid, {r, 0});
+      bool remote = false;
+      const float* src = source_ptr(w, g.a, {r, 0}, SourcePolicy::Peer, &remote);
+      StoredBlock blk;
+      blk.rows = br;
+      blk.cols = bc;
+      blk.version_seen = da.version;
+      blk.mem = w.pool->acquire(static_cast<std::size_t>(br * bc) * 4);
+      cuda_check(cudaMemcpyAsync(blk.mem.data(), src, static_cast<std::size_t>(br * bc) * 4,
+                                 cudaMemcpyDefault, w.side),
+                 "cache copy");
+      w.stats.peer_bytes_read += static_cast<std::uint64_t>(br * bc) * 4;
+      w.cache[{g.a, {r, 0}}] = std::move(blk);
+    }
+  }
+  sync_local();
+}
+
+void Session::general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
+                           bool tb) {
+  require_live();
+  GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, false);
+  validate_general(g);
+  run_gemm(g, SourcePolicy::Peer);
+  bump_version(c);  // runtime_types.hpp:296-301
+  end_command();
+}
+
+void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
+                          bool tb, bool cache_a) {
+  require_live();
+  GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, cache_a);
+  validate_cyclic(g, nullptr);
+  run_gemm(g, SourcePolicy::Peer);
+  if (cache_a) {
+    cache_foreign_a(g);  // CyclicGemmExec::finish, ops.hpp:278-289
+    cache_meta_[a] = table_.at(a).version;
+  } else {
+    for (auto& w : workers_) {
+      if (!w) continue;
+      auto it = w->cache.lower_bound({a, {0, 0}});
+      while (it != w->cache.end() && it->first.matrix == a) it = w->cache.erase(it);
+    }
+    cache_meta_.erase(a);
+  }
+  bump_version(c);
+  end_command();
+}
+
+void Session::cached_backward_gemm(MatrixId w_id, MatrixId dy, MatrixId dx) {
+  require_live();
+  GemmArgs g = gemm_command(1.0, w_id, dy, 0.0, dx, false, false, false);
+  std::vector<WorkerId> strip_owners;
+  validate_cyclic(g, &strip_owners);
+  // Session::backward_missing_coords (session.hpp:547-559)
+  const MatrixDescriptor& dw = table_.at(w_id);
+  auto meta = cache_meta_.find(w_id);
+  const bool fresh = meta != cache_meta_.end() && meta->second == dw.version;
+  std::set<std::pair<int, int>> missing;
+  for (WorkerId cw : std::set<WorkerId>(strip_owners.begin(), strip_owners.end()))
+    for (int r = 0; r < dw.layout.grid.n_block_rows(); ++r)
+      if (dw.layout.owner({r, 0}) != cw && !fresh) missing.insert({r, 0});
+  if (!missing.empty())
+    throw CacheMissError("cached_backward_gemm: blocks not cached at the current version",
+                         {missing.begin(), missing.end()});
+  run_gemm(g, SourcePolicy::LocalOnly);
+  bump_version(dx);
+  end_command();
+}
+
+// ----------------------------------------------------------- introspection
+
+DevicePool::Stats Session::pool_stats(int w) const { return worker(w).pool->stats(); }
+
+std::uint64_t Session::pool_trim(int w) {
+  Worker& wk = worker(w);
+  DeviceGuard g(wk.device);
+  cuda_check(cudaStreamSynchronize(wk.stream), "sync");
+  return wk.pool->trim();
+}
+
+dm_worker_stats Session::worker_stats(int w) const { return worker(w).stats; }
+
+void Session::reset_worker_stats() {
+  for (auto& w : workers_)
+    if (w) w->stats = dm_worker_stats{};
+}
+
+std::uint64_t Session::worker_seed(int w) const {
+  if (w < 0 || w >= P_) throw UsageError("unknown worker id");
+  return mix64(root_seed_, static_cast<std::uint64_t>(w));
+}
+
+std::uint64_t Session::master_digest() const { return table_digest(table_); }
+
+std::vector<std::uint64_t> Session::worker_digests() const {
+  std::vector<std::uint64_t> out;
+  for (const auto& w : workers_)
+    if (w) out.push_back(table_digest(w->descriptors));
+  return out;
+}
+
+void* Session::block_device_ptr(MatrixId id, BlockCoord c, int* device) const {
+  const MatrixDescriptor& d = descriptor(id);
+  const int owner = d.layout.owner(c);
+  const Worker* w = local(owner);
+  if (w == nullptr) throw UsageError("block is not owned by a local worker");
+  *device = w->device;
+  return w->owned.at({id, c}).mem.data();
+}
+
+}  // namespace dm

@@ -1,0 +1,176 @@
+// Session: the master facade of the distributed-matrix runtime on B200.
+//
+// Reference: gridgemm::Session (session.hpp:53-725) with WorkerContext
+// (runtime_types.hpp:167-260) and the GEMM executors of ops.hpp.  The
+// reference emulates workers as threads exchanging memcpy'd messages; here a
+// worker is a GPU:
+//   * owned / cached blocks live in HBM, allocated from a per-worker caching
+//     DevicePool (pool.hpp);
+//   * a GEMM is executed by every worker as a pipeline of K panels: operand
+//     pieces are PULLED straight from the owning worker's HBM (same device,
+//     CUDA peer access, or CUDA-IPC mapped across processes over NVLink) by
+//     the split kernel, which writes the tf32 hi/lo K-major panels the
+//     tcgen05 GEMM consumes; panel p+1 is pulled on a side stream while
+//     panel p multiplies (double-buffered);
+//   * LOCAL mode: one process drives all P workers (tests, 1-GPU parity at
+//     any P);  SPMD mode: one process per GPU (torchrun), every rank issues
+//     the same calls in the same order, NCCL provides the barrier and the
+//     IPC-handle exchange.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "layout.hpp"
+#include "pool.hpp"
+
+namespace dm {
+
+enum class FillKind : std::uint8_t { Zeros = 0, SeededRandom = 1, FromHost = 2 };
+
+struct StoredBlock {
+  std::int64_t rows = 0, cols = 0;
+  std::uint64_t version_seen = 0;
+  DeviceBuffer mem;
+};
+
+struct BlockKey {
+  MatrixId matrix = 0;
+  BlockCoord coord;
+  friend bool operator<(const BlockKey& a, const BlockKey& b) {
+    return a.matrix != b.matrix ? a.matrix < b.matrix : a.coord < b.coord;
+  }
+};
+
+struct GemmArgs {
+  double alpha = 1.0, beta = 0.0;
+  MatrixId a = 0, b = 0, c = 0;
+  bool trans_a = false, trans_b = false, cache_a = false;
+};
+
+enum class SourcePolicy { Peer, LocalOnly };
+
+struct Worker {
+  int id = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;  // GEMM stream
+  cudaStream_t side = nullptr;    // pull/split stream
+  std::unique_ptr<DevicePool> pool;
+  std::map<MatrixId, MatrixDescriptor> descriptors;
+  std::map<BlockKey, StoredBlock> owned;
+  std::map<BlockKey, StoredBlock> cache;
+  std::uint64_t seed = 0;
+  dm_worker_stats stats{};
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_events;
+  std::size_t timing_used = 0;
+};
+
+class Comm;  // NCCL bootstrap + IPC directory (comm.cpp)
+
+class Session {
+ public:
+  explicit Session(const dm_session_config& cfg);
+  ~Session();
+  Session(const Session&) = delete;
+  Session& operator=(const Session&) = delete;
+
+  int worker_count() const { return P_; }
+  bool spmd() const { return mode_ == DM_MODE_SPMD; }
+  int rank() const { return rank_; }
+  std::vector<int> local_worker_ids() const;
+
+  MatrixId create_matrix(const LayoutSpec& layout, Precision p, FillKind fill, const float* host);
+  void destroy_matrix(MatrixId id);
+  void scatter(MatrixId id, const float* host, std::int64_t rows, std::int64_t cols);
+  void gather(MatrixId id, float* host, std::int64_t rows, std::int64_t cols, int root);
+  void general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
+                    bool tb);
+  void cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta, bool tb,
+                   bool cache_a);
+  void cached_backward_gemm(MatrixId w, MatrixId dy, MatrixId dx);
+  void shutdown();
+  bool live() const { return live_; }
+
+  const MatrixDescriptor& descriptor(MatrixId id) const;
+  DevicePool::Stats pool_stats(int w) const;
+  std::uint64_t pool_trim(int w);
+  dm_worker_stats worker_stats(int w) const;
+  void reset_worker_stats();
+  void set_gemm_timing(bool on) { timing_ = on; }
+  std::uint64_t worker_seed(int w) const;
+  std::uint64_t master_digest() const;
+  std::vector<std::uint64_t> worker_digests() const;
+  void* block_device_ptr(MatrixId id, BlockCoord c, int* device) const;
+  void barrier();
+
+ private:
+  struct Piece {
+    MatrixId matrix = 0;
+    BlockCoord coord;
+    std::int64_t src_off = 0, lds = 0;
+    int trans = 0;
+    std::int64_t rows = 0, kcols = 0;
+    std::int64_t dst_row = 0, dst_k = 0;
+    std::size_t bytes() const { return static_cast<std::size_t>(rows * kcols) * 4; }
+  };
+  struct Range {
+    std::int64_t start = 0, len = 0;
+    std::vector<std::vector<Piece>> panels;  // [panel] -> pieces
+  };
+  struct Task {
+    BlockCoord c;
+    int ra = 0, rb = 0;
+  };
+  struct WorkerPlan {
+    std::vector<Range> ar, br;
+    std::vector<Task> tasks;
+    std::vector<std::int64_t> k0;  // panel starts, size np+1
+    bool has_remote = false;
+  };
+
+  Worker& worker(int w);
+  const Worker& worker(int w) const;
+  Worker* local(int w);
+  const Worker* local(int w) const;
+  void require_live() const;
+  void validate_layout_workers(const LayoutSpec& l) const;
+  void apply_effects_create(const MatrixDescriptor& d);
+  void bump_version(MatrixId id);
+  void end_command();
+  void sync_local();
+
+  GemmArgs gemm_command(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
+                        bool tb, bool cache_a) const;
+  void validate_general(const GemmArgs& g) const;
+  void validate_cyclic(const GemmArgs& g, std::vector<WorkerId>* strip_owners) const;
+
+  WorkerPlan plan_worker(const GemmArgs& g, int w, SourcePolicy pol) const;
+  void add_range_pieces(Range& rg, const MatrixDescriptor& d, bool op_rows_trans, bool is_a,
+                        const std::vector<std::int64_t>& k0) const;
+  const float* source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
+                          bool* remote) const;
+  void run_gemm(const GemmArgs& g, SourcePolicy pol);
+  void cache_foreign_a(const GemmArgs& g);
+  void record_timing(Worker& w, bool start);
+  void collect_timing();
+
+  int P_ = 1;
+  int mode_ = DM_MODE_LOCAL;
+  int rank_ = 0;
+  bool coherence_ = true;
+  bool live_ = false;
+  bool timing_ = false;
+  std::uint64_t root_seed_ = 0;
+  std::uint64_t next_matrix_id_ = 1;
+  std::vector<std::unique_ptr<Worker>> workers_;  // index = worker id; null if not local
+  std::map<MatrixId, MatrixDescriptor> table_;
+  std::map<MatrixId, std::uint64_t> cache_meta_;
+  std::unique_ptr<Comm> comm_;
+};
+
+}  // namespace dm

@@ -1,0 +1,398 @@
+"""Python mirror of the reference's distributed-matrix API over the C ABI.
+
+Names, argument meaning and error behaviour follow gridgemm::Session
+(/root/reference/proj/include/gridgemm/session.hpp:53-485) and the layout
+helpers of gridgemm/layout.hpp so parity tests read like the reference's own
+tests.  Every call goes through libdmath_b200.so; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._lib import Descriptor, Layout, PoolStats, SessionConfig, WorkerStats, lib
+
+
+# --------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """gridgemm::Error (common.hpp:22-25)."""
+
+
+class UsageError(Error): ...
+class ConfigError(Error): ...
+class ShapeError(Error): ...
+class ProtocolError(Error): ...
+class DeadlockError(Error): ...
+class IntegrityError(Error): ...
+class PlanError(Error): ...
+class CudaError(Error): ...
+class NcclError(Error): ...
+class UnsupportedError(Error): ...
+
+
+class CacheMissError(Error):
+    """gridgemm::CacheMissError (common.hpp:72-78)."""
+
+    def __init__(self, what: str, missing_coords):
+        super().__init__(what)
+        self.missing_coords = list(missing_coords)
+
+
+_CODES = {1: UsageError, 2: ConfigError, 3: ShapeError, 4: ProtocolError, 5: DeadlockError,
+          6: IntegrityError, 7: PlanError, 8: CacheMissError, 9: CudaError, 10: NcclError,
+          11: UnsupportedError}
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = (lib.dm_last_error() or b"").decode(errors="replace")
+    cls = _CODES.get(rc, Error)
+    if cls is CacheMissError:
+        buf = (C.c_int32 * 4096)()
+        n = lib.dm_last_error_missing(buf, 2048)
+        raise CacheMissError(msg, [(buf[2 * i], buf[2 * i + 1]) for i in range(min(n, 2048))])
+    raise cls(msg)
+
+
+# --------------------------------------------------------------- enums
+class LayoutKind(enum.IntEnum):
+    """layout.hpp:69-75"""
+    RowBlocks1D = 0
+    ColBlocks1D = 1
+    RowCyclic1D = 2
+    Checkerboard2D = 3
+    Custom = 4
+
+
+class Precision(enum.IntEnum):
+    """precision.hpp:14"""
+    Half16 = 0
+    Single32 = 1
+    Double64 = 2
+
+
+class FillKind(enum.IntEnum):
+    """runtime_types.hpp:68"""
+    Zeros = 0
+    SeededRandom = 1
+    FromHost = 2
+
+
+# --------------------------------------------------------------- layouts
+@dataclass
+class LayoutSpec:
+    """LayoutSpec (layout.hpp:116-142).  block_rows/cols are the nominal
+    (un-clamped) sizes as given; the library clamps like make_grid."""
+    kind: LayoutKind
+    global_rows: int
+    global_cols: int
+    block_rows: int
+    block_cols: int
+    worker_count: int
+    custom: Optional[Sequence[int]] = None
+    _keep: list = field(default_factory=list, repr=False, compare=False)
+
+    def _abi(self) -> Layout:
+        l = Layout(int(self.kind), int(self.worker_count), int(self.global_rows),
+                   int(self.global_cols), int(self.block_rows), int(self.block_cols), None, 0)
+        if self.custom is not None:
+            arr = (C.c_int32 * len(self.custom))(*self.custom)
+            self._keep[:] = [arr]
+            l.custom = C.cast(arr, C.POINTER(C.c_int32))
+            l.custom_len = len(self.custom)
+        return l
+
+    def owner(self, row: int, col: int) -> int:
+        o = C.c_int()
+        _check(lib.dm_layout_owner(C.byref(self._abi()), row, col, C.byref(o)))
+        return o.value
+
+    def grid(self):
+        r, c, cl = C.c_int(), C.c_int(), C.c_int()
+        _check(lib.dm_layout_grid(C.byref(self._abi()), C.byref(r), C.byref(c), C.byref(cl)))
+        return r.value, c.value, bool(cl.value)
+
+    def block_extent(self, row: int, col: int):
+        r, c = C.c_int64(), C.c_int64()
+        _check(lib.dm_block_extent(C.byref(self._abi()), row, col, C.byref(r), C.byref(c)))
+        return r.value, c.value
+
+    def to_string(self) -> str:
+        buf = C.create_string_buffer(1 << 16)
+        n = lib.dm_layout_to_string(C.byref(self._abi()), buf, len(buf))
+        if n < 0:
+            _check(-n)
+        return buf.value.decode()
+
+
+def make_layout(kind, global_rows, global_cols, block_rows, block_cols, worker_count) -> LayoutSpec:
+    """make_layout (layout.hpp:146-156)."""
+    spec = LayoutSpec(LayoutKind(kind), global_rows, global_cols, block_rows, block_cols, worker_count)
+    spec.grid()  # validates (UsageError on non-positive sizes)
+    return spec
+
+
+def make_custom_layout(global_rows, global_cols, block_rows, block_cols, worker_count, table) -> LayoutSpec:
+    """make_custom_layout (layout.hpp:158-171)."""
+    spec = LayoutSpec(LayoutKind.Custom, global_rows, global_cols, block_rows, block_cols,
+                      worker_count, list(table))
+    spec.grid()
+    return spec
+
+
+def checkerboard_dims(workers: int):
+    pr, pc = C.c_int(), C.c_int()
+    _check(lib.dm_checkerboard_dims(workers, C.byref(pr), C.byref(pc)))
+    return pr.value, pc.value
+
+
+def pool_size_class(nbytes: int) -> int:
+    return int(lib.dm_pool_size_class(nbytes))
+
+
+def plan_general_gemm(la: LayoutSpec, ta: bool, lb: LayoutSpec, tb: bool, lc: LayoutSpec, worker: int):
+    """Distinct peer blocks (and bytes) `worker` reads for general_gemm."""
+    nb, by = C.c_int64(), C.c_int64()
+    _check(lib.dm_plan_general_gemm(C.byref(la._abi()), int(ta), C.byref(lb._abi()), int(tb),
+                                    C.byref(lc._abi()), worker, C.byref(nb), C.byref(by)))
+    return nb.value, by.value
+
+
+# --------------------------------------------------------------- session
+@dataclass
+class Config:
+    """Session::Config (session.hpp:55-62) plus the B200 placement fields."""
+    worker_count: int = 1
+    root_seed: int = 0
+    coherence_checks: bool = True
+    mode: str = "local"              # "local" (one process, all workers) | "spmd" (one per GPU)
+    rank: int = 0                    # spmd only
+    devices: Optional[Sequence[int]] = None  # local: device per worker; spmd: [device]
+    nccl_id: Optional[bytes] = None  # spmd only: 128-byte id from nccl_unique_id() on rank 0
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.dm_nccl_unique_id(buf))
+    return buf.raw
+
+
+@dataclass
+class MatrixDescriptor:
+    matrix_id: int
+    precision: Precision
+    replicated: bool
+    version: int
+    replica_version: int
+    seed: int
+    layout: LayoutSpec
+
+
+def _host_ptr(arr: np.ndarray):
+    return C.c_void_p(arr.ctypes.data)
+
+
+class Session:
+    """gridgemm::Session on B200 workers (one GPU each)."""
+
+    def __init__(self, cfg: Config):
+        self._cfg = cfg
+        mode = {"local": 0, "spmd": 1}[cfg.mode]
+        devs = None
+        if cfg.devices is not None:
+            devs = (C.c_int32 * len(cfg.devices))(*cfg.devices)
+        nid = None
+        if cfg.nccl_id is not None:
+            nid = C.create_string_buffer(bytes(cfg.nccl_id), 128)
+        c = SessionConfig(cfg.worker_count, mode, cfg.rank, int(cfg.coherence_checks),
+                          cfg.root_seed & (2**64 - 1),
+                          C.cast(devs, C.POINTER(C.c_int32)) if devs is not None else None,
+                          C.cast(nid, C.c_void_p) if nid is not None else None)
+        h = C.c_void_p()
+        _check(lib.dm_session_create(C.byref(c), C.byref(h)))
+        self._h = h
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.dm_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def shutdown(self):
+        _check(lib.dm_session_shutdown(self._h))
+
+    # -- introspection
+    def worker_count(self) -> int:
+        n = C.c_int()
+        _check(lib.dm_worker_count(self._h, C.byref(n)))
+        return n.value
+
+    def local_workers(self):
+        buf = (C.c_int32 * 1024)()
+        n = lib.dm_local_workers(self._h, buf, 1024)
+        if n < 0:
+            _check(-n)
+        return list(buf[:n])
+
+    def descriptor(self, mid: int) -> MatrixDescriptor:
+        d = Descriptor()
+        _check(lib.dm_descriptor_get(self._h, mid, C.byref(d)))
+        l = d.layout
+        custom = [l.custom[i] for i in range(l.custom_len)] if l.custom_len else None
+        spec = LayoutSpec(LayoutKind(l.kind), l.global_rows, l.global_cols, l.block_rows,
+                          l.block_cols, l.worker_count, custom)
+        return MatrixDescriptor(d.matrix_id, Precision(d.precision), bool(d.replicated), d.version,
+                                d.replica_version, d.seed, spec)
+
+    def worker_pool_stats(self, w: int) -> PoolStats:
+        s = PoolStats()
+        _check(lib.dm_pool_stats_get(self._h, w, C.byref(s)))
+        return s
+
+    def pool_trim(self, w: int) -> int:
+        f = C.c_uint64()
+        _check(lib.dm_pool_trim(self._h, w, C.byref(f)))
+        return f.value
+
+    def worker_stats(self, w: int) -> WorkerStats:
+        s = WorkerStats()
+        _check(lib.dm_worker_stats_get(self._h, w, C.byref(s)))
+        return s
+
+    def reset_worker_stats(self):
+        _check(lib.dm_worker_stats_reset(self._h))
+
+    def set_gemm_timing(self, on: bool):
+        _check(lib.dm_set_gemm_timing(self._h, int(on)))
+
+    def worker_seed(self, w: int) -> int:
+        v = C.c_uint64()
+        _check(lib.dm_worker_seed(self._h, w, C.byref(v)))
+        return v.value
+
+    def descriptor_digests(self):
+        m = C.c_uint64()
+        buf = (C.c_uint64 * 1024)()
+        n = lib.dm_descriptor_digest(self._h, C.byref(m), buf, 1024)
+        if n < 0:
+            _check(-n)
+        return [m.value] + list(buf[:n])
+
+    def block_device_ptr(self, mid: int, row: int, col: int):
+        p, d = C.c_void_p(), C.c_int()
+        _check(lib.dm_block_device_ptr(self._h, mid, row, col, C.byref(p), C.byref(d)))
+        return p.value, d.value
+
+    def barrier(self):
+        _check(lib.dm_barrier(self._h))
+
+    # -- matrices
+    def create_matrix(self, layout: LayoutSpec, precision=Precision.Single32,
+                      fill=FillKind.Zeros, host: Optional[np.ndarray] = None) -> int:
+        """Session::create_matrix (session.hpp:129-150)."""
+        hp = None
+        if fill == FillKind.FromHost:
+            if host is None:
+                raise UsageError("create_matrix: FromHost requires host data")
+            host = self._host_in(host)
+            if host.shape != (layout.global_rows, layout.global_cols):
+                raise ShapeError("create_matrix: host data shape does not match the layout")
+            hp = _host_ptr(host)
+        out = C.c_uint64()
+        _check(lib.dm_create_matrix(self._h, C.byref(layout._abi()), int(precision), int(fill), hp,
+                                    C.byref(out)))
+        return out.value
+
+    def destroy_matrix(self, mid: int):
+        _check(lib.dm_destroy_matrix(self._h, mid))
+
+    @staticmethod
+    def _host_in(host: np.ndarray) -> np.ndarray:
+        if host.dtype != np.float32:
+            raise UnsupportedError("host data must be float32 (Single32)")
+        return np.ascontiguousarray(host)
+
+    def scatter(self, mid: int, host: np.ndarray):
+        """Session::scatter (session.hpp:164-175); bit-exact."""
+        host = self._host_in(host)
+        if host.ndim != 2:
+            raise ShapeError("scatter: host data must be 2-D")
+        _check(lib.dm_scatter(self._h, mid, _host_ptr(host), host.shape[0], host.shape[1]))
+
+    def gather(self, mid: int, out: Optional[np.ndarray] = None, root: int = 0) -> np.ndarray:
+        """Session::gather (session.hpp:179-201); bit-exact, owned blocks only."""
+        d = self.descriptor(mid)
+        shape = (d.layout.global_rows, d.layout.global_cols)
+        if out is None:
+            out = np.empty(shape, dtype=np.float32)
+        if out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+            raise ShapeError("gather: output buffer shape does not match the matrix")
+        _check(lib.dm_gather(self._h, mid, _host_ptr(out), shape[0], shape[1], root))
+        return out
+
+    # -- distributed operations
+    def general_gemm(self, alpha, a, b, beta, c, trans_a=False, trans_b=False):
+        """Session::general_gemm (session.hpp:244-250)."""
+        _check(lib.dm_general_gemm(self._h, float(alpha), a, b, float(beta), c, int(trans_a), int(trans_b)))
+
+    def cyclic_gemm(self, alpha, a, b, beta, c, trans_a=False, trans_b=False, cache_a=False):
+        """Session::cyclic_gemm (session.hpp:226-234)."""
+        _check(lib.dm_cyclic_gemm(self._h, float(alpha), a, b, float(beta), c, int(trans_a),
+                                  int(trans_b), int(cache_a)))
+
+    def broadcast_gemm_reference(self, alpha, a, b, beta, c, trans_a=False, trans_b=False):
+        """Session::broadcast_gemm_reference (session.hpp:236-242)."""
+        _check(lib.dm_broadcast_gemm_reference(self._h, float(alpha), a, b, float(beta), c,
+                                               int(trans_a), int(trans_b)))
+
+    def cached_backward_gemm(self, w, dy, dx):
+        """Session::cached_backward_gemm (session.hpp:254-264)."""
+        _check(lib.dm_cached_backward_gemm(self._h, w, dy, dx))
+
+
+# --------------------------------------------------------------- device seam
+def local_gemm(alpha, a, trans_a, b, trans_b, beta, c, cta_group: int = 0, stream=None):
+    """local_gemm (kernels.hpp:81-89) on CUDA tensors (anything exposing
+    data_ptr()/shape/stride, e.g. torch float32 CUDA tensors, row-major)."""
+    def dims(t):
+        r, cc = t.shape
+        if t.stride(1) != 1:
+            raise UsageError("local_gemm: operands must be row-major (unit column stride)")
+        return r, cc, t.stride(0)
+    ar, ac, lda = dims(a)
+    br, bc, ldb = dims(b)
+    cr, cc, ldc = dims(c)
+    m, k = (ac, ar) if trans_a else (ar, ac)
+    kb, n = (bc, br) if trans_b else (br, bc)
+    if k != kb:
+        raise ShapeError("local_gemm: inner dimensions do not conform")
+    if (cr, cc) != (m, n):
+        raise ShapeError("local_gemm: output dimensions do not conform")
+    st = C.c_void_p(stream) if stream is not None else None
+    _check(lib.dm_local_gemm_f32_ex(float(alpha), C.c_void_p(a.data_ptr()), lda, int(trans_a),
+                                    C.c_void_p(b.data_ptr()), ldb, int(trans_b), float(beta),
+                                    C.c_void_p(c.data_ptr()), ldc, m, n, k, cta_group, st))
+
+
+def fill_seeded(t, matrix_seed: int, block_row: int, block_col: int, stream=None):
+    """WorkerContext::fill_seeded (runtime_types.hpp:208-218) into a CUDA tensor."""
+    st = C.c_void_p(stream) if stream is not None else None
+    _check(lib.dm_fill_seeded_f32(C.c_void_p(t.data_ptr()), t.numel(), matrix_seed & (2**64 - 1),
+                                  block_row, block_col, st))

@@ -1,0 +1,79 @@
+"""Numerics of the tcgen05 3xTF32 GEMM through the local_gemm seam
+(kernels.hpp:81-89 semantics) against an fp64 PyTorch reference.
+
+Tolerance: relative Frobenius error <= 1e-5 (the reference's fp32 bar,
+harness.hpp:114-120); 3xTF32 lands near 1e-7 at these sizes.
+"""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _relfro(got, want):
+    import torch
+    d = (got.double() - want).norm()
+    n = want.norm()
+    return float(d / n) if n > 0 else float(d)
+
+
+def _run(cuda, m, n, k, ta, tb, alpha, beta, cg, seed=0):
+    import torch
+    from paper_1604_01416_b200 import local_gemm
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    A = (torch.rand((k, m) if ta else (m, k), generator=g) * 2 - 1).to(cuda)
+    B = (torch.rand((n, k) if tb else (k, n), generator=g) * 2 - 1).to(cuda)
+    C0 = (torch.rand((m, n), generator=g) * 2 - 1).to(cuda)
+    C = C0.clone()
+    local_gemm(alpha, A, ta, B, tb, beta, C, cta_group=cg)
+    torch.cuda.synchronize()
+    opA = A.double().T if ta else A.double()
+    opB = B.double().T if tb else B.double()
+    want = alpha * (opA @ opB)
+    if beta != 0.0:
+        want = want + beta * C0.double()
+    return _relfro(C, want)
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("m,n,k", [(128, 128, 32), (256, 256, 64), (300, 200, 100), (3, 5, 7),
+                                   (1024, 1024, 1024), (1000, 1500, 777)])
+def test_shapes(cuda, cg, m, n, k):
+    assert _run(cuda, m, n, k, False, False, 1.0, 0.0, cg) <= TOL
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_transposes_alpha_beta(cuda, cg, ta, tb):
+    assert _run(cuda, 520, 390, 260, ta, tb, 1.5, -0.5, cg, seed=3) <= TOL
+
+
+def test_beta_zero_ignores_garbage_c(cuda):
+    """test_core.cpp:264-275: beta == 0 must not read C (NaN garbage stays out)."""
+    import torch
+    from paper_1604_01416_b200 import local_gemm
+    A = torch.rand(64, 48, device=cuda)
+    B = torch.rand(48, 80, device=cuda)
+    C = torch.full((64, 80), float("nan"), device=cuda)
+    local_gemm(1.0, A, False, B, False, 0.0, C)
+    torch.cuda.synchronize()
+    assert torch.isfinite(C).all()
+    assert _relfro(C, A.double() @ B.double()) <= TOL
+
+
+def test_k_zero_scales_c(cuda):
+    import torch
+    from paper_1604_01416_b200 import local_gemm
+    A = torch.empty(16, 0, device=cuda)
+    B = torch.empty(0, 8, device=cuda)
+    C = torch.ones(16, 8, device=cuda)
+    local_gemm(2.0, A, False, B, False, 0.5, C)
+    torch.cuda.synchronize()
+    assert torch.equal(C, torch.full_like(C, 0.5))
+
+
+@pytest.mark.parametrize("cg", [1, 2])
+def test_large_k_accuracy(cuda, cg):
+    """K=16384: fp32-level accuracy (1xTF32 would sit near 2.5e-4)."""
+    assert _run(cuda, 512, 512, 16384, False, False, 1.0, 0.0, cg, seed=7) <= 2e-6

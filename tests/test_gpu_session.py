@@ -1,0 +1,142 @@
+"""Distributed-matrix session on the GPU: distribute/collect bit-exactness and
+general/cyclic/cached-backward GEMM parity, LOCAL mode (all workers driven by
+this process; P workers may share one GPU).
+
+Mirrors tests/test_runtime.cpp:106-141 (scatter/gather bitwise, 4 layouts)
+and tests/test_dist_ops.cpp:149-155, 206-249, 267-306 of the reference.
+"""
+import numpy as np
+import pytest
+
+from paper_1604_01416_b200 import (CacheMissError, Config, FillKind, LayoutKind, PlanError,
+                                   Session, ShapeError, UsageError, make_layout)
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+KINDS = [LayoutKind.RowBlocks1D, LayoutKind.ColBlocks1D, LayoutKind.RowCyclic1D,
+         LayoutKind.Checkerboard2D]
+
+
+def relfro(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    den = np.linalg.norm(want)
+    return float(np.linalg.norm(got - want) / den) if den else float(np.linalg.norm(got - want))
+
+
+def ref_gemm(alpha, A, ta, B, tb, beta, C0):
+    a = A.astype(np.float64)
+    b = B.astype(np.float64)
+    out = alpha * ((a.T if ta else a) @ (b.T if tb else b))
+    if beta != 0.0:
+        out = out + beta * C0.astype(np.float64)
+    return out
+
+
+@pytest.mark.parametrize("P", [1, 2, 4])
+@pytest.mark.parametrize("kind", KINDS)
+def test_scatter_gather_bitwise(cuda, P, kind):
+    rng = np.random.default_rng(P * 10 + int(kind))
+    host = rng.standard_normal((37, 53)).astype(np.float32)
+    with Session(Config(worker_count=P, root_seed=5, devices=[0] * P)) as s:
+        lay = make_layout(kind, 37, 53, 8, 16, P)
+        m = s.create_matrix(lay, fill=FillKind.FromHost, host=host)
+        assert s.descriptor(m).version == 1
+        back = s.gather(m)
+        assert back.tobytes() == host.tobytes()
+
+
+@pytest.mark.parametrize("P", [1, 3, 4])
+@pytest.mark.parametrize("trans", [0, 1, 2, 3])
+def test_general_gemm_mixed_layouts(cuda, P, trans):
+    ta, tb = bool(trans & 1), bool(trans & 2)
+    n = 96
+    with Session(Config(worker_count=P, root_seed=9000 + trans, devices=[0] * P)) as s:
+        la = make_layout(KINDS[trans % 4], n, n, 20, 24, P)
+        lb = make_layout(KINDS[(trans + 1) % 4], n, n, 24, 20, P)
+        lc = make_layout(KINDS[(trans + 2) % 4], n, n, 32, 16, P)
+        a = s.create_matrix(la, fill=FillKind.SeededRandom)
+        b = s.create_matrix(lb, fill=FillKind.SeededRandom)
+        c = s.create_matrix(lc, fill=FillKind.SeededRandom)
+        A, B, C0 = s.gather(a), s.gather(b), s.gather(c)
+        s.general_gemm(1.5, a, b, -0.5, c, ta, tb)
+        got = s.gather(c)
+        assert relfro(got, ref_gemm(1.5, A, ta, B, tb, -0.5, C0)) <= TOL
+        assert s.descriptor(c).version == 1
+
+
+def test_general_gemm_checkerboard_2048(cuda):
+    """BASELINE config 1: 2048^3 on a 2x2 checkerboard of 1024^2 blocks, P=4."""
+    n, P = 2048, 4
+    with Session(Config(worker_count=P, root_seed=42, devices=[0] * P)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
+        a = s.create_matrix(lay, fill=FillKind.SeededRandom)
+        b = s.create_matrix(lay, fill=FillKind.SeededRandom)
+        c = s.create_matrix(lay, fill=FillKind.SeededRandom)
+        A, B = s.gather(a), s.gather(b)
+        s.general_gemm(1.0, a, b, 0.0, c, False, False)
+        got = s.gather(c)
+        assert relfro(got, ref_gemm(1.0, A, False, B, False, 0.0, None)) <= TOL
+        st = [s.worker_stats(w) for w in range(P)]
+        # every worker pulls one A block and one B block of 4 MiB (2N^2 bytes ingress)
+        assert all(x.peer_bytes_read == 2 * 1024 * 1024 * 4 for x in st)
+
+
+def test_cyclic_and_cached_backward(cuda):
+    """FC pattern: fwd Y=W^T X (TN, cache W), bwd dX=W dY (NN, cached)."""
+    P, fin, fout, batch = 4, 96, 64, 32
+    with Session(Config(worker_count=P, root_seed=3, devices=[0] * P)) as s:
+        W = s.create_matrix(make_layout(LayoutKind.RowBlocks1D, fin, fout, fin // P, fout, P),
+                            fill=FillKind.SeededRandom)
+        strip = batch // P
+        X = s.create_matrix(make_layout(LayoutKind.ColBlocks1D, fin, batch, fin, strip, P),
+                            fill=FillKind.SeededRandom)
+        Y = s.create_matrix(make_layout(LayoutKind.ColBlocks1D, fout, batch, fout, strip, P))
+        dY = s.create_matrix(make_layout(LayoutKind.ColBlocks1D, fout, batch, fout, strip, P),
+                             fill=FillKind.SeededRandom)
+        dX = s.create_matrix(make_layout(LayoutKind.ColBlocks1D, fin, batch, fin, strip, P))
+        Wh, Xh, dYh = s.gather(W), s.gather(X), s.gather(dY)
+        with pytest.raises(CacheMissError) as ei:
+            s.cached_backward_gemm(W, dY, dX)
+        assert len(ei.value.missing_coords) > 0
+        s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+        assert relfro(s.gather(Y), ref_gemm(1.0, Wh, True, Xh, False, 0.0, None)) <= TOL
+        s.reset_worker_stats()
+        s.cached_backward_gemm(W, dY, dX)
+        assert relfro(s.gather(dX), ref_gemm(1.0, Wh, False, dYh, False, 0.0, None)) <= TOL
+        assert all(s.worker_stats(w).peer_bytes_read == 0 for w in range(P))
+        # stale cache after W changes -> CacheMissError
+        s.scatter(W, np.zeros((fin, fout), np.float32))
+        with pytest.raises(CacheMissError):
+            s.cached_backward_gemm(W, dY, dX)
+
+
+def test_plan_and_usage_errors(cuda):
+    with Session(Config(worker_count=2, devices=[0, 0])) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, 8, 8, 4, 4, 2)
+        a = s.create_matrix(lay, fill=FillKind.SeededRandom)
+        b = s.create_matrix(lay, fill=FillKind.SeededRandom)
+        with pytest.raises(UsageError):
+            s.general_gemm(1.0, a, b, 0.0, a)
+        with pytest.raises(PlanError):
+            s.cyclic_gemm(1.0, a, b, 0.0, s.create_matrix(lay))
+        c = s.create_matrix(make_layout(LayoutKind.Checkerboard2D, 8, 9, 4, 4, 2))
+        with pytest.raises(ShapeError):
+            s.general_gemm(1.0, a, b, 0.0, c)
+
+
+def test_pool_steady_state(cuda):
+    """acceptance.cpp:437-457: repeated GEMM allocates only on its first iteration."""
+    P = 4
+    with Session(Config(worker_count=P, root_seed=11, devices=[0] * P)) as s:
+        la = make_layout(LayoutKind.RowBlocks1D, 16, 16, 2, 16, P)
+        lbc = make_layout(LayoutKind.ColBlocks1D, 16, 16, 16, 4, P)
+        a = s.create_matrix(la, fill=FillKind.SeededRandom)
+        b = s.create_matrix(lbc, fill=FillKind.SeededRandom)
+        c = s.create_matrix(lbc)
+        s.cyclic_gemm(1.0, a, b, 0.0, c)
+        fresh = [s.worker_pool_stats(w).fresh_allocations for w in range(P)]
+        for _ in range(10):
+            s.cyclic_gemm(1.0, a, b, 0.0, c)
+        assert [s.worker_pool_stats(w).fresh_allocations for w in range(P)] == fresh
