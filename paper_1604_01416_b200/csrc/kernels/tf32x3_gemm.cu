@@ -14,9 +14,9 @@
 // Structure (one persistent CTA per SM, or one CTA pair per TPC for CG=2):
 //   warp 0      TMA producer   4 tiles per stage (A hi/lo, B hi/lo), 128B swizzle
 //   warp 1      MMA issuer     tcgen05.mma.kind::tf32, 3 MMAs per k8 step; owns TMEM
-//   warps 2..5  epilogue       tcgen05.ld -> alpha/beta -> global stores
-// Pipelines: smem full/empty mbarriers (TMA<->MMA) and a double-buffered TMEM
-// accumulator with full/empty mbarriers (MMA<->epilogue).
+//   warps 2..9  epilogue       tcgen05.ld -> fp32 master (RN) -> alpha/beta -> stores
+// Pipelines: smem full/empty mbarriers (TMA<->MMA) and double-buffered TMEM
+// K-chunk accumulators with full/empty mbarriers (MMA<->epilogue).
 //
 // CG=1: tile 128x128 (UMMA M=128,N=128), cta_group::1.
 // CG=2: CTA pair computes a 256x256 tile (UMMA M=256,N=256, cta_group::2);
@@ -44,9 +44,11 @@ struct Cfg {
   static constexpr int kStages = 3;
   static constexpr int kTileBytes = kRowsPerCta * kBK * 4;  // 16 KB
   static constexpr int kStageBytes = 4 * kTileBytes;        // 64 KB
-  static constexpr int kAccCols = kUmmaN;                    // fp32 TMEM columns per buffer
-  static constexpr int kTmemCols = 2 * kAccCols;             // double-buffered
-  static constexpr int kThreads = 192;
+  static constexpr int kAccCols = kUmmaN;                    // fp32 TMEM columns per chunk buffer
+  static constexpr int kTmemCols = 2 * kAccCols;             // double-buffered chunks
+  static constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quadrant
+  static constexpr int kColsPerThread = kAccCols / 2;        // master accumulator registers
+  static constexpr int kThreads = 64 + 32 * kEpiWarps;
   static constexpr int kGroupM = 8;                          // rasterisation group
   static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -71,12 +73,20 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nt = r / gsize;
 }
 
+// Numerics note.  The tensor core adds each MMA's products into the fp32
+// accumulator with truncation (round toward zero), so the relative error of
+// one TMEM accumulator grows linearly with the number of MMAs issued into it
+// (measured ~2e-8 per MMA: 1.1e-4 at K=16384 without chunking).  The K loop is
+// therefore cut into chunks of `kc_blocks` k-blocks: each chunk accumulates in
+// a fresh TMEM buffer and the epilogue warps fold it into an fp32 register
+// master with round-to-nearest adds, making the error K-independent.
 template <int CG>
 __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     tf32x3_gemm_kernel(const __grid_constant__ CUtensorMap tm_ahi,
                        const __grid_constant__ CUtensorMap tm_alo,
                        const __grid_constant__ CUtensorMap tm_bhi,
-                       const __grid_constant__ CUtensorMap tm_blo, int K, EpiParams ep) {
+                       const __grid_constant__ CUtensorMap tm_blo, int K, int kc_blocks,
+                       EpiParams ep) {
   using C = Cfg<CG>;
   using namespace ptx;
 
@@ -87,8 +97,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* full_bar = bars;                        // [kStages]
   uint64_t* empty_bar = bars + C::kStages;          // [kStages]
-  uint64_t* tfull_bar = bars + 2 * C::kStages;      // [2]
-  uint64_t* tempty_bar = bars + 2 * C::kStages + 2; // [2]
+  uint64_t* cfull_bar = bars + 2 * C::kStages;      // [2] chunk accumulated
+  uint64_t* cempty_bar = bars + 2 * C::kStages + 2; // [2] chunk drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * C::kStages + 4);
 
   const int warp = threadIdx.x / 32;
@@ -102,6 +112,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   const int unit = blockIdx.x / CG;
   const int num_units = gridDim.x / CG;
   const int num_kb = (K + C::kBK - 1) / C::kBK;
+  const int num_chunks = (num_kb + kc_blocks - 1) / kc_blocks;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -109,8 +120,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       mbar_init(smem_u32(&empty_bar[s]), 1);
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(smem_u32(&tfull_bar[a]), 1);
-      mbar_init(smem_u32(&tempty_bar[a]), 4 * CG);
+      mbar_init(smem_u32(&cfull_bar[a]), 1);
+      mbar_init(smem_u32(&cempty_bar[a]), C::kEpiWarps * CG);
     }
     fence_barrier_init();
     prefetch_tmap(&tm_ahi);
@@ -129,6 +140,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      const uint64_t pol = policy_evict_last();
       for (int t = unit; t < total_tiles; t += num_units) {
         int mt, nt;
         tile_coords<CG>(t, tiles_m, tiles_n, mt, nt);
@@ -141,7 +153,6 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           const int kx = kb * C::kBK;
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(fb, C::kStageBytes);
-            const uint64_t pol = policy_evict_last();
             tma_load_2d(&tm_ahi, smem_u32(st), fb, kx, arow, pol);
             tma_load_2d(&tm_alo, smem_u32(st + C::kTileBytes), fb, kx, arow, pol);
             tma_load_2d(&tm_bhi, smem_u32(st + 2 * C::kTileBytes), fb, kx, brow, pol);
@@ -151,7 +162,6 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             uint32_t fb_leader;
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb_leader) : "r"(fb));
             if (leader) mbar_arrive_expect_tx(fb, 2 * C::kStageBytes);
-            const uint64_t pol = policy_evict_last();
             tma_load_2d_cg2(&tm_ahi, smem_u32(st), fb_leader, kx, arow, pol);
             tma_load_2d_cg2(&tm_alo, smem_u32(st + C::kTileBytes), fb_leader, kx, arow, pol);
             tma_load_2d_cg2(&tm_bhi, smem_u32(st + 2 * C::kTileBytes), fb_leader, kx, brow, pol);
@@ -167,98 +177,109 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       constexpr uint32_t idesc = idesc_tf32(C::kUmmaM, C::kUmmaN);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = unit; t < total_tiles; t += num_units, ++it) {
-        const int acc = it & 1;
-        const uint32_t aphase = (it >> 1) & 1;
-        mbar_wait(smem_u32(&tempty_bar[acc]), aphase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * C::kAccCols);
-        for (int kb = 0; kb < num_kb; ++kb) {
-          mbar_wait(smem_u32(&full_bar[stage]), phase);
+      uint32_t chunk_ctr = 0;
+      for (int t = unit; t < total_tiles; t += num_units) {
+        for (int ch = 0; ch < num_chunks; ++ch, ++chunk_ctr) {
+          const int buf = chunk_ctr & 1;
+          mbar_wait(smem_u32(&cempty_bar[buf]), ((chunk_ctr >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t s0 = smem_u32(smem + stage * C::kStageBytes);
-          const uint64_t ahi = sdesc_k_sw128(s0);
-          const uint64_t alo = sdesc_k_sw128(s0 + C::kTileBytes);
-          const uint64_t bhi = sdesc_k_sw128(s0 + 2 * C::kTileBytes);
-          const uint64_t blo = sdesc_k_sw128(s0 + 3 * C::kTileBytes);
+          const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * C::kAccCols);
+          const int kb0 = ch * kc_blocks;
+          const int kb1 = min(num_kb, kb0 + kc_blocks);
+          for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(smem_u32(&full_bar[stage]), phase);
+            tc_fence_after();
+            const uint32_t s0 = smem_u32(smem + stage * C::kStageBytes);
+            const uint64_t ahi = sdesc_k_sw128(s0);
+            const uint64_t alo = sdesc_k_sw128(s0 + C::kTileBytes);
+            const uint64_t bhi = sdesc_k_sw128(s0 + 2 * C::kTileBytes);
+            const uint64_t blo = sdesc_k_sw128(s0 + 3 * C::kTileBytes);
 #pragma unroll
-          for (int j = 0; j < C::kBK / 8; ++j) {
-            // advance 8 tf32 = 32 B along K inside the swizzle row (16-B units)
-            const uint64_t off = static_cast<uint64_t>(j * 2);
-            mma_tf32<CG>(d_tmem, alo + off, bhi + off, idesc, (kb | j) != 0);
-            mma_tf32<CG>(d_tmem, ahi + off, blo + off, idesc, 1u);
-            mma_tf32<CG>(d_tmem, ahi + off, bhi + off, idesc, 1u);
+            for (int j = 0; j < C::kBK / 8; ++j) {
+              // advance 8 tf32 = 32 B along K inside the swizzle row (16-B units);
+              // small terms first, then hi*hi
+              const uint64_t off = static_cast<uint64_t>(j * 2);
+              mma_tf32<CG>(d_tmem, alo + off, bhi + off, idesc, (kb != kb0 || j != 0) ? 1u : 0u);
+              mma_tf32<CG>(d_tmem, ahi + off, blo + off, idesc, 1u);
+              mma_tf32<CG>(d_tmem, ahi + off, bhi + off, idesc, 1u);
+            }
+            if constexpr (CG == 1) mma_commit(smem_u32(&empty_bar[stage]));
+            else mma_commit_cg2(smem_u32(&empty_bar[stage]), 0x3);
+            if (++stage == C::kStages) { stage = 0; phase ^= 1; }
           }
-          if constexpr (CG == 1) mma_commit(smem_u32(&empty_bar[stage]));
-          else mma_commit_cg2(smem_u32(&empty_bar[stage]), 0x3);
-          if (++stage == C::kStages) { stage = 0; phase ^= 1; }
+          if constexpr (CG == 1) mma_commit(smem_u32(&cfull_bar[buf]));
+          else mma_commit_cg2(smem_u32(&cfull_bar[buf]), 0x3);
         }
-        if constexpr (CG == 1) mma_commit(smem_u32(&tfull_bar[acc]));
-        else mma_commit_cg2(smem_u32(&tfull_bar[acc]), 0x3);
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int q = warp % 4;  // TMEM lane quadrant this warp may access
-    int it = 0;
-    for (int t = unit; t < total_tiles; t += num_units, ++it) {
+    const int e = warp - 2;
+    const int q = warp % 4;           // TMEM lane quadrant this warp may access
+    const int half = e / 4;           // which half of the accumulator columns
+    const int col_off = half * C::kColsPerThread;
+    const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
+    uint32_t chunk_ctr = 0;
+    for (int t = unit; t < total_tiles; t += num_units) {
       int mt, nt;
       tile_coords<CG>(t, tiles_m, tiles_n, mt, nt);
-      const int acc = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
-      mbar_wait(smem_u32(&tfull_bar[acc]), aphase);
-      tc_fence_after();
+      float master[C::kColsPerThread];
+#pragma unroll
+      for (int j = 0; j < C::kColsPerThread; ++j) master[j] = 0.0f;
+      for (int ch = 0; ch < num_chunks; ++ch, ++chunk_ctr) {
+        const int buf = chunk_ctr & 1;
+        mbar_wait(smem_u32(&cfull_bar[buf]), (chunk_ctr >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * C::kAccCols + col_off) + lane_addr;
+#pragma unroll
+        for (int g = 0; g < C::kColsPerThread / 16; ++g) {
+          uint32_t v[16];
+          tmem_ld_32x32b_x16(taddr + static_cast<uint32_t>(g * 16), v);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) master[g * 16 + j] = __fadd_rn(master[g * 16 + j], __uint_as_float(v[j]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) mbar_arrive(smem_u32(&cempty_bar[buf]));
+          else mbar_arrive_cluster(smem_u32(&cempty_bar[buf]), 0);
+        }
+      }
+      // alpha / beta epilogue straight from the master registers
       const int row = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta + q * 32 +
                       static_cast<int>(lane);
-      const int col_base = nt * C::kUmmaN;
-      const bool row_ok = row < ep.m;
-      float* crow = ep.c + static_cast<int64_t>(row) * ep.ldc;
-      const bool vec_ok =
-          ((ep.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(ep.c) & 15) == 0);
-#pragma unroll 1
-      for (int ch = 0; ch < C::kAccCols / 32; ++ch) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem_base + static_cast<uint32_t>(acc * C::kAccCols + ch * 32) +
-                               (static_cast<uint32_t>(q * 32) << 16),
-                           v);
-        tmem_ld_wait();
-        const int c0 = col_base + ch * 32;
-        if (!row_ok || c0 >= ep.n) continue;
-        if (vec_ok && c0 + 32 <= ep.n) {
-          float4* dst = reinterpret_cast<float4*>(crow + c0);
+      if (row >= ep.m) continue;
+      const int c0 = nt * C::kUmmaN + col_off;
+      float* crow = ep.c + static_cast<int64_t>(row) * ep.ldc + c0;
+      const bool vec_ok = ((ep.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(ep.c) & 15) == 0);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 o;
-            o.x = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 0]));
-            o.y = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 1]));
-            o.z = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 2]));
-            o.w = __fmul_rn(ep.alpha, __uint_as_float(v[4 * j + 3]));
-            if (ep.read_c) {
-              const float4 cv = dst[j];
-              o.x = __fadd_rn(o.x, __fmul_rn(ep.beta, cv.x));
-              o.y = __fadd_rn(o.y, __fmul_rn(ep.beta, cv.y));
-              o.z = __fadd_rn(o.z, __fmul_rn(ep.beta, cv.z));
-              o.w = __fadd_rn(o.w, __fmul_rn(ep.beta, cv.w));
-            }
-            dst[j] = o;
+      for (int j = 0; j < C::kColsPerThread / 4; ++j) {
+        const int cc = c0 + 4 * j;
+        if (cc >= ep.n) break;
+        float o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[u] = __fmul_rn(ep.alpha, master[4 * j + u]);
+        if (vec_ok && cc + 4 <= ep.n) {
+          float4* dst = reinterpret_cast<float4*>(crow + 4 * j);
+          if (ep.read_c) {
+            const float4 cv = *dst;
+            o[0] = __fadd_rn(o[0], __fmul_rn(ep.beta, cv.x));
+            o[1] = __fadd_rn(o[1], __fmul_rn(ep.beta, cv.y));
+            o[2] = __fadd_rn(o[2], __fmul_rn(ep.beta, cv.z));
+            o[3] = __fadd_rn(o[3], __fmul_rn(ep.beta, cv.w));
           }
+          *dst = make_float4(o[0], o[1], o[2], o[3]);
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            if (c0 + j < ep.n) {
-              float o = __fmul_rn(ep.alpha, __uint_as_float(v[j]));
-              if (ep.read_c) o = __fadd_rn(o, __fmul_rn(ep.beta, crow[c0 + j]));
-              crow[c0 + j] = o;
+          for (int u = 0; u < 4; ++u) {
+            if (cc + u < ep.n) {
+              float v = o[u];
+              if (ep.read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, crow[4 * j + u]));
+              crow[4 * j + u] = v;
             }
           }
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 1) mbar_arrive(smem_u32(&tempty_bar[acc]));
-        else mbar_arrive_cluster(smem_u32(&tempty_bar[acc]), 0);
       }
     }
   }
@@ -357,8 +378,9 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const int kc_blocks = a.flush_k > 0 ? static_cast<int>((a.flush_k + C::kBK - 1) / C::kBK) : 8;
   return cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG>, maps[0], maps[1], maps[2], maps[3],
-                            static_cast<int>(a.k), ep);
+                            static_cast<int>(a.k), kc_blocks, ep);
 }
 
 }  // namespace

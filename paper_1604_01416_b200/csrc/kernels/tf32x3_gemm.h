@@ -25,6 +25,7 @@ struct Tf32x3Args {
   int read_c = 0;
   int cta_group = 0;  // 0 = auto, 1 = single-CTA 128x128 tiles, 2 = CTA-pair 256x256 tiles
   int num_sms = 0;    // 0 = all SMs of the current device
+  int64_t flush_k = 0;  // K per TMEM accumulation chunk (0 = default 256)
 };
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);

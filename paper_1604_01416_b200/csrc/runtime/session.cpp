@@ -580,6 +580,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   const float beta = static_cast<float>(g.beta);
   const bool read_c0 = g.beta != 0.0;  // kernels.hpp:69-71: beta == 0 never reads C
   const int cta_group = static_cast<int>(env_int("DM_CTA_GROUP", 0));
+  const std::int64_t flush_k = env_int("DM_FLUSH_K", 0);
 
   for (auto& wp : workers_) {
     if (!wp) continue;
@@ -658,6 +659,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         a.beta = p == 0 ? beta : 1.0f;
         a.read_c = p == 0 ? (read_c0 ? 1 : 0) : 1;
         a.cta_group = cta_group;
+        a.flush_k = flush_k;
         record_timing(w, true);
         cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");
         record_timing(w, false);

@@ -74,6 +74,9 @@ def test_k_zero_scales_c(cuda):
 
 
 @pytest.mark.parametrize("cg", [1, 2])
-def test_large_k_accuracy(cuda, cg):
-    """K=16384: fp32-level accuracy (1xTF32 would sit near 2.5e-4)."""
-    assert _run(cuda, 512, 512, 16384, False, False, 1.0, 0.0, cg, seed=7) <= 2e-6
+@pytest.mark.parametrize("k", [16384, 32768])
+def test_large_k_accuracy(cuda, cg, k):
+    """fp32-level accuracy at the BASELINE K (1xTF32 sits near 2.5e-4; a single
+    truncating TMEM accumulator near 1e-4).  The reference's own fp32
+    k-ascending loop is ~3e-6 from exact at K=32768."""
+    assert _run(cuda, 512, 512, k, False, False, 1.0, 0.0, cg, seed=7) <= 3e-6
