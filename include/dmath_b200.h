@@ -184,6 +184,10 @@ int dm_descriptor_digest(dm_session* s, uint64_t* master, uint64_t* workers, int
 int dm_block_device_ptr(dm_session* s, dm_matrix_id id, int row, int col, void** ptr,
                         int* device);
 int dm_barrier(dm_session* s);
+/* Device-time markers on worker `worker`'s GEMM stream (bench timing):
+ * record CUDA event `slot` (0..15); elapsed ms between two recorded slots. */
+int dm_marker_record(dm_session* s, int worker, int slot);
+int dm_marker_elapsed(dm_session* s, int worker, int slot_a, int slot_b, float* ms);
 
 /* ---- the per-worker BLAS seam: local_gemm (kernels.hpp:81-89) on device
  * memory.  op(A) is m x k (A stored k x m when trans_a), op(B) is k x n (B

@@ -369,6 +369,14 @@ int dm_block_device_ptr(dm_session* s, dm_matrix_id id, int row, int col, void**
 
 int dm_barrier(dm_session* s) { return guarded([&] { S(s).barrier(); }); }
 
+int dm_marker_record(dm_session* s, int worker, int slot) {
+  return guarded([&] { S(s).marker_record(worker, slot); });
+}
+
+int dm_marker_elapsed(dm_session* s, int worker, int slot_a, int slot_b, float* ms) {
+  return guarded([&] { *ms = S(s).marker_elapsed(worker, slot_a, slot_b); });
+}
+
 int dm_local_gemm_f32(double alpha, const float* a, int64_t lda, int ta, const float* b,
                       int64_t ldb, int tb, double beta, float* c, int64_t ldc, int64_t m,
                       int64_t n, int64_t k, void* stream) {

@@ -109,6 +109,8 @@ Session::~Session() {
       cudaEventDestroy(a);
       cudaEventDestroy(b);
     }
+    for (cudaEvent_t e : w->markers)
+      if (e) cudaEventDestroy(e);
     w->owned.clear();
     w->cache.clear();
     w->pool.reset();
@@ -210,6 +212,25 @@ void Session::end_command() {
 void Session::barrier() {
   sync_local();
   if (comm_) comm_->barrier();
+}
+
+void Session::marker_record(int w, int slot) {
+  Worker& wk = worker(w);
+  if (slot < 0 || slot >= 16) throw UsageError("marker slot out of range");
+  DeviceGuard g(wk.device);
+  if (!wk.markers[slot]) cuda_check(cudaEventCreate(&wk.markers[slot]), "cudaEventCreate");
+  cuda_check(cudaEventRecord(wk.markers[slot], wk.stream), "cudaEventRecord");
+}
+
+float Session::marker_elapsed(int w, int a, int b) {
+  Worker& wk = worker(w);
+  if (a < 0 || a >= 16 || b < 0 || b >= 16 || !wk.markers[a] || !wk.markers[b])
+    throw UsageError("marker slot not recorded");
+  DeviceGuard g(wk.device);
+  cuda_check(cudaEventSynchronize(wk.markers[b]), "cudaEventSynchronize");
+  float ms = 0;
+  cuda_check(cudaEventElapsedTime(&ms, wk.markers[a], wk.markers[b]), "cudaEventElapsedTime");
+  return ms;
 }
 
 // --------------------------------------------------------------- matrices

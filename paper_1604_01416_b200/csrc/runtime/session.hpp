@@ -67,6 +67,7 @@ struct Worker {
   std::uint64_t seed = 0;
   dm_worker_stats stats{};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_events;
+  cudaEvent_t markers[16] = {};
   std::size_t timing_used = 0;
 };
 
@@ -107,6 +108,8 @@ class Session {
   std::vector<std::uint64_t> worker_digests() const;
   void* block_device_ptr(MatrixId id, BlockCoord c, int* device) const;
   void barrier();
+  void marker_record(int w, int slot);
+  float marker_elapsed(int w, int a, int b);
 
  private:
   struct Piece {

@@ -303,6 +303,15 @@ class Session:
     def barrier(self):
         _check(lib.dm_barrier(self._h))
 
+    def marker_record(self, worker: int, slot: int):
+        """Record device-time marker `slot` on the worker's GEMM stream."""
+        _check(lib.dm_marker_record(self._h, worker, slot))
+
+    def marker_elapsed(self, worker: int, a: int, b: int) -> float:
+        ms = C.c_float()
+        _check(lib.dm_marker_elapsed(self._h, worker, a, b, C.byref(ms)))
+        return ms.value
+
     # -- matrices
     def create_matrix(self, layout: LayoutSpec, precision=Precision.Single32,
                       fill=FillKind.Zeros, host: Optional[np.ndarray] = None) -> int:
