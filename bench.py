@@ -195,12 +195,23 @@ def run_ours(args):
     # ---- end to end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        hA = torch.empty((N, N), dtype=torch.float32, pin_memory=True).numpy()
-        hB = torch.empty((N, N), dtype=torch.float32, pin_memory=True).numpy()
-        hC = torch.empty((N, N), dtype=torch.float32, pin_memory=True).numpy()
-        rng = np.random.default_rng(rank)
-        hA[:] = rng.random((N, N), dtype=np.float32)
-        hB[:] = rng.random((N, N), dtype=np.float32)
+        # Pinned host operands.  Every rank copies only its own blocks, so at
+        # N > 1 only the rank's block-row band of each host matrix is touched
+        # and page-locked (cudaHostRegister); at N = 1 the whole matrix is.
+        r_lo, r_hi = (me // pc) * (N // pr), (me // pc + 1) * (N // pr)
+        cudart = torch.cuda.cudart()
+
+        def host_matrix(fill_seed):
+            h = np.empty((N, N), dtype=np.float32)
+            band = h[r_lo:r_hi]
+            rc = cudart.cudaHostRegister(band.ctypes.data, band.nbytes, 0)
+            if int(rc) != 0:
+                raise RuntimeError(f"cudaHostRegister failed: {rc}")
+            if fill_seed is not None:
+                band[:] = np.random.default_rng(fill_seed).random(band.shape, dtype=np.float32)
+            return h, band
+
+        (hA, bA), (hB, bB), (hC, bC) = host_matrix(rank), host_matrix(rank + 1000), host_matrix(None)
         root = -1 if world > 1 else 0
         s.scatter(a, hA)
         s.scatter(b, hB)
@@ -222,6 +233,8 @@ def run_ours(args):
                "h2d_bytes_per_step": 2 * blk * world, "d2h_bytes_per_step": blk * world,
                "ms_per_step": e2e_ms / args.steps,
                "path": "Session.scatter(A,B from pinned host) + general_gemm + gather(C to pinned host)"}
+        for band in (bA, bB, bC):
+            cudart.cudaHostUnregister(band.ctypes.data)
         del hA, hB, hC
 
     # ---- CPU baseline + full-size sampled parity (rank 0 at N=1 only)

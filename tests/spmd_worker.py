@@ -1,0 +1,126 @@
+"""One rank of an SPMD (one process per GPU) parity run; launched by
+tests/test_gpu_spmd.py through torch.distributed.run.  Every rank issues the
+same calls in the same order (the reference's single global command order,
+session.hpp:585-605); rank 0 checks results against the pinned oracle.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_1604_01416_b200 as dm  # noqa: E402
+from oracle import COracle  # noqa: E402
+
+GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    obj = [dm.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    orc = COracle()
+    results = {}
+
+    def session(seed):
+        return dm.Session(dm.Config(worker_count=world, root_seed=seed, mode="spmd", rank=rank,
+                                    devices=[local], nccl_id=obj[0]))
+
+    # 1. checkerboard SUMMA-pull general_gemm, alpha/beta, all transposes
+    s = session(42)
+    pr, pc = dm.checkerboard_dims(world)
+    n = 1536
+    lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // pr, n // pc, world)
+    a, b, c = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(3))
+    A, B, C0 = s.gather(a), s.gather(b), s.gather(c)   # root 0 assembles (others untouched)
+    for trans in range(4):
+        ta, tb = bool(trans & 1), bool(trans & 2)
+        s.general_gemm(1.5, a, b, -0.5, c, ta, tb)
+        got = s.gather(c)
+        if rank == 0:
+            want = orc.local_gemm(1.5, A, ta, B, tb, -0.5, C0)
+            results[f"general_t{trans}"] = orc.rel_frobenius(got, want)
+            C0 = got  # next GEMM reads this C
+        else:
+            C0 = None
+        st = s.worker_stats(rank)
+        results[f"peer_bytes_r{rank}_t{trans}"] = int(st.peer_bytes_read)
+        s.reset_worker_stats()
+    # inputs bit-exact with the reference's seeded fill (same layout, same ids)
+    if rank == 0:
+        results["A_bitexact"] = bool(A.tobytes() == orc.seeded_matrix(42, 1, 3, n, n, n // pr, n // pc).tobytes())
+    # root=-1: every rank writes its own blocks
+    own = np.zeros((n, n), np.float32)
+    s.gather(a, own, root=-1)
+    full = orc.seeded_matrix(42, 1, 3, n, n, n // pr, n // pc)
+    mask = np.zeros((n, n), bool)
+    for r in range(pr):
+        for cc in range(pc):
+            if lay.owner(r, cc) == rank:
+                mask[r * (n // pr):(r + 1) * (n // pr), cc * (n // pc):(cc + 1) * (n // pc)] = True
+    results[f"own_blocks_r{rank}"] = bool(np.array_equal(own[mask], full[mask]))
+    s.close()
+
+    # 2. golden sweep cases with this worker count (general + cyclic)
+    cases = [g for g in GOLDEN["sweep"] if g["workers"] == world][:12]
+    worst = 0.0
+    for case in cases:
+        s = session(case["root_seed"])
+        ma = s.create_matrix(dm.make_layout(*case["la"]), fill=dm.FillKind.SeededRandom)
+        mb = s.create_matrix(dm.make_layout(*case["lb"]), fill=dm.FillKind.SeededRandom)
+        mc = s.create_matrix(dm.make_layout(*case["lc"]), fill=dm.FillKind.SeededRandom)
+        A, B, C0 = s.gather(ma), s.gather(mb), s.gather(mc)
+        if case["op"] == "general":
+            s.general_gemm(case["alpha"], ma, mb, case["beta"], mc, case["ta"], case["tb"])
+        else:
+            s.cyclic_gemm(case["alpha"], ma, mb, case["beta"], mc, case["ta"], case["tb"], False)
+        got = s.gather(mc)
+        if rank == 0:
+            assert f"{orc.fnv1a(A):016x}" == case["A"]
+            want = orc.local_gemm(case["alpha"], A, case["ta"], B, case["tb"], case["beta"], C0)
+            assert f"{orc.fnv1a(want):016x}" == case["C"]
+            worst = max(worst, orc.rel_frobenius(got, want))
+        s.close()
+    results["sweep_cases"] = len(cases)
+    results["sweep_worst"] = worst
+
+    # 3. FC: cyclic fwd with cache, cached backward (zero peer bytes)
+    s = session(3)
+    fin, fout, batch = 96 * world, 64, 16 * world
+    strip = batch // world
+    W = s.create_matrix(dm.make_layout(0, fin, fout, fin // world, fout, world), fill=dm.FillKind.SeededRandom)
+    X = s.create_matrix(dm.make_layout(1, fin, batch, fin, strip, world), fill=dm.FillKind.SeededRandom)
+    Y = s.create_matrix(dm.make_layout(1, fout, batch, fout, strip, world))
+    dY = s.create_matrix(dm.make_layout(1, fout, batch, fout, strip, world), fill=dm.FillKind.SeededRandom)
+    dX = s.create_matrix(dm.make_layout(1, fin, batch, fin, strip, world))
+    Wh, Xh, dYh = s.gather(W), s.gather(X), s.gather(dY)
+    s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+    Yh = s.gather(Y)
+    s.reset_worker_stats()
+    s.cached_backward_gemm(W, dY, dX)
+    results[f"bwd_peer_bytes_r{rank}"] = int(s.worker_stats(rank).peer_bytes_read)
+    dXh = s.gather(dX)
+    if rank == 0:
+        results["fc_fwd"] = orc.rel_frobenius(Yh, orc.local_gemm(1.0, Wh, True, Xh, False, 0.0))
+        results["fc_bwd"] = orc.rel_frobenius(dXh, orc.local_gemm(1.0, Wh, False, dYh, False, 0.0))
+    s.close()
+
+    allres = [None] * world
+    dist.all_gather_object(allres, results)
+    if rank == 0:
+        merged = {}
+        for r in allres:
+            merged.update(r)
+        print("SPMD_RESULTS " + json.dumps(merged), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
