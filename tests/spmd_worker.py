@@ -24,12 +24,13 @@ def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
-    obj = [dm.nccl_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(obj, src=0)
     orc = COracle()
     results = {}
 
     def session(seed):
+        # an NCCL unique id initialises exactly one communicator: fresh id per session
+        obj = [dm.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
         return dm.Session(dm.Config(worker_count=world, root_seed=seed, mode="spmd", rank=rank,
                                     devices=[local], nccl_id=obj[0]))
 

@@ -32,7 +32,7 @@ def test_spmd_parity(cuda):
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "spmd_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-6000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("SPMD_RESULTS ")][-1]
     res = json.loads(line[len("SPMD_RESULTS "):])
     for t in range(4):
