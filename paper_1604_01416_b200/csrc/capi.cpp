@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <set>
@@ -54,6 +55,12 @@ dm::Session& S(dm_session* s) {
   return *s->impl;
 }
 
+int gemm_mode_from_env() {
+  const char* v = std::getenv("DM_GEMM_MODE");
+  if (v == nullptr || *v == 0) return dm::kModeMixed;
+  return std::atoi(v) == 0 ? dm::kModeTf32x3 : dm::kModeMixed;
+}
+
 // Scratch for the stateless local_gemm seam: one pool per device.
 dm::DevicePool& seam_pool(int dev) {
   static std::mutex mu;
@@ -77,24 +84,43 @@ int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const flo
     int dev = 0;
     dm::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     dm::DevicePool& pool = seam_pool(dev);
-    const int64_t kp = std::max<int64_t>(4, (k + 3) / 4 * 4);
+    const int mode = gemm_mode_from_env();
+    const int64_t kp = std::max<int64_t>(8, (k + 7) / 8 * 8);
     dm::DeviceBuffer ah, al, bh, bl;
     if (k > 0 && m > 0 && n > 0) {
+      // tf32x3: hi/lo fp32 planes; mixed: fp32 hi + two bf16 planes (same 8 B/elem)
       ah = pool.acquire(static_cast<size_t>(m * kp) * 4);
       al = pool.acquire(static_cast<size_t>(m * kp) * 4);
       bh = pool.acquire(static_cast<size_t>(n * kp) * 4);
       bl = pool.acquire(static_cast<size_t>(n * kp) * 4);
-      dm::cuda_check(dm::split_tf32(a, lda, ta, m, k, ah.f32(), al.f32(), kp, st), "split A");
-      dm::cuda_check(dm::split_tf32(b, ldb, tb ? 0 : 1, n, k, bh.f32(), bl.f32(), kp, st),
-                     "split B");
     }
     dm::Tf32x3Args args;
+    args.mode = mode;
     args.a_hi = ah.f32();
-    args.a_lo = al.f32();
-    args.lda = kp;
     args.b_hi = bh.f32();
-    args.b_lo = bl.f32();
+    args.lda = kp;
     args.ldb = kp;
+    if (mode == dm::kModeMixed) {
+      args.a_hi16 = al.f32();
+      args.a_lo16 = static_cast<const char*>(al.data()) + m * kp * 2;
+      args.b_hi16 = bl.f32();
+      args.b_lo16 = static_cast<const char*>(bl.data()) + n * kp * 2;
+      args.lda16 = kp;
+      args.ldb16 = kp;
+    } else {
+      args.a_lo = al.f32();
+      args.b_lo = bl.f32();
+    }
+    if (k > 0 && m > 0 && n > 0) {
+      dm::cuda_check(dm::split_tf32(a, lda, ta, m, k, ah.f32(), const_cast<float*>(args.a_lo), kp,
+                                    const_cast<void*>(args.a_hi16), const_cast<void*>(args.a_lo16),
+                                    kp, st),
+                     "split A");
+      dm::cuda_check(dm::split_tf32(b, ldb, tb ? 0 : 1, n, k, bh.f32(), const_cast<float*>(args.b_lo),
+                                    kp, const_cast<void*>(args.b_hi16),
+                                    const_cast<void*>(args.b_lo16), kp, st),
+                     "split B");
+    }
     args.c = c;
     args.ldc = ldc;
     args.m = m;

@@ -8,6 +8,7 @@
 // fill_seeded: bit-exact device restatement of WorkerContext::fill_seeded
 //   (runtime_types.hpp:208-218) using mix64 / u64_to_unit_double
 //   (common.hpp:107-121).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,10 +25,23 @@ __device__ __forceinline__ float tf32_rne(float x) {
   return __uint_as_float(u & 0xFFFFE000u);
 }
 
-__device__ __forceinline__ void split_store(float x, float* hi, float* lo, int64_t idx) {
+struct Planes {
+  float* hi;
+  float* lo;            // tf32 lo (kModeTf32x3) or null
+  __nv_bfloat16* hi16;  // bf16(hi) (kModeMixed) or null
+  __nv_bfloat16* lo16;
+  int64_t ldo, ldo16;
+};
+
+__device__ __forceinline__ void split_store(float x, const Planes& p, int64_t r, int64_t k) {
   const float h = tf32_rne(x);
-  hi[idx] = h;
-  lo[idx] = tf32_rne(x - h);
+  const float l = x - h;  // exact
+  p.hi[r * p.ldo + k] = h;
+  if (p.lo) p.lo[r * p.ldo + k] = tf32_rne(l);
+  if (p.hi16) {
+    p.hi16[r * p.ldo16 + k] = __float2bfloat16_rn(h);
+    p.lo16[r * p.ldo16 + k] = __float2bfloat16_rn(l);
+  }
 }
 
 constexpr int kT = 32;  // tile edge
@@ -35,21 +49,19 @@ constexpr int kRowsPerPass = 8;
 
 // One 32x32 output tile per block (32 x 8 threads).
 __global__ void split_direct_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
-                                    int64_t kcols, float* __restrict__ hi, float* __restrict__ lo,
-                                    int64_t ldo) {
+                                    int64_t kcols, Planes p) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kT;
   if (k >= kcols) return;
 #pragma unroll
   for (int i = 0; i < kT; i += kRowsPerPass) {
     const int64_t r = r0 + threadIdx.y + i;
-    if (r < rows) split_store(__ldg(src + r * lds + k), hi, lo, r * ldo + k);
+    if (r < rows) split_store(__ldg(src + r * lds + k), p, r, k);
   }
 }
 
 __global__ void split_trans_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
-                                   int64_t kcols, float* __restrict__ hi, float* __restrict__ lo,
-                                   int64_t ldo) {
+                                   int64_t kcols, Planes p) {
   __shared__ float tile[kT][kT + 1];
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kT;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kT;
@@ -64,7 +76,7 @@ __global__ void split_trans_kernel(const float* __restrict__ src, int64_t lds, i
 #pragma unroll
   for (int i = 0; i < kT; i += kRowsPerPass) {
     const int64_t r = r0 + threadIdx.y + i, k = k0 + threadIdx.x;
-    if (k < kcols && r < rows) split_store(tile[threadIdx.x][threadIdx.y + i], hi, lo, r * ldo + k);
+    if (k < kcols && r < rows) split_store(tile[threadIdx.x][threadIdx.y + i], p, r, k);
   }
 }
 
@@ -87,13 +99,15 @@ __global__ void fill_seeded_kernel(float* __restrict__ dst, int64_t count, uint6
 }  // namespace
 
 cudaError_t split_tf32(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols,
-                       float* hi, float* lo, int64_t ldo, cudaStream_t stream) {
+                       float* hi, float* lo, int64_t ldo, void* hi16, void* lo16, int64_t ldo16,
+                       cudaStream_t stream) {
   if (rows <= 0 || kcols <= 0) return cudaSuccess;
+  Planes p{hi, lo, static_cast<__nv_bfloat16*>(hi16), static_cast<__nv_bfloat16*>(lo16), ldo, ldo16};
   dim3 block(kT, kRowsPerPass);
   dim3 grid(static_cast<unsigned>((kcols + kT - 1) / kT), static_cast<unsigned>((rows + kT - 1) / kT));
   if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
-  if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, hi, lo, ldo);
-  else split_direct_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, hi, lo, ldo);
+  if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, p);
+  else split_direct_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, p);
   return cudaGetLastError();
 }
 

@@ -80,13 +80,18 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 // therefore cut into chunks of `kc_blocks` k-blocks: each chunk accumulates in
 // a fresh TMEM buffer and the epilogue warps fold it into an fp32 register
 // master with round-to-nearest adds, making the error K-independent.
-template <int CG>
+// Stage layout (per CTA, 64 KB):
+//   kModeTf32x3: [A_hi f32 16K | A_lo f32 16K | B_hi f32 16K | B_lo f32 16K]     (128B swizzle)
+//   kModeMixed : [A_hi f32 16K | B_hi f32 16K | A_hi bf16 8K | A_lo bf16 8K |
+//                 B_hi bf16 8K | B_lo bf16 8K]          (f32: 128B swizzle, bf16: 64B swizzle)
+// The tensor-map array is in that order.
+struct Maps {
+  CUtensorMap m[6];
+};
+
+template <int CG, int MODE>
 __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
-    tf32x3_gemm_kernel(const __grid_constant__ CUtensorMap tm_ahi,
-                       const __grid_constant__ CUtensorMap tm_alo,
-                       const __grid_constant__ CUtensorMap tm_bhi,
-                       const __grid_constant__ CUtensorMap tm_blo, int K, int kc_blocks,
-                       EpiParams ep) {
+    tf32x3_gemm_kernel(const __grid_constant__ Maps maps, int K, int kc_blocks, EpiParams ep) {
   using C = Cfg<CG>;
   using namespace ptx;
 
@@ -124,10 +129,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       mbar_init(smem_u32(&cempty_bar[a]), C::kEpiWarps * CG);
     }
     fence_barrier_init();
-    prefetch_tmap(&tm_ahi);
-    prefetch_tmap(&tm_alo);
-    prefetch_tmap(&tm_bhi);
-    prefetch_tmap(&tm_blo);
+    for (int i = 0; i < (MODE == kModeMixed ? 6 : 4); ++i) prefetch_tmap(&maps.m[i]);
   }
   if (warp == 1) tmem_alloc<CG>(smem_u32(tmem_slot), C::kTmemCols);
   tc_fence_before();
@@ -151,21 +153,27 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           uint8_t* st = smem + stage * C::kStageBytes;
           const uint32_t fb = smem_u32(&full_bar[stage]);
           const int kx = kb * C::kBK;
-          if constexpr (CG == 1) {
-            mbar_arrive_expect_tx(fb, C::kStageBytes);
-            tma_load_2d(&tm_ahi, smem_u32(st), fb, kx, arow, pol);
-            tma_load_2d(&tm_alo, smem_u32(st + C::kTileBytes), fb, kx, arow, pol);
-            tma_load_2d(&tm_bhi, smem_u32(st + 2 * C::kTileBytes), fb, kx, brow, pol);
-            tma_load_2d(&tm_blo, smem_u32(st + 3 * C::kTileBytes), fb, kx, brow, pol);
+          uint32_t fb_tx = fb;  // barrier receiving the bytes (leader's for pairs)
+          if constexpr (CG == 2)
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb_tx) : "r"(fb));
+          if (leader) mbar_arrive_expect_tx(fb, CG * C::kStageBytes);
+          auto load = [&](int i, uint32_t off, int row) {
+            if constexpr (CG == 1) tma_load_2d(&maps.m[i], smem_u32(st + off), fb_tx, kx, row, pol);
+            else tma_load_2d_cg2(&maps.m[i], smem_u32(st + off), fb_tx, kx, row, pol);
+          };
+          if constexpr (MODE == kModeTf32x3) {
+            load(0, 0, arow);
+            load(1, C::kTileBytes, arow);
+            load(2, 2 * C::kTileBytes, brow);
+            load(3, 3 * C::kTileBytes, brow);
           } else {
-            // Completion bytes of both CTAs land on the leader's barrier.
-            uint32_t fb_leader;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb_leader) : "r"(fb));
-            if (leader) mbar_arrive_expect_tx(fb, 2 * C::kStageBytes);
-            tma_load_2d_cg2(&tm_ahi, smem_u32(st), fb_leader, kx, arow, pol);
-            tma_load_2d_cg2(&tm_alo, smem_u32(st + C::kTileBytes), fb_leader, kx, arow, pol);
-            tma_load_2d_cg2(&tm_bhi, smem_u32(st + 2 * C::kTileBytes), fb_leader, kx, brow, pol);
-            tma_load_2d_cg2(&tm_blo, smem_u32(st + 3 * C::kTileBytes), fb_leader, kx, brow, pol);
+            constexpr uint32_t h = C::kTileBytes / 2;  // bf16 tile: 128 rows x 64 B
+            load(0, 0, arow);
+            load(1, C::kTileBytes, brow);
+            load(2, 2 * C::kTileBytes, arow);
+            load(3, 2 * C::kTileBytes + h, arow);
+            load(4, 3 * C::kTileBytes, brow);
+            load(5, 3 * C::kTileBytes + h, brow);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
@@ -190,18 +198,40 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             mbar_wait(smem_u32(&full_bar[stage]), phase);
             tc_fence_after();
             const uint32_t s0 = smem_u32(smem + stage * C::kStageBytes);
-            const uint64_t ahi = sdesc_k_sw128(s0);
-            const uint64_t alo = sdesc_k_sw128(s0 + C::kTileBytes);
-            const uint64_t bhi = sdesc_k_sw128(s0 + 2 * C::kTileBytes);
-            const uint64_t blo = sdesc_k_sw128(s0 + 3 * C::kTileBytes);
+            const uint32_t acc0 = (kb != kb0) ? 1u : 0u;
+            if constexpr (MODE == kModeTf32x3) {
+              const uint64_t ahi = sdesc_k_sw128(s0);
+              const uint64_t alo = sdesc_k_sw128(s0 + C::kTileBytes);
+              const uint64_t bhi = sdesc_k_sw128(s0 + 2 * C::kTileBytes);
+              const uint64_t blo = sdesc_k_sw128(s0 + 3 * C::kTileBytes);
 #pragma unroll
-            for (int j = 0; j < C::kBK / 8; ++j) {
-              // advance 8 tf32 = 32 B along K inside the swizzle row (16-B units);
-              // small terms first, then hi*hi
-              const uint64_t off = static_cast<uint64_t>(j * 2);
-              mma_tf32<CG>(d_tmem, alo + off, bhi + off, idesc, (kb != kb0 || j != 0) ? 1u : 0u);
-              mma_tf32<CG>(d_tmem, ahi + off, blo + off, idesc, 1u);
-              mma_tf32<CG>(d_tmem, ahi + off, bhi + off, idesc, 1u);
+              for (int j = 0; j < C::kBK / 8; ++j) {
+                // advance 8 tf32 = 32 B along K inside the swizzle row (16-B units);
+                // small terms first, then hi*hi
+                const uint64_t off = static_cast<uint64_t>(j * 2);
+                mma_tf32<CG>(d_tmem, alo + off, bhi + off, idesc, (acc0 | j) != 0);
+                mma_tf32<CG>(d_tmem, ahi + off, blo + off, idesc, 1u);
+                mma_tf32<CG>(d_tmem, ahi + off, bhi + off, idesc, 1u);
+              }
+            } else {
+              constexpr uint32_t h = C::kTileBytes / 2;
+              constexpr uint32_t idesc16 = idesc_bf16(C::kUmmaM, C::kUmmaN);
+              const uint64_t ahi = sdesc_k_sw128(s0);
+              const uint64_t bhi = sdesc_k_sw128(s0 + C::kTileBytes);
+              const uint64_t ah16 = sdesc_k_sw64(s0 + 2 * C::kTileBytes);
+              const uint64_t al16 = sdesc_k_sw64(s0 + 2 * C::kTileBytes + h);
+              const uint64_t bh16 = sdesc_k_sw64(s0 + 3 * C::kTileBytes);
+              const uint64_t bl16 = sdesc_k_sw64(s0 + 3 * C::kTileBytes + h);
+#pragma unroll
+              for (int j = 0; j < C::kBK / 16; ++j) {
+                // bf16 cross terms for k16 step j (32 B along the 64-B row) ...
+                const uint64_t o16 = static_cast<uint64_t>(j * 2);
+                mma_bf16<CG>(d_tmem, ah16 + o16, bl16 + o16, idesc16, (acc0 | j) != 0);
+                mma_bf16<CG>(d_tmem, al16 + o16, bh16 + o16, idesc16, 1u);
+                // ... then hi*hi in tf32 for the same 16 k (two k8 MMAs)
+                mma_tf32<CG>(d_tmem, ahi + 4 * j, bhi + 4 * j, idesc, 1u);
+                mma_tf32<CG>(d_tmem, ahi + 4 * j + 2, bhi + 4 * j + 2, idesc, 1u);
+              }
             }
             if constexpr (CG == 1) mma_commit(smem_u32(&empty_bar[stage]));
             else mma_commit_cg2(smem_u32(&empty_bar[stage]), 0x3);
@@ -324,38 +354,53 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// K-major fp32 operand [rows x K] with row pitch `ld` elements; box 32 x 128.
-int make_operand_map(CUtensorMap* map, const float* base, int64_t rows, int64_t k, int64_t ld) {
+// K-major operand plane [rows x K] with row pitch `ld` elements; box 32 x 128
+// elements: fp32 with the 128-B swizzle, bf16 with the 64-B swizzle.
+int make_operand_map(CUtensorMap* map, const void* base, int64_t rows, int64_t k, int64_t ld,
+                     bool bf16) {
   EncodeTiledFn enc = encode_fn();
   if (enc == nullptr) return -1;
+  const int esz = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esz};
   cuuint32_t box[2] = {32, 128};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims,
-                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   2, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
-template <int CG>
+template <int CG, int MODE>
 cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   using C = Cfg<CG>;
-  CUtensorMap maps[4];
-  if (make_operand_map(&maps[0], a.a_hi, a.m, a.k, a.lda) != 0 ||
-      make_operand_map(&maps[1], a.a_lo, a.m, a.k, a.lda) != 0 ||
-      make_operand_map(&maps[2], a.b_hi, a.n, a.k, a.ldb) != 0 ||
-      make_operand_map(&maps[3], a.b_lo, a.n, a.k, a.ldb) != 0)
-    return cudaErrorInvalidValue;
-  static bool attr_set[2][64] = {};
+  Maps maps;
+  int bad = 0;
+  if constexpr (MODE == kModeTf32x3) {
+    bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false);
+    bad |= make_operand_map(&maps.m[1], a.a_lo, a.m, a.k, a.lda, false);
+    bad |= make_operand_map(&maps.m[2], a.b_hi, a.n, a.k, a.ldb, false);
+    bad |= make_operand_map(&maps.m[3], a.b_lo, a.n, a.k, a.ldb, false);
+  } else {
+    bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false);
+    bad |= make_operand_map(&maps.m[1], a.b_hi, a.n, a.k, a.ldb, false);
+    bad |= make_operand_map(&maps.m[2], a.a_hi16, a.m, a.k, a.lda16, true);
+    bad |= make_operand_map(&maps.m[3], a.a_lo16, a.m, a.k, a.lda16, true);
+    bad |= make_operand_map(&maps.m[4], a.b_hi16, a.n, a.k, a.ldb16, true);
+    bad |= make_operand_map(&maps.m[5], a.b_lo16, a.n, a.k, a.ldb16, true);
+  }
+  if (bad) return cudaErrorInvalidValue;
+  static bool attr_set[2][2][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!attr_set[CG - 1][dev & 63]) {
-    cudaError_t e = cudaFuncSetAttribute(tf32x3_gemm_kernel<CG>,
+  if (!attr_set[CG - 1][MODE][dev & 63]) {
+    cudaError_t e = cudaFuncSetAttribute(tf32x3_gemm_kernel<CG, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set[CG - 1][dev & 63] = true;
+    attr_set[CG - 1][MODE][dev & 63] = true;
   }
   int sms = a.num_sms;
   if (sms <= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -379,8 +424,8 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int kc_blocks = a.flush_k > 0 ? static_cast<int>((a.flush_k + C::kBK - 1) / C::kBK) : 8;
-  return cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG>, maps[0], maps[1], maps[2], maps[3],
-                            static_cast<int>(a.k), kc_blocks, ep);
+  return cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG, MODE>, maps, static_cast<int>(a.k),
+                            kc_blocks, ep);
 }
 
 }  // namespace
@@ -396,9 +441,11 @@ cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
     return cudaGetLastError();
   }
   // TMA needs 16-B aligned bases and pitches.
-  if ((a.lda & 3) || (a.ldb & 3) || (reinterpret_cast<uintptr_t>(a.a_hi) & 15) ||
-      (reinterpret_cast<uintptr_t>(a.a_lo) & 15) || (reinterpret_cast<uintptr_t>(a.b_hi) & 15) ||
-      (reinterpret_cast<uintptr_t>(a.b_lo) & 15))
+  auto mis = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) != 0; };
+  if ((a.lda & 3) || (a.ldb & 3) || mis(a.a_hi) || mis(a.b_hi)) return cudaErrorMisalignedAddress;
+  if (a.mode == kModeTf32x3 && (mis(a.a_lo) || mis(a.b_lo))) return cudaErrorMisalignedAddress;
+  if (a.mode == kModeMixed && ((a.lda16 & 7) || (a.ldb16 & 7) || mis(a.a_hi16) || mis(a.a_lo16) ||
+                               mis(a.b_hi16) || mis(a.b_lo16)))
     return cudaErrorMisalignedAddress;
   int cg = a.cta_group;
   if (cg == 0) {
@@ -406,7 +453,8 @@ cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
     const int64_t pair_tiles = ((a.m + 255) / 256) * ((a.n + 255) / 256);
     cg = pair_tiles >= 74 ? 2 : 1;
   }
-  return cg == 2 ? launch<2>(a, stream) : launch<1>(a, stream);
+  if (a.mode == kModeMixed) return cg == 2 ? launch<2, kModeMixed>(a, stream) : launch<1, kModeMixed>(a, stream);
+  return cg == 2 ? launch<2, kModeTf32x3>(a, stream) : launch<1, kModeTf32x3>(a, stream);
 }
 
 }  // namespace dm

@@ -7,17 +7,31 @@
 
 namespace dm {
 
+// Split-product modes.  Both keep fp32 accuracy:
+//   kModeTf32x3 : acc += lo*hi + hi*lo + hi*hi, three kind::tf32 MMAs per k8 step
+//   kModeMixed  : acc += hi*hi (kind::tf32) + bf16(hi)*bf16(lo) + bf16(lo)*bf16(hi)
+//                 (kind::f16, bf16 inputs): the cross terms are 2^-11 smaller than
+//                 the product and need only bf16's 8 bits; BF16 MMAs run at twice
+//                 the TF32 rate, so a k16 step costs 4 TF32-MMA slots instead of 6.
+constexpr int kModeTf32x3 = 0;
+constexpr int kModeMixed = 1;
+
 // C[m x n] (row pitch ldc) <- alpha * A B^T + beta * C, where A and B are
-// given as K-major tf32 hi/lo splits: A_{hi,lo} [m x k] pitch lda,
-// B_{hi,lo} [n x k] pitch ldb (i.e. op(B) transposed).  read_c == 0 means C
-// is never read (reference rule: beta == 0 ignores prior C contents).
+// given as K-major splits: A planes [m x k] (fp32 containers pitch lda, bf16
+// planes pitch lda16), B planes [n x k] (i.e. op(B) transposed).
+// read_c == 0 means C is never read (reference rule: beta == 0 ignores C).
 struct Tf32x3Args {
-  const float* a_hi = nullptr;
-  const float* a_lo = nullptr;
-  int64_t lda = 0;
+  const float* a_hi = nullptr;   // tf32-rounded hi (fp32 container)
+  const float* a_lo = nullptr;   // kModeTf32x3: tf32 lo
+  const void* a_hi16 = nullptr;  // kModeMixed: bf16(hi)
+  const void* a_lo16 = nullptr;  // kModeMixed: bf16(lo)
+  int64_t lda = 0, lda16 = 0;
   const float* b_hi = nullptr;
   const float* b_lo = nullptr;
-  int64_t ldb = 0;
+  const void* b_hi16 = nullptr;
+  const void* b_lo16 = nullptr;
+  int64_t ldb = 0, ldb16 = 0;
+  int mode = kModeTf32x3;
   float* c = nullptr;
   int64_t ldc = 0;
   int64_t m = 0, n = 0, k = 0;
@@ -30,11 +44,15 @@ struct Tf32x3Args {
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);
 
-// Elementwise split of a strided fp32 panel into K-major tf32 hi/lo planes:
-//   out[r][k] = trans ? src[k*lds + r] : src[r*lds + k],  r < rows, k < kcols
-// written at hi/lo + r*ldo + k.  `src` may be a peer-GPU (UVA) pointer.
+// Elementwise split of a strided fp32 panel into K-major planes:
+//   x[r][k] = trans ? src[k*lds + r] : src[r*lds + k],  r < rows, k < kcols
+//   hi = rn_tf32(x) at hi + r*ldo + k;   lo = x - hi rounded to tf32 (lo != null)
+//   and/or bf16(hi), bf16(lo) at hi16/lo16 + r*ldo16 + k (when non-null).
+// `src` may be a peer-GPU (UVA / IPC-mapped) pointer: the pull and the split are
+// one kernel.
 cudaError_t split_tf32(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols,
-                       float* hi, float* lo, int64_t ldo, cudaStream_t stream);
+                       float* hi, float* lo, int64_t ldo, void* hi16, void* lo16, int64_t ldo16,
+                       cudaStream_t stream);
 
 // Seeded synthetic fill, bit-exact with the reference's WorkerContext::fill_seeded
 // (runtime_types.hpp:208-218): v[e] = float(2*u53(mix64(key, e)) - 1).

@@ -602,6 +602,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   const bool read_c0 = g.beta != 0.0;  // kernels.hpp:69-71: beta == 0 never reads C
   const int cta_group = static_cast<int>(env_int("DM_CTA_GROUP", 0));
   const std::int64_t flush_k = env_int("DM_FLUSH_K", 0);
+  const int gemm_mode = env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed;
 
   for (auto& wp : workers_) {
     if (!wp) continue;
@@ -613,20 +614,32 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     const int np = static_cast<int>(plan.k0.size()) - 1;
     std::int64_t kmax = 0;
     for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
-    const std::int64_t kpitch = std::max<std::int64_t>(4, (kmax + 3) / 4 * 4);
+    const std::int64_t kpitch = std::max<std::int64_t>(8, (kmax + 7) / 8 * 8);
     const int nbuf = np > 1 ? 2 : 1;
-    // panel buffers: [range][buf] -> (hi, lo)
-    auto alloc_planes = [&](const std::vector<Range>& rs, std::vector<std::array<float*, 4>>& out) {
+    // panel planes per range and buffer: fp32 hi, and either fp32 lo
+    // (tf32x3) or bf16 hi + bf16 lo packed in one buffer (mixed); 8 B/element
+    struct Planes {
+      float* hi;
+      float* lo;
+      void* hi16;
+      void* lo16;
+    };
+    auto alloc_planes = [&](const std::vector<Range>& rs, std::vector<std::array<Planes, 2>>& out) {
       out.resize(rs.size());
       for (std::size_t i = 0; i < rs.size(); ++i)
-        for (int b = 0; b < nbuf; ++b)
-          for (int h = 0; h < 2; ++h) {
-            lv.bufs.push_back(
-                w.pool->acquire(static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1) * kpitch) * 4));
-            out[i][b * 2 + h] = lv.bufs.back().f32();
-          }
+        for (int b = 0; b < nbuf; ++b) {
+          const std::size_t elems = static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1) * kpitch);
+          lv.bufs.push_back(w.pool->acquire(elems * 4));
+          float* hi = lv.bufs.back().f32();
+          lv.bufs.push_back(w.pool->acquire(elems * 4));
+          char* second = static_cast<char*>(lv.bufs.back().data());
+          if (gemm_mode == kModeMixed)
+            out[i][b] = Planes{hi, nullptr, second, second + elems * 2};
+          else
+            out[i][b] = Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr};
+        }
     };
-    std::vector<std::array<float*, 4>> pa, pb;
+    std::vector<std::array<Planes, 2>> pa, pb;
     alloc_planes(plan.ar, pa);
     alloc_planes(plan.br, pb);
     cudaEvent_t split_done[2], gemm_done[2];
@@ -644,14 +657,18 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     for (int p = 0; p < np; ++p) {
       const int buf = p % nbuf;
       if (p >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_done[buf], 0), "wait");
-      auto issue = [&](const std::vector<Range>& rs, const std::vector<std::array<float*, 4>>& planes) {
+      auto issue = [&](const std::vector<Range>& rs, const std::vector<std::array<Planes, 2>>& planes) {
         for (std::size_t i = 0; i < rs.size(); ++i)
           for (const Piece& pc : rs[i].panels[p]) {
             bool remote = false;
             const float* src = source_ptr(w, pc.matrix, pc.coord, pol, &remote) + pc.src_off;
-            float* hi = planes[i][buf * 2] + pc.dst_row * kpitch + pc.dst_k;
-            float* lo = planes[i][buf * 2 + 1] + pc.dst_row * kpitch + pc.dst_k;
-            cuda_check(split_tf32(src, pc.lds, pc.trans, pc.rows, pc.kcols, hi, lo, kpitch, w.side),
+            const Planes& pl = planes[i][buf];
+            const std::int64_t off = pc.dst_row * kpitch + pc.dst_k;
+            cuda_check(split_tf32(src, pc.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
+                                  pl.lo ? pl.lo + off : nullptr, kpitch,
+                                  pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
+                                  pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch,
+                                  w.side),
                        "split_tf32");
             w.stats.split_launches += 1;
             (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes();
@@ -665,12 +682,19 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
       for (const Task& t : plan.tasks) {
         StoredBlock& cb = w.owned.at({g.c, t.c});
         Tf32x3Args a;
-        a.a_hi = pa[t.ra][buf * 2];
-        a.a_lo = pa[t.ra][buf * 2 + 1];
-        a.lda = kpitch;
-        a.b_hi = pb[t.rb][buf * 2];
-        a.b_lo = pb[t.rb][buf * 2 + 1];
-        a.ldb = kpitch;
+        a.mode = gemm_mode;
+        const Planes& A = pa[t.ra][buf];
+        const Planes& B = pb[t.rb][buf];
+        a.a_hi = A.hi;
+        a.a_lo = A.lo;
+        a.a_hi16 = A.hi16;
+        a.a_lo16 = A.lo16;
+        a.lda = a.lda16 = kpitch;
+        a.b_hi = B.hi;
+        a.b_lo = B.lo;
+        a.b_hi16 = B.hi16;
+        a.b_lo16 = B.lo16;
+        a.ldb = a.ldb16 = kpitch;
         a.c = cb.mem.f32();
         a.ldc = cb.cols;
         a.m = cb.rows;

@@ -11,6 +11,13 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
+@pytest.fixture(params=[0, 1], ids=["tf32x3", "mixed"])
+def mode(request, monkeypatch):
+    """Split-product mode: 0 = 3xTF32, 1 = TF32 + 2xBF16."""
+    monkeypatch.setenv("DM_GEMM_MODE", str(request.param))
+    return request.param
+
+
 def _relfro(got, want):
     import torch
     d = (got.double() - want).norm()
@@ -39,13 +46,13 @@ def _run(cuda, m, n, k, ta, tb, alpha, beta, cg, seed=0):
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("m,n,k", [(128, 128, 32), (256, 256, 64), (300, 200, 100), (3, 5, 7),
                                    (1024, 1024, 1024), (1000, 1500, 777)])
-def test_shapes(cuda, cg, m, n, k):
+def test_shapes(cuda, mode, cg, m, n, k):
     assert _run(cuda, m, n, k, False, False, 1.0, 0.0, cg) <= TOL
 
 
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
-def test_transposes_alpha_beta(cuda, cg, ta, tb):
+def test_transposes_alpha_beta(cuda, mode, cg, ta, tb):
     assert _run(cuda, 520, 390, 260, ta, tb, 1.5, -0.5, cg, seed=3) <= TOL
 
 
@@ -75,7 +82,7 @@ def test_k_zero_scales_c(cuda):
 
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("k", [16384, 32768])
-def test_large_k_accuracy(cuda, cg, k):
+def test_large_k_accuracy(cuda, mode, cg, k):
     """fp32-level accuracy at the BASELINE K (1xTF32 sits near 2.5e-4; a single
     truncating TMEM accumulator near 1e-4).  The reference's own fp32
     k-ascending loop is ~3e-6 from exact at K=32768."""

@@ -24,4 +24,4 @@ for k in [1024, 4096, 16384, 32768]:
         acc = (acc + np.outer(a[:, kk], b[kk]).astype(np.float32)).astype(np.float32)
     w8 = want[:8].cpu().numpy()
     ref = float(np.linalg.norm(acc - w8) / np.linalg.norm(w8))
-    print(f"K={k} flush={os.environ.get('DM_FLUSH_K','256')} relFro cg1={row[0]:.3e} cg2={row[1]:.3e} fp32-kasc(8 rows)={ref:.3e}", flush=True)
+    print(f"mode={os.environ.get('DM_GEMM_MODE','1')} K={k} flush={os.environ.get('DM_FLUSH_K','256')} relFro cg1={row[0]:.3e} cg2={row[1]:.3e} fp32-kasc(8 rows)={ref:.3e}", flush=True)

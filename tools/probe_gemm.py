@@ -24,6 +24,6 @@ for n in sizes:
         st = s.worker_stats(0)
         kms = st.gemm_ms / reps
         fl = 2.0 * n ** 3
-        print(f"N={n} cg={os.environ.get('DM_CTA_GROUP', 'auto')} gemm_kernel={kms:.2f} ms "
+        print(f"mode={os.environ.get('DM_GEMM_MODE', '1')} N={n} cg={os.environ.get('DM_CTA_GROUP', 'auto')} gemm_kernel={kms:.2f} ms "
               f"({fl / kms / 1e9:.1f} TFLOP/s)  command={wall * 1e3:.2f} ms ({fl / wall / 1e12:.1f} TFLOP/s)",
               flush=True)
