@@ -29,7 +29,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "distributed SGEMM TFLOP/s at N=32768 (fp32, 3xTF32 tcgen05), % of roofline, vs CPU ref"
+METRIC = "distributed SGEMM TFLOP/s at N=32768 on 1/2/4/8 B200; % of roofline; vs CPU ref"
 
 
 # ------------------------------------------------------------------ helpers
@@ -38,16 +38,24 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def gemm_mode() -> int:
+    return 0 if os.environ.get("DM_GEMM_MODE", "1") == "0" else 1
+
+
 def measured_peaks():
-    """3xTF32 useful-flop peak = measured bf16 dense / 6 (TF32 = bf16/2, three
-    MMAs per product)."""
+    """Useful-fp32-flop peak of the MMA mix actually executed, from the measured
+    dense bf16 rate: TF32 runs at bf16/2, so per useful k16 step
+      3xTF32: 6 TF32 k8 MMAs            = 6 bf16-k16 slots -> peak = bf16 / 6
+      mixed : 2 TF32 k8 + 2 BF16 k16    = 4 bf16-k16 slots -> peak = bf16 / 4"""
+    div = 6.0 if gemm_mode() == 0 else 4.0
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         with open(path) as f:
             p = json.load(f)
-        return p["bf16_tflops"] / 6.0, p["bf16_tflops_sustained"] / 6.0, "measured (MEASURED_PEAKS.json bf16 / 6)"
+        return (p["bf16_tflops"] / div, p["bf16_tflops_sustained"] / div,
+                f"measured (MEASURED_PEAKS.json bf16 / {div:.0f})", p["bf16_tflops_sustained"] / 6.0)
     except Exception:
-        return 1590.0 / 6.0, 1400.0 / 6.0, "fallback (B200_PROFILING.md bf16 / 6)"
+        return 1590.0 / div, 1400.0 / div, f"fallback (B200_PROFILING.md bf16 / {div:.0f})", 1400.0 / 6.0
 
 
 class ClockSampler:
@@ -189,7 +197,7 @@ def run_ours(args):
     kern_flops = st.gemm_flops / max(1, st.gemm_launches)
     kern_tflops = kern_flops / (kern_ms_avg / 1e3) / 1e12
     gemm_share = st.gemm_ms / dev_ms if dev_ms else None
-    peak_burst, peak_sust, peak_src = measured_peaks()
+    peak_burst, peak_sust, peak_src, peak_3x = measured_peaks()
     traffic, _ = load_ncu_traffic()
 
     # ---- end to end through the public API with pinned host buffers
@@ -262,7 +270,10 @@ def run_ours(args):
                      "unit": "TFLOP/s", "frac": round(kern_tflops / peak_sust, 4),
                      "traffic": traffic,
                      "peak_source": peak_src + " sustained; burst=" + f"{peak_burst:.1f}",
-                     "kernel": "dm::tf32x3_gemm_kernel<2> (tcgen05 kind::tf32 x3, CTA pair)",
+                     "kernel": ("dm::tf32x3_gemm_kernel<2,1> (CTA pair; hi*hi tcgen05 kind::tf32 + "
+                                "bf16 cross terms kind::f16)") if gemm_mode() else
+                               "dm::tf32x3_gemm_kernel<2,0> (CTA pair; tcgen05 kind::tf32 x3)",
+                     "frac_vs_3xtf32_roofline": round(kern_tflops / peak_3x, 4),
                      "flops_per_launch": kern_flops, "avg_launch_ms": round(kern_ms_avg, 3),
                      "launches": int(st.gemm_launches), "gemm_share_of_step": round(gemm_share, 4) if gemm_share else None},
         "e2e": e2e, "cpu_baseline": cpu, "parity_sampled": parity,
