@@ -59,11 +59,14 @@ struct EpiParams {
   int m, n;
   float alpha, beta;
   int read_c;
+  int group_m;          // rasterisation: tiles walk n inside groups of group_m m-tiles
+  int l2_policy;        // 0 evict_normal, 1 evict_last, 2 evict_first (TMA cache hint)
+  int lockstep;         // >0: producers of a wave stay within `lockstep` k-blocks
+  unsigned* sync;       // lockstep counters [waves * epochs], zeroed per launch
 };
 
 template <int CG>
-__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int& mt, int& nt) {
-  constexpr int G = Cfg<CG>::kGroupM;
+__device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int G, int& mt, int& nt) {
   const int per_group = G * tiles_n;
   const int group = t / per_group;
   const int first_m = group * G;
@@ -142,13 +145,36 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      const uint64_t pol = policy_evict_last();
-      for (int t = unit; t < total_tiles; t += num_units) {
+      const uint64_t pol = ep.l2_policy == 1   ? policy_evict_last()
+                           : ep.l2_policy == 2 ? policy_evict_first()
+                                               : policy_evict_normal();
+      const int epochs = ep.lockstep > 0 ? (num_kb + ep.lockstep - 1) / ep.lockstep : 0;
+      int wave = 0;
+      for (int t = unit; t < total_tiles; t += num_units, ++wave) {
+        // CTAs of this wave (the last wave may be partial)
+        const int wave_ctas = CG * min(num_units, total_tiles - wave * num_units);
         int mt, nt;
-        tile_coords<CG>(t, tiles_m, tiles_n, mt, nt);
+        tile_coords<CG>(t, tiles_m, tiles_n, ep.group_m, mt, nt);
         const int arow = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta;
         const int brow = nt * C::kUmmaN + static_cast<int>(cta_rank) * C::kRowsPerCta;
         for (int kb = 0; kb < num_kb; ++kb) {
+          if (epochs > 0 && kb % ep.lockstep == 0) {
+            // Software lockstep: CTAs sharing A/B tiles read the same k-slices
+            // at about the same time, so L2 serves the sharers instead of DRAM.
+            // Arrive on this epoch, then let at most one epoch of slack build up.
+            const int e = kb / ep.lockstep;
+            unsigned* ctr = ep.sync + static_cast<int64_t>(wave) * epochs;
+            atomicAdd(ctr + e, 1u);
+            if (e > 0) {
+              unsigned seen;
+              uint32_t spins = 0;
+              do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr + e - 1) : "memory");
+                if (seen >= static_cast<unsigned>(wave_ctas)) break;
+                __nanosleep(64);
+              } while (++spins < (1u << 26));
+            }
+          }
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
           uint8_t* st = smem + stage * C::kStageBytes;
           const uint32_t fb = smem_u32(&full_bar[stage]);
@@ -252,7 +278,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     uint32_t chunk_ctr = 0;
     for (int t = unit; t < total_tiles; t += num_units) {
       int mt, nt;
-      tile_coords<CG>(t, tiles_m, tiles_n, mt, nt);
+      tile_coords<CG>(t, tiles_m, tiles_n, ep.group_m, mt, nt);
       float master[C::kColsPerThread];
 #pragma unroll
       for (int j = 0; j < C::kColsPerThread; ++j) master[j] = 0.0f;
@@ -410,7 +436,24 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   if (units < 1) units = 1;
 
   EpiParams ep{a.c, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
-               a.read_c};
+               a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr};
+  if (a.lockstep > 0) {
+    // one counter per (wave, epoch); scratch kept per device, zeroed on the stream
+    const int num_kb = static_cast<int>((a.k + C::kBK - 1) / C::kBK);
+    const int epochs = (num_kb + a.lockstep - 1) / a.lockstep;
+    const int waves = (tiles + units - 1) / units;
+    const size_t bytes = static_cast<size_t>(waves) * epochs * sizeof(unsigned);
+    static void* scratch[64] = {};
+    static size_t scratch_bytes[64] = {};
+    if (scratch_bytes[dev & 63] < bytes) {
+      if (scratch[dev & 63]) cudaFree(scratch[dev & 63]);
+      if (cudaMalloc(&scratch[dev & 63], bytes) != cudaSuccess) return cudaErrorMemoryAllocation;
+      scratch_bytes[dev & 63] = bytes;
+    }
+    ep.sync = static_cast<unsigned*>(scratch[dev & 63]);
+    cudaError_t e = cudaMemsetAsync(ep.sync, 0, bytes, stream);
+    if (e != cudaSuccess) return e;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
   cfg.blockDim = dim3(C::kThreads);

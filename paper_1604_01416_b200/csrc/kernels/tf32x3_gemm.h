@@ -40,6 +40,9 @@ struct Tf32x3Args {
   int cta_group = 0;  // 0 = auto, 1 = single-CTA 128x128 tiles, 2 = CTA-pair 256x256 tiles
   int num_sms = 0;    // 0 = all SMs of the current device
   int64_t flush_k = 0;  // K per TMEM accumulation chunk (0 = default 256)
+  int group_m = 0;      // rasterisation group of m-tiles (0 = default)
+  int l2_policy = 1;    // TMA L2 hint: 0 evict_normal, 1 evict_last, 2 evict_first
+  int lockstep = 0;     // >0: producers stay within this many k-blocks of each other
 };
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);

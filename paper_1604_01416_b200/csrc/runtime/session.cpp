@@ -603,6 +603,9 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   const int cta_group = static_cast<int>(env_int("DM_CTA_GROUP", 0));
   const std::int64_t flush_k = env_int("DM_FLUSH_K", 0);
   const int gemm_mode = env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed;
+  const int group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
+  const int l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
+  const int lockstep = static_cast<int>(env_int("DM_LOCKSTEP", 0));
 
   for (auto& wp : workers_) {
     if (!wp) continue;
@@ -705,6 +708,9 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         a.read_c = p == 0 ? (read_c0 ? 1 : 0) : 1;
         a.cta_group = cta_group;
         a.flush_k = flush_k;
+        a.group_m = group_m;
+        a.l2_policy = l2_policy;
+        a.lockstep = lockstep;
         record_timing(w, true);
         cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");
         record_timing(w, false);
