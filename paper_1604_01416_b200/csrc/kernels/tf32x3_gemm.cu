@@ -166,13 +166,15 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             unsigned* ctr = ep.sync + static_cast<int64_t>(wave) * epochs;
             atomicAdd(ctr + e, 1u);
             if (e > 0) {
+              // bounded wait (~1e7 cycles): lockstep is a locality hint, never a
+              // correctness dependency, so a CTA that is not co-resident cannot hang it
+              const long long t0 = clock64();
               unsigned seen;
-              uint32_t spins = 0;
               do {
                 asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(ctr + e - 1) : "memory");
                 if (seen >= static_cast<unsigned>(wave_ctas)) break;
                 __nanosleep(64);
-              } while (++spins < (1u << 26));
+              } while (clock64() - t0 < 10000000ll);
             }
           }
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
@@ -437,22 +439,15 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
 
   EpiParams ep{a.c, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
                a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr};
-  if (a.lockstep > 0) {
-    // one counter per (wave, epoch); scratch kept per device, zeroed on the stream
-    const int num_kb = static_cast<int>((a.k + C::kBK - 1) / C::kBK);
-    const int epochs = (num_kb + a.lockstep - 1) / a.lockstep;
-    const int waves = (tiles + units - 1) / units;
-    const size_t bytes = static_cast<size_t>(waves) * epochs * sizeof(unsigned);
-    static void* scratch[64] = {};
-    static size_t scratch_bytes[64] = {};
-    if (scratch_bytes[dev & 63] < bytes) {
-      if (scratch[dev & 63]) cudaFree(scratch[dev & 63]);
-      if (cudaMalloc(&scratch[dev & 63], bytes) != cudaSuccess) return cudaErrorMemoryAllocation;
-      scratch_bytes[dev & 63] = bytes;
-    }
-    ep.sync = static_cast<unsigned*>(scratch[dev & 63]);
-    cudaError_t e = cudaMemsetAsync(ep.sync, 0, bytes, stream);
+  if (a.lockstep > 0 && a.sync != nullptr) {
+    const size_t need = tf32x3_sync_bytes(a);
+    if (a.sync_bytes < need) return cudaErrorInvalidValue;
+    ep.lockstep = a.lockstep;
+    ep.sync = a.sync;
+    cudaError_t e = cudaMemsetAsync(ep.sync, 0, need, stream);
     if (e != cudaSuccess) return e;
+  } else {
+    ep.lockstep = 0;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(units * CG);
@@ -472,6 +467,14 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
 }
 
 }  // namespace
+
+size_t tf32x3_sync_bytes(const Tf32x3Args& a) {
+  if (a.lockstep <= 0 || a.m <= 0 || a.n <= 0 || a.k <= 0) return 0;
+  const int64_t tiles = ((a.m + 127) / 128) * ((a.n + 127) / 128);  // upper bound (1-CTA tiles)
+  const int64_t num_kb = (a.k + 31) / 32;
+  const int64_t epochs = (num_kb + a.lockstep - 1) / a.lockstep;
+  return static_cast<size_t>(tiles * epochs) * sizeof(unsigned);  // waves <= tiles
+}
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
   if (a.m <= 0 || a.n <= 0) return cudaSuccess;

@@ -43,9 +43,16 @@ struct Tf32x3Args {
   int group_m = 0;      // rasterisation group of m-tiles (0 = default)
   int l2_policy = 1;    // TMA L2 hint: 0 evict_normal, 1 evict_last, 2 evict_first
   int lockstep = 0;     // >0: producers stay within this many k-blocks of each other
+  unsigned* sync = nullptr;  // lockstep counters (>= tf32x3_sync_bytes), private to this launch
+  size_t sync_bytes = 0;
 };
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);
+
+// Bytes of lockstep counters a launch with these arguments needs (0 if off).
+// Lockstep requires every CTA of the launch to be co-resident: do not enable it
+// when other persistent kernels can share the device concurrently.
+size_t tf32x3_sync_bytes(const Tf32x3Args& args);
 
 // Elementwise split of a strided fp32 panel into K-major planes:
 //   x[r][k] = trans ? src[k*lds + r] : src[r*lds + k],  r < rows, k < kcols

@@ -605,7 +605,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   const int gemm_mode = env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed;
   const int group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
   const int l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
-  const int lockstep = static_cast<int>(env_int("DM_LOCKSTEP", 0));
+  const int lockstep_env = static_cast<int>(env_int("DM_LOCKSTEP", 32));
 
   for (auto& wp : workers_) {
     if (!wp) continue;
@@ -614,6 +614,13 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     WorkerPlan plan = plan_worker(g, w.id, pol);
     if (plan.tasks.empty()) continue;
     Live& lv = live[w.id];
+    // Producer lockstep needs the GEMM's CTAs co-resident: off when another
+    // local worker shares this device (its GEMMs run concurrently).
+    int sharing = 0;
+    for (auto& o : workers_) sharing += (o && o->device == w.device) ? 1 : 0;
+    const int lockstep = sharing == 1 ? lockstep_env : 0;
+    unsigned* sync = nullptr;
+    std::size_t sync_bytes = 0;
     const int np = static_cast<int>(plan.k0.size()) - 1;
     std::int64_t kmax = 0;
     for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
@@ -711,6 +718,16 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         a.group_m = group_m;
         a.l2_policy = l2_policy;
         a.lockstep = lockstep;
+        if (lockstep > 0) {
+          const std::size_t need = tf32x3_sync_bytes(a);
+          if (need > sync_bytes) {
+            lv.bufs.push_back(w.pool->acquire(need));
+            sync = static_cast<unsigned*>(lv.bufs.back().data());
+            sync_bytes = lv.bufs.back().capacity();
+          }
+          a.sync = sync;
+          a.sync_bytes = sync_bytes;
+        }
         record_timing(w, true);
         cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");
         record_timing(w, false);
