@@ -456,12 +456,13 @@ const float* Session::source_ptr(const Worker& reader, MatrixId m, BlockCoord c,
   const int owner = d.layout.owner(c);
   *remote = false;
   if (owner == reader.id) return reader.owned.at({m, c}).mem.f32();
-  if (pol == SourcePolicy::LocalOnly) {
-    auto it = reader.cache.find({m, c});
-    if (it != reader.cache.end() && it->second.version_seen == d.version)
-      return it->second.mem.f32();
+  // A version-fresh cached copy (CyclicGemmExec cache, ops.hpp:278-289) holds the
+  // owner's exact bytes: read it instead of crossing the link again.
+  auto hit = reader.cache.find({m, c});
+  if (hit != reader.cache.end() && hit->second.version_seen == d.version)
+    return hit->second.mem.f32();
+  if (pol == SourcePolicy::LocalOnly)
     throw CacheMissError("cached_backward_gemm: stale or missing cached blocks", {{c.row, c.col}});
-  }
   *remote = true;
   if (const Worker* ow = local(owner)) return ow->owned.at({m, c}).mem.f32();
   return comm_->remote_ptr(m, c);
@@ -545,7 +546,13 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     for (const auto* ranges : {&plan.ar, &plan.br})
       for (const Range& r : *ranges)
         for (const Piece& pc : r.panels[0])
-          if (table_.at(pc.matrix).layout.owner(pc.coord) != w) plan.has_remote = true;
+          if (table_.at(pc.matrix).layout.owner(pc.coord) != w) {
+            const Worker* me = local(w);
+            auto hit = me->cache.find({pc.matrix, pc.coord});
+            const bool fresh = hit != me->cache.end() &&
+                               hit->second.version_seen == table_.at(pc.matrix).version;
+            if (!fresh) plan.has_remote = true;
+          }
   }
   const std::int64_t target = env_int("DM_PANEL_K", 8192);
   if (plan.has_remote && K > 2 * 256 && target > 0) {

@@ -140,3 +140,46 @@ def test_pool_steady_state(cuda):
         for _ in range(10):
             s.cyclic_gemm(1.0, a, b, 0.0, c)
         assert [s.worker_pool_stats(w).fresh_allocations for w in range(P)] == fresh
+
+
+def test_chained_gemms_pool_steady(cuda):
+    """BASELINE config 5 (small): C = A*B; D = C*E on device-resident matrices;
+    no host round trip between the GEMMs and no fresh allocations after the
+    first iteration (acceptance.cpp:437-457 contract)."""
+    from oracle import COracle
+    orc = COracle()
+    P, n = 4, 384
+    with Session(Config(worker_count=P, root_seed=5, devices=[0] * P)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
+        A, B, E = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(3))
+        C, D = s.create_matrix(lay), s.create_matrix(lay)
+        for it in range(4):
+            s.general_gemm(1.0, A, B, 0.0, C)
+            s.general_gemm(1.0, C, E, 0.0, D)
+            if it == 0:
+                fresh = [s.worker_pool_stats(w).fresh_allocations for w in range(P)]
+        assert [s.worker_pool_stats(w).fresh_allocations for w in range(P)] == fresh
+        Ah, Bh, Eh, Ch, Dh = (s.gather(m) for m in (A, B, E, C, D))
+    assert orc.rel_frobenius(Ch, orc.local_gemm(1.0, Ah, False, Bh, False, 0.0)) <= TOL
+    assert orc.rel_frobenius(Dh, orc.local_gemm(1.0, Ch, False, Eh, False, 0.0)) <= TOL
+
+
+def test_fresh_cache_serves_repeated_forward(cuda):
+    """A second cyclic forward with W unchanged reads the version-fresh cached
+    blocks (zero peer bytes); after W changes it pulls again."""
+    P, fin, fout, batch = 4, 128, 64, 32
+    with Session(Config(worker_count=P, root_seed=3, devices=[0] * P)) as s:
+        W = s.create_matrix(make_layout(LayoutKind.RowBlocks1D, fin, fout, fin // P, fout, P),
+                            fill=FillKind.SeededRandom)
+        X = s.create_matrix(make_layout(LayoutKind.ColBlocks1D, fin, batch, fin, batch // P, P),
+                            fill=FillKind.SeededRandom)
+        Y = s.create_matrix(make_layout(LayoutKind.ColBlocks1D, fout, batch, fout, batch // P, P))
+        s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+        s.reset_worker_stats()
+        s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+        assert sum(s.worker_stats(w).peer_bytes_read for w in range(P)) == 0
+        s.scatter(W, np.ones((fin, fout), np.float32))
+        s.reset_worker_stats()
+        s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+        assert sum(s.worker_stats(w).peer_bytes_read for w in range(P)) > 0
+        assert relfro(s.gather(Y), ref_gemm(1.0, np.ones((fin, fout), np.float32), True, s.gather(X), False, 0.0, None)) <= TOL
