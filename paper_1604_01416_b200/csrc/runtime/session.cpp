@@ -671,9 +671,29 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     cuda_check(cudaEventRecord(gemm_done[1], w.stream), "event");
     cuda_check(cudaStreamWaitEvent(w.side, gemm_done[1], 0), "wait");
 
-    for (int p = 0; p < np; ++p) {
-      const int buf = p % nbuf;
-      if (p >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_done[buf], 0), "wait");
+    // Panels with the fewest peer bytes first: the GEMM starts on local data
+    // while the first remote pulls are still in flight (K order does not
+    // matter mathematically; every panel accumulates into C).
+    std::vector<int> order(np);
+    for (int p = 0; p < np; ++p) order[p] = p;
+    if (np > 1) {
+      std::vector<std::uint64_t> remote_bytes(np, 0);
+      for (int p = 0; p < np; ++p)
+        for (const auto* ranges : {&plan.ar, &plan.br})
+          for (const Range& r : *ranges)
+            for (const Piece& pc : r.panels[p]) {
+              bool remote = false;
+              source_ptr(w, pc.matrix, pc.coord, pol, &remote);
+              if (remote) remote_bytes[p] += pc.bytes();
+            }
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int x, int y) { return remote_bytes[x] < remote_bytes[y]; });
+    }
+
+    for (int step = 0; step < np; ++step) {
+      const int p = order[step];
+      const int buf = step % nbuf;
+      if (step >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_done[buf], 0), "wait");
       auto issue = [&](const std::vector<Range>& rs, const std::vector<std::array<Planes, 2>>& planes) {
         for (std::size_t i = 0; i < rs.size(); ++i)
           for (const Piece& pc : rs[i].panels[p]) {
@@ -718,8 +738,8 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         a.n = cb.cols;
         a.k = kw;
         a.alpha = alpha;
-        a.beta = p == 0 ? beta : 1.0f;
-        a.read_c = p == 0 ? (read_c0 ? 1 : 0) : 1;
+        a.beta = step == 0 ? beta : 1.0f;
+        a.read_c = step == 0 ? (read_c0 ? 1 : 0) : 1;
         a.cta_group = cta_group;
         a.flush_k = flush_k;
         a.group_m = group_m;
@@ -761,6 +781,8 @@ void Session::cache_foreign_a(const GemmArgs& g) {
     DeviceGuard guard(w.device);
     for (int r = 0; r < da.layout.grid.n_block_rows(); ++r) {
       if (da.layout.owner({r, 0}) == w.id) continue;
+      auto cached = w.cache.find({g.a, {r, 0}});
+      if (cached != w.cache.end() && cached->second.version_seen == da.version) continue;
       auto [br, bc] = block_extent(da.layout.grid, {r, 0});
       bool remote = false;
       const float* src = source_ptr(w, g.a, {r, 0}, SourcePolicy::Peer, &remote);
