@@ -59,16 +59,26 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 200 ms from before the
+    warm-up; stop() keeps the samples whose host timestamp falls inside the
+    timed window [mark_start, mark_end] (the nearest one if the window is
+    shorter than the sampling period)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis:
+            try:
+                gpu = int(vis.split(",")[gpu])
+            except (ValueError, IndexError):
+                pass
         self.gpu = gpu
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
@@ -83,20 +93,32 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)  # let the sample after the window land
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
         self.thread.join(timeout=2)
+        t0 = self.t0 or 0.0
+        t1 = self.t1 or time.time()
+        inside = [(t, ln) for t, ln in self.lines if t0 <= t <= t1 + 0.2]
+        if not inside and self.lines:
+            inside = [min(self.lines, key=lambda x: abs(x[0] - t0))]
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for _, ln in inside:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 9:
                 continue
@@ -110,7 +132,8 @@ class ClockSampler:
                     reasons.add(nm)
         busy = [x for x in sm if mx and x > 0.3 * mx] or sm
         return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window_s": round(t1 - t0, 3) if self.t0 else None}
 
 
 def load_ncu_traffic():
@@ -167,6 +190,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         return float(t.item())
 
+    clocks = ClockSampler(local if world > 1 else 0)
+    clocks.start()
     # ---- warm-up
     for _ in range(args.warmup):
         s.general_gemm(1.0, a, b, 0.0, c)
@@ -176,14 +201,14 @@ def run_ours(args):
     torch.cuda.synchronize()
     s.reset_worker_stats()
     s.set_gemm_timing(True)
-    clocks = ClockSampler(local if world > 1 else 0)
-    clocks.start()
+    clocks.mark_start()
     s.marker_record(me, 0)
     for _ in range(args.steps):
         s.general_gemm(1.0, a, b, 0.0, c)
     s.marker_record(me, 1)
     s.barrier()
     torch.cuda.synchronize()
+    clocks.mark_end()
     clk = clocks.stop()
     dev_ms = s.marker_elapsed(me, 0, 1)
     st = s.worker_stats(me)
@@ -198,7 +223,10 @@ def run_ours(args):
     kern_tflops = kern_flops / (kern_ms_avg / 1e3) / 1e12
     gemm_share = st.gemm_ms / dev_ms if dev_ms else None
     peak_burst, peak_sust, peak_src, peak_3x = measured_peaks()
-    traffic, _ = load_ncu_traffic()
+    traffic, ncu = load_ncu_traffic()
+    if not (ncu and world == 1 and f"{N}^3" in ncu.get("problem", "") and
+            ("mixed" in ncu.get("kernel", "")) == bool(gemm_mode())):
+        traffic = None  # the committed capture is of a different launch shape
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
