@@ -156,6 +156,30 @@ int dm_scatter(dm_session* s, dm_matrix_id id, const void* host, int64_t rows, i
  * LOCAL sessions always fill the whole matrix; root = -1 (SPMD): every rank
  * writes only the blocks it owns into its own `host`. */
 int dm_gather(dm_session* s, dm_matrix_id id, void* host, int64_t rows, int64_t cols, int root);
+/* update_block (session.hpp:203-222): one block from host data of the
+ * matrix's precision (rows x cols = the block extent); version += 1. */
+int dm_update_block(dm_session* s, dm_matrix_id id, int row, int col, const void* host,
+                    int64_t rows, int64_t cols);
+/* replicate (session.hpp:266-274): every worker keeps version-tagged copies
+ * of all blocks it does not own (ReplicateExec, ops.hpp:660-702). */
+int dm_replicate(dm_session* s, dm_matrix_id id, int enable);
+/* replica_read (session.hpp:276-297): lazy resync of stale replicas, then the
+ * full matrix assembled from worker `reader` (its process fills `host`). */
+int dm_replica_read(dm_session* s, dm_matrix_id id, int reader, void* host, int64_t rows,
+                    int64_t cols);
+/* reshape (session.hpp:299-317): new matrix, same row-major element order,
+ * any layout/precision; narrowing happens before the link (ops.hpp:772-944). */
+int dm_reshape(dm_session* s, dm_matrix_id src, const dm_layout* layout, int precision,
+               dm_matrix_id* out);
+/* add_row_col_sum (session.hpp:321-348): axis 0 = row sums (global_rows x 1),
+ * 1 = column sums; deterministic != 0 folds partials in worker order. */
+int dm_add_row_col_sum(dm_session* s, dm_matrix_id id, int axis, int deterministic,
+                       dm_matrix_id* out);
+/* checkpoint / restore (session.hpp:395-465), "DMTH" v1 file format of
+ * checkpoint.hpp:1-12 (interchangeable with the reference's files). */
+int dm_checkpoint(dm_session* s, const char* path);
+int dm_restore(const char* path, const dm_session_config* cfg, dm_session** out);
+
 /* general_gemm (session.hpp:244-250): C <- alpha op(A) op(B) + beta C */
 int dm_general_gemm(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b, double beta,
                     dm_matrix_id c, int trans_a, int trans_b);

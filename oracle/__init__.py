@@ -172,6 +172,16 @@ class RefOracle:
             "ref_sampled_rows": (C.c_int, [f64, FP, i64, i64, FP, i64, i64, C.c_int, f64, FP, FP, i64, C.c_int]),
             "ref_fill_block": (C.c_int, [FP, i64, i64, u64, C.c_int, C.c_int]),
             "ref_fnv1a": (u64, [vp, i64]),
+            "ref_create_matrix_p": (C.c_int, [vp, C.c_int, i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, P(u64)]),
+            "ref_gather_bytes": (C.c_int, [vp, u64, vp, i64]),
+            "ref_update_block": (C.c_int, [vp, u64, C.c_int, C.c_int, C.c_int, vp, i64, i64]),
+            "ref_reshape": (C.c_int, [vp, u64, C.c_int, i64, i64, i64, i64, C.c_int, C.c_int, P(u64)]),
+            "ref_add_row_col_sum": (C.c_int, [vp, u64, C.c_int, C.c_int, P(u64)]),
+            "ref_replicate": (C.c_int, [vp, u64, C.c_int]),
+            "ref_replica_read": (C.c_int, [vp, u64, C.c_int, vp, i64]),
+            "ref_checkpoint": (C.c_int, [vp, C.c_char_p]),
+            "ref_restore": (C.c_int, [C.c_char_p, P(vp)]),
+            "ref_descriptor_full": (C.c_int, [vp, u64, P(u64), C.c_char_p, C.c_int]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -233,13 +243,86 @@ class RefOracle:
         return RefSession(self, workers, root_seed, deterministic)
 
 
+_NP = {0: np.float16, 1: np.float32, 2: np.float64}
+
+
 class RefSession:
-    def __init__(self, ro: RefOracle, workers, root_seed, deterministic=True):
+    def __init__(self, ro: RefOracle, workers, root_seed, deterministic=True, _handle=None):
         self.ro = ro
+        self.shapes = {}
+        if _handle is not None:
+            self.h = _handle
+            return
         h = vp()
         ro.check(ro.lib.ref_session_create(workers, root_seed & (2**64 - 1), int(deterministic), C.byref(h)))
         self.h = h
-        self.shapes = {}
+
+    @classmethod
+    def restore(cls, ro: RefOracle, path: str) -> "RefSession":
+        h = vp()
+        ro.check(ro.lib.ref_restore(path.encode(), C.byref(h)))
+        return cls(ro, 0, 0, _handle=h)
+
+    def describe(self, mid):
+        """(version, replica_version, replicated, precision, seed, layout string)"""
+        buf = (u64 * 6)()
+        ls = C.create_string_buffer(4096)
+        self.ro.check(self.ro.lib.ref_descriptor_full(self.h, mid, buf, ls, 4096))
+        rows, cols = buf[5] >> 32, buf[5] & 0xFFFFFFFF
+        self.shapes[mid] = (rows, cols, buf[3])
+        return buf[0], buf[1], bool(buf[2]), buf[3], buf[4], ls.value.decode()
+
+    def create_p(self, kind, gr, gc, br, bc, workers, precision, fill=1, host=None) -> int:
+        out = u64()
+        hp = None
+        if host is not None:
+            host = np.ascontiguousarray(host, _NP[precision])
+            hp = C.c_void_p(host.ctypes.data)
+        self.ro.check(self.ro.lib.ref_create_matrix_p(self.h, int(kind), gr, gc, br, bc, workers, precision,
+                                                      fill, hp, C.byref(out)))
+        self.shapes[out.value] = (gr, gc, precision)
+        return out.value
+
+    def gather_p(self, mid) -> np.ndarray:
+        if mid not in self.shapes or len(self.shapes[mid]) < 3:
+            self.describe(mid)
+        gr, gc, p = self.shapes[mid]
+        out = np.empty((gr, gc), _NP[p])
+        self.ro.check(self.ro.lib.ref_gather_bytes(self.h, mid, C.c_void_p(out.ctypes.data), out.nbytes))
+        return out
+
+    def update_block(self, mid, row, col, data):
+        gr, gc, p = self.shapes[mid]
+        data = np.ascontiguousarray(data, _NP[p])
+        self.ro.check(self.ro.lib.ref_update_block(self.h, mid, row, col, p, C.c_void_p(data.ctypes.data),
+                                                   data.shape[0], data.shape[1]))
+
+    def reshape(self, src, kind, gr, gc, br, bc, workers, precision) -> int:
+        out = u64()
+        self.ro.check(self.ro.lib.ref_reshape(self.h, src, int(kind), gr, gc, br, bc, workers, precision,
+                                              C.byref(out)))
+        self.shapes[out.value] = (gr, gc, precision)
+        return out.value
+
+    def add_row_col_sum(self, mid, axis, deterministic=True) -> int:
+        out = u64()
+        self.ro.check(self.ro.lib.ref_add_row_col_sum(self.h, mid, axis, int(deterministic), C.byref(out)))
+        self.describe(out.value)
+        return out.value
+
+    def replicate(self, mid, enable=True):
+        self.ro.check(self.ro.lib.ref_replicate(self.h, mid, int(enable)))
+
+    def replica_read(self, mid, reader) -> np.ndarray:
+        if len(self.shapes.get(mid, ())) < 3:
+            self.describe(mid)
+        gr, gc, p = self.shapes[mid]
+        out = np.empty((gr, gc), _NP[p])
+        self.ro.check(self.ro.lib.ref_replica_read(self.h, mid, reader, C.c_void_p(out.ctypes.data), out.nbytes))
+        return out
+
+    def checkpoint(self, path):
+        self.ro.check(self.ro.lib.ref_checkpoint(self.h, path.encode()))
 
     def close(self):
         if self.h:

@@ -220,6 +220,90 @@ int ref_sampled_rows(double alpha, const float* a_rows, int64_t nrows, int64_t k
   });
 }
 
+// ---- precision-generic entry points (SURVEY 8(f) operations) ----
+int ref_create_matrix_p(void* s, int kind, int64_t gr, int64_t gc, int64_t br, int64_t bc,
+                        int workers, int precision, int fill, const void* host, uint64_t* out) {
+  return guarded([&] {
+    const LayoutSpec l = mk_layout(kind, gr, gc, br, bc, workers);
+    const Precision p = static_cast<Precision>(precision);
+    if (fill == 2) {
+      HostMatrix hm(gr, gc, p);
+      std::memcpy(hm.raw(), host, hm.byte_size());
+      *out = static_cast<Session*>(s)->create_matrix(l, p, FillKind::FromHost, &hm);
+    } else {
+      *out = static_cast<Session*>(s)->create_matrix(l, p, static_cast<FillKind>(fill));
+    }
+  });
+}
+
+int ref_gather_bytes(void* s, uint64_t id, void* out, int64_t nbytes) {
+  return guarded([&] {
+    HostMatrix hm = static_cast<Session*>(s)->gather(id);
+    if (static_cast<int64_t>(hm.byte_size()) != nbytes) throw UsageError("ref_gather_bytes: size");
+    std::memcpy(out, hm.raw(), hm.byte_size());
+  });
+}
+
+int ref_update_block(void* s, uint64_t id, int row, int col, int precision, const void* host,
+                     int64_t rows, int64_t cols) {
+  return guarded([&] {
+    HostMatrix hm(rows, cols, static_cast<Precision>(precision));
+    std::memcpy(hm.raw(), host, hm.byte_size());
+    static_cast<Session*>(s)->update_block(id, {row, col}, hm);
+  });
+}
+
+int ref_reshape(void* s, uint64_t src, int kind, int64_t gr, int64_t gc, int64_t br, int64_t bc,
+                int workers, int precision, uint64_t* out) {
+  return guarded([&] {
+    *out = static_cast<Session*>(s)->reshape(src, mk_layout(kind, gr, gc, br, bc, workers),
+                                             static_cast<Precision>(precision));
+  });
+}
+
+int ref_add_row_col_sum(void* s, uint64_t id, int axis, int deterministic, uint64_t* out) {
+  return guarded([&] {
+    *out = static_cast<Session*>(s)->add_row_col_sum(id, axis == 0 ? Axis::Rows : Axis::Cols,
+                                                     deterministic != 0);
+  });
+}
+
+int ref_replicate(void* s, uint64_t id, int enable) {
+  return guarded([&] { static_cast<Session*>(s)->replicate(id, enable != 0); });
+}
+
+int ref_replica_read(void* s, uint64_t id, int reader, void* out, int64_t nbytes) {
+  return guarded([&] {
+    HostMatrix hm = static_cast<Session*>(s)->replica_read(id, reader);
+    if (static_cast<int64_t>(hm.byte_size()) != nbytes) throw UsageError("ref_replica_read: size");
+    std::memcpy(out, hm.raw(), hm.byte_size());
+  });
+}
+
+int ref_checkpoint(void* s, const char* path) {
+  return guarded([&] { static_cast<Session*>(s)->checkpoint(path); });
+}
+
+int ref_restore(const char* path, void** out) {
+  return guarded([&] { *out = Session::restore(path).release(); });
+}
+
+int ref_descriptor_full(void* s, uint64_t id, uint64_t* out6, char* layout, int cap) {
+  return guarded([&] {
+    const MatrixDescriptor& d = static_cast<Session*>(s)->descriptor(id);
+    out6[0] = d.version;
+    out6[1] = d.replica_version;
+    out6[2] = d.replicated ? 1 : 0;
+    out6[3] = static_cast<uint64_t>(d.precision);
+    out6[4] = d.seed;
+    out6[5] = static_cast<uint64_t>(d.layout.grid.global_rows) << 32 |
+              static_cast<uint64_t>(d.layout.grid.global_cols);
+    const std::string ls = layout_to_string(d.layout);
+    std::strncpy(layout, ls.c_str(), static_cast<size_t>(cap));
+    layout[cap - 1] = 0;
+  });
+}
+
 // WorkerContext::fill_seeded (runtime_types.hpp:208-218) for one block.
 int ref_fill_block(float* out, int64_t rows, int64_t cols, uint64_t matrix_seed, int brow, int bcol) {
   return guarded([&] {

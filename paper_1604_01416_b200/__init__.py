@@ -4,7 +4,7 @@ The public API mirrors the reference's gridgemm::Session; all work happens in
 libdmath_b200.so (tcgen05 3xTF32 GEMM, peer-pull panel pipeline, device pool).
 """
 from .session import (  # noqa: F401
-    CacheMissError, Config, ConfigError, CudaError, DeadlockError, Error, FillKind, IntegrityError,
+    Axis, CacheMissError, Config, ConfigError, CudaError, DeadlockError, Error, FillKind, IntegrityError,
     LayoutKind, LayoutSpec, MatrixDescriptor, NcclError, PlanError, Precision, ProtocolError,
     Session, ShapeError, UnsupportedError, UsageError, checkerboard_dims, fill_seeded, local_gemm,
     make_custom_layout, make_layout, nccl_unique_id, plan_general_gemm, pool_size_class,

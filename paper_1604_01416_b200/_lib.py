@@ -67,6 +67,13 @@ def _load() -> C.CDLL:
         "dm_destroy_matrix": (C.c_int, [vp, u64]),
         "dm_scatter": (C.c_int, [vp, u64, vp, i64, i64]),
         "dm_gather": (C.c_int, [vp, u64, vp, i64, i64, C.c_int]),
+        "dm_update_block": (C.c_int, [vp, u64, C.c_int, C.c_int, vp, i64, i64]),
+        "dm_replicate": (C.c_int, [vp, u64, C.c_int]),
+        "dm_replica_read": (C.c_int, [vp, u64, C.c_int, vp, i64, i64]),
+        "dm_reshape": (C.c_int, [vp, u64, P(Layout), C.c_int, P(u64)]),
+        "dm_add_row_col_sum": (C.c_int, [vp, u64, C.c_int, C.c_int, P(u64)]),
+        "dm_checkpoint": (C.c_int, [vp, C.c_char_p]),
+        "dm_restore": (C.c_int, [C.c_char_p, P(SessionConfig), P(vp)]),
         "dm_general_gemm": (C.c_int, [vp, f64, u64, u64, f64, u64, C.c_int, C.c_int]),
         "dm_cyclic_gemm": (C.c_int, [vp, f64, u64, u64, f64, u64, C.c_int, C.c_int, C.c_int]),
         "dm_broadcast_gemm_reference": (C.c_int, [vp, f64, u64, u64, f64, u64, C.c_int, C.c_int]),
@@ -106,7 +113,8 @@ EXPORTED = [
     "dm_layout_owner", "dm_layout_grid", "dm_block_extent", "dm_layout_to_string",
     "dm_pool_size_class", "dm_plan_general_gemm", "dm_session_create", "dm_session_destroy",
     "dm_session_shutdown", "dm_nccl_unique_id", "dm_create_matrix", "dm_destroy_matrix",
-    "dm_scatter", "dm_gather", "dm_general_gemm", "dm_cyclic_gemm", "dm_broadcast_gemm_reference",
+    "dm_scatter", "dm_gather", "dm_update_block", "dm_replicate", "dm_replica_read", "dm_reshape",
+    "dm_add_row_col_sum", "dm_checkpoint", "dm_restore", "dm_general_gemm", "dm_cyclic_gemm", "dm_broadcast_gemm_reference",
     "dm_cached_backward_gemm", "dm_worker_count", "dm_local_workers", "dm_descriptor_get",
     "dm_pool_stats_get", "dm_pool_trim", "dm_worker_stats_get", "dm_worker_stats_reset",
     "dm_set_gemm_timing", "dm_worker_seed", "dm_descriptor_digest", "dm_block_device_ptr",

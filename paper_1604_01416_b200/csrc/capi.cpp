@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -112,11 +113,11 @@ int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const flo
       args.b_lo = bl.f32();
     }
     if (k > 0 && m > 0 && n > 0) {
-      dm::cuda_check(dm::split_tf32(a, lda, ta, m, k, ah.f32(), const_cast<float*>(args.a_lo), kp,
+      dm::cuda_check(dm::split_tf32(a, 0, lda, ta, m, k, ah.f32(), const_cast<float*>(args.a_lo), kp,
                                     const_cast<void*>(args.a_hi16), const_cast<void*>(args.a_lo16),
                                     kp, st),
                      "split A");
-      dm::cuda_check(dm::split_tf32(b, ldb, tb ? 0 : 1, n, k, bh.f32(), const_cast<float*>(args.b_lo),
+      dm::cuda_check(dm::split_tf32(b, 0, ldb, tb ? 0 : 1, n, k, bh.f32(), const_cast<float*>(args.b_lo),
                                     kp, const_cast<void*>(args.b_hi16),
                                     const_cast<void*>(args.b_lo16), kp, st),
                      "split B");
@@ -272,7 +273,7 @@ int dm_create_matrix(dm_session* s, const dm_layout* layout, int precision, int 
     dm::Session& ss = S(s);
     const dm::LayoutSpec l = dm::layout_from_abi(layout);
     *out = ss.create_matrix(l, static_cast<dm::Precision>(precision),
-                            static_cast<dm::FillKind>(fill), static_cast<const float*>(host));
+                            static_cast<dm::FillKind>(fill), host);
   });
 }
 
@@ -284,11 +285,75 @@ int dm_destroy_matrix(dm_session* s, dm_matrix_id id) {
 }
 
 int dm_scatter(dm_session* s, dm_matrix_id id, const void* host, int64_t rows, int64_t cols) {
-  return guarded([&] { S(s).scatter(id, static_cast<const float*>(host), rows, cols); });
+  return guarded([&] { S(s).scatter(id, host, rows, cols); });
 }
 
 int dm_gather(dm_session* s, dm_matrix_id id, void* host, int64_t rows, int64_t cols, int root) {
-  return guarded([&] { S(s).gather(id, static_cast<float*>(host), rows, cols, root); });
+  return guarded([&] { S(s).gather(id, host, rows, cols, root); });
+}
+
+int dm_update_block(dm_session* s, dm_matrix_id id, int row, int col, const void* host,
+                    int64_t rows, int64_t cols) {
+  return guarded([&] { S(s).update_block(id, {row, col}, host, rows, cols); });
+}
+
+int dm_replicate(dm_session* s, dm_matrix_id id, int enable) {
+  return guarded([&] { S(s).replicate(id, enable != 0); });
+}
+
+int dm_replica_read(dm_session* s, dm_matrix_id id, int reader, void* host, int64_t rows,
+                    int64_t cols) {
+  return guarded([&] { S(s).replica_read(id, reader, host, rows, cols); });
+}
+
+int dm_reshape(dm_session* s, dm_matrix_id src, const dm_layout* layout, int precision,
+               dm_matrix_id* out) {
+  return guarded([&] {
+    if (precision < 0 || precision > 2) throw dm::ConfigError("unknown precision");
+    *out = S(s).reshape(src, dm::layout_from_abi(layout), static_cast<dm::Precision>(precision));
+  });
+}
+
+int dm_add_row_col_sum(dm_session* s, dm_matrix_id id, int axis, int deterministic,
+                       dm_matrix_id* out) {
+  return guarded([&] {
+    if (axis != 0 && axis != 1) throw dm::UsageError("add_row_col_sum: axis must be 0 (rows) or 1 (cols)");
+    *out = S(s).add_row_col_sum(id, axis, deterministic != 0);
+  });
+}
+
+int dm_checkpoint(dm_session* s, const char* path) {
+  return guarded([&] {
+    if (path == nullptr) throw dm::UsageError("checkpoint: null path");
+    S(s).checkpoint(path);
+  });
+}
+
+int dm_restore(const char* path, const dm_session_config* cfg, dm_session** out) {
+  return guarded([&] {
+    if (path == nullptr || cfg == nullptr || out == nullptr)
+      throw dm::UsageError("restore: null argument");
+    // the image decides worker count and root seed (session.hpp:427-432)
+    std::FILE* f = std::fopen(path, "rb");
+    if (f == nullptr) throw dm::ConfigError(std::string("checkpoint: cannot open ") + path);
+    unsigned char hdr[20] = {};
+    const std::size_t got = std::fread(hdr, 1, sizeof(hdr), f);
+    std::fclose(f);
+    if (got < sizeof(hdr) || std::memcmp(hdr, "DMTH", 4) != 0)
+      throw dm::IntegrityError("checkpoint: bad magic or truncated file");
+    auto le = [&](int at, int n) {
+      uint64_t v = 0;
+      for (int i = 0; i < n; ++i) v |= static_cast<uint64_t>(hdr[at + i]) << (8 * i);
+      return v;
+    };
+    dm_session_config c = *cfg;
+    c.worker_count = static_cast<int32_t>(le(8, 4));
+    c.root_seed = le(12, 8);
+    auto sess = std::make_unique<dm_session>();
+    sess->impl = std::make_unique<dm::Session>(c);
+    sess->impl->restore_image(path);
+    *out = sess.release();
+  });
 }
 
 int dm_general_gemm(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b, double beta,
@@ -421,7 +486,7 @@ int dm_fill_seeded_f32(float* dst, int64_t count, uint64_t matrix_seed, int bloc
     const uint64_t key =
         dm::mix64(matrix_seed, (static_cast<uint64_t>(static_cast<uint32_t>(block_row)) << 32) |
                                    static_cast<uint32_t>(block_col));
-    dm::cuda_check(dm::fill_seeded(dst, count, key, static_cast<cudaStream_t>(stream)),
+    dm::cuda_check(dm::fill_seeded(dst, 1, count, key, static_cast<cudaStream_t>(stream)),
                    "fill_seeded");
   });
 }

@@ -9,6 +9,7 @@
 //   (runtime_types.hpp:208-218) using mix64 / u64_to_unit_double
 //   (common.hpp:107-121).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -47,8 +48,15 @@ __device__ __forceinline__ void split_store(float x, const Planes& p, int64_t r,
 constexpr int kT = 32;  // tile edge
 constexpr int kRowsPerPass = 8;
 
+template <typename T>
+__device__ __forceinline__ float load_widen(const T* p) {
+  if constexpr (sizeof(T) == 2) return __half2float(__ldg(reinterpret_cast<const __half*>(p)));
+  else return __ldg(p);
+}
+
 // One 32x32 output tile per block (32 x 8 threads).
-__global__ void split_direct_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
+template <typename T>
+__global__ void split_direct_kernel(const T* __restrict__ src, int64_t lds, int64_t rows,
                                     int64_t kcols, Planes p) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * kT + threadIdx.x;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * kT;
@@ -56,11 +64,12 @@ __global__ void split_direct_kernel(const float* __restrict__ src, int64_t lds, 
 #pragma unroll
   for (int i = 0; i < kT; i += kRowsPerPass) {
     const int64_t r = r0 + threadIdx.y + i;
-    if (r < rows) split_store(__ldg(src + r * lds + k), p, r, k);
+    if (r < rows) split_store(load_widen(src + r * lds + k), p, r, k);
   }
 }
 
-__global__ void split_trans_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
+template <typename T>
+__global__ void split_trans_kernel(const T* __restrict__ src, int64_t lds, int64_t rows,
                                    int64_t kcols, Planes p) {
   __shared__ float tile[kT][kT + 1];
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kT;
@@ -69,7 +78,7 @@ __global__ void split_trans_kernel(const float* __restrict__ src, int64_t lds, i
 #pragma unroll
   for (int i = 0; i < kT; i += kRowsPerPass) {
     const int64_t k = k0 + threadIdx.y + i, r = r0 + threadIdx.x;
-    if (k < kcols && r < rows) tile[threadIdx.y + i][threadIdx.x] = __ldg(src + k * lds + r);
+    if (k < kcols && r < rows) tile[threadIdx.y + i][threadIdx.x] = load_widen(src + k * lds + r);
   }
   __syncthreads();
   // write: out[r][k], coalesced along k
@@ -87,35 +96,49 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-__global__ void fill_seeded_kernel(float* __restrict__ dst, int64_t count, uint64_t key) {
+template <typename T>
+__global__ void fill_seeded_kernel(T* __restrict__ dst, int64_t count, uint64_t key) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < count;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint64_t h = mix64(key ^ mix64(static_cast<uint64_t>(e)));
     const double u = static_cast<double>(h >> 11) * 0x1.0p-53;
-    dst[e] = __double2float_rn(2.0 * u - 1.0);
+    const double v = 2.0 * u - 1.0;
+    if constexpr (sizeof(T) == 8) dst[e] = v;
+    else if constexpr (sizeof(T) == 4) dst[e] = __double2float_rn(v);
+    else dst[e] = __double2half(v);  // RNE from double, as half_bits_from_double
   }
 }
 
 }  // namespace
 
-cudaError_t split_tf32(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols,
-                       float* hi, float* lo, int64_t ldo, void* hi16, void* lo16, int64_t ldo16,
-                       cudaStream_t stream) {
+cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, int64_t rows,
+                       int64_t kcols, float* hi, float* lo, int64_t ldo, void* hi16, void* lo16,
+                       int64_t ldo16, cudaStream_t stream) {
   if (rows <= 0 || kcols <= 0) return cudaSuccess;
   Planes p{hi, lo, static_cast<__nv_bfloat16*>(hi16), static_cast<__nv_bfloat16*>(lo16), ldo, ldo16};
   dim3 block(kT, kRowsPerPass);
   dim3 grid(static_cast<unsigned>((kcols + kT - 1) / kT), static_cast<unsigned>((rows + kT - 1) / kT));
   if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
-  if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, p);
-  else split_direct_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, p);
+  if (src_half) {
+    const __half* s16 = static_cast<const __half*>(src);
+    if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(s16, lds, rows, kcols, p);
+    else split_direct_kernel<<<grid, block, 0, stream>>>(s16, lds, rows, kcols, p);
+  } else {
+    const float* s32 = static_cast<const float*>(src);
+    if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(s32, lds, rows, kcols, p);
+    else split_direct_kernel<<<grid, block, 0, stream>>>(s32, lds, rows, kcols, p);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t fill_seeded(float* dst, int64_t count, uint64_t key, cudaStream_t stream) {
+cudaError_t fill_seeded(void* dst, int precision, int64_t count, uint64_t key, cudaStream_t stream) {
   if (count <= 0) return cudaSuccess;
   int64_t blocks = (count + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  fill_seeded_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(dst, count, key);
+  const unsigned g = static_cast<unsigned>(blocks);
+  if (precision == 0) fill_seeded_kernel<<<g, 256, 0, stream>>>(static_cast<__half*>(dst), count, key);
+  else if (precision == 2) fill_seeded_kernel<<<g, 256, 0, stream>>>(static_cast<double*>(dst), count, key);
+  else fill_seeded_kernel<<<g, 256, 0, stream>>>(static_cast<float*>(dst), count, key);
   return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@
 //       each CTA stages its 128 rows of A and 128 rows of B^T, the leader
 //       issues the MMAs, both CTAs drain their own 128 accumulator lanes.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -55,6 +56,7 @@ struct Cfg {
 
 struct EpiParams {
   float* c;
+  int c_half;
   int64_t ldc;
   int m, n;
   float alpha, beta;
@@ -309,6 +311,19 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
                       static_cast<int>(lane);
       if (row >= ep.m) continue;
       const int c0 = nt * C::kUmmaN + col_off;
+      if (ep.c_half) {
+        // Half16 C: beta*C widened exactly, result rounded once (narrow_store)
+        __half* hrow = reinterpret_cast<__half*>(ep.c) + static_cast<int64_t>(row) * ep.ldc + c0;
+#pragma unroll
+        for (int j = 0; j < C::kColsPerThread; ++j) {
+          if (c0 + j < ep.n) {
+            float v = __fmul_rn(ep.alpha, master[j]);
+            if (ep.read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, __half2float(hrow[j])));
+            hrow[j] = __float2half_rn(v);
+          }
+        }
+        continue;
+      }
       float* crow = ep.c + static_cast<int64_t>(row) * ep.ldc + c0;
       const bool vec_ok = ((ep.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(ep.c) & 15) == 0);
 #pragma unroll
@@ -351,15 +366,21 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
 }
 
 // C <- alpha*0 + beta*C for K == 0 (no tensor-core work).
-__global__ void scale_c_kernel(float* c, int64_t ldc, int m, int n, float alpha_zero, float beta,
-                               int read_c) {
+__global__ void scale_c_kernel(float* c, int c_half, int64_t ldc, int m, int n, float alpha_zero,
+                               float beta, int read_c) {
   const int64_t total = static_cast<int64_t>(m) * n;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(i / n), cc = static_cast<int>(i % n);
     float o = __fmul_rn(alpha_zero, 0.0f);
-    if (read_c) o = __fadd_rn(o, __fmul_rn(beta, c[r * ldc + cc]));
-    c[r * ldc + cc] = o;
+    if (c_half) {
+      __half* h = reinterpret_cast<__half*>(c);
+      if (read_c) o = __fadd_rn(o, __fmul_rn(beta, __half2float(h[r * ldc + cc])));
+      h[r * ldc + cc] = __float2half_rn(o);
+    } else {
+      if (read_c) o = __fadd_rn(o, __fmul_rn(beta, c[r * ldc + cc]));
+      c[r * ldc + cc] = o;
+    }
   }
 }
 
@@ -437,7 +458,7 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   if (units > tiles) units = tiles;
   if (units < 1) units = 1;
 
-  EpiParams ep{a.c, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
+  EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
                a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr};
   if (a.lockstep > 0 && a.sync != nullptr) {
     const size_t need = tf32x3_sync_bytes(a);
@@ -482,7 +503,7 @@ cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
     const int64_t total = a.m * a.n;
     int blocks = static_cast<int>((total + 255) / 256);
     if (blocks > 4096) blocks = 4096;
-    scale_c_kernel<<<blocks, 256, 0, stream>>>(a.c, a.ldc, static_cast<int>(a.m),
+    scale_c_kernel<<<blocks, 256, 0, stream>>>(a.c, a.c_half, a.ldc, static_cast<int>(a.m),
                                                static_cast<int>(a.n), a.alpha, a.beta, a.read_c);
     return cudaGetLastError();
   }

@@ -32,7 +32,8 @@ struct Tf32x3Args {
   const void* b_lo16 = nullptr;
   int64_t ldb = 0, ldb16 = 0;
   int mode = kModeTf32x3;
-  float* c = nullptr;
+  float* c = nullptr;   // fp32 C, or fp16 C (reinterpreted) when c_half != 0
+  int c_half = 0;       // Half16 storage: beta*C widened exactly, result rounded RNE once
   int64_t ldc = 0;
   int64_t m = 0, n = 0, k = 0;
   float alpha = 1.0f, beta = 0.0f;
@@ -60,12 +61,16 @@ size_t tf32x3_sync_bytes(const Tf32x3Args& args);
 //   and/or bf16(hi), bf16(lo) at hi16/lo16 + r*ldo16 + k (when non-null).
 // `src` may be a peer-GPU (UVA / IPC-mapped) pointer: the pull and the split are
 // one kernel.
-cudaError_t split_tf32(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols,
-                       float* hi, float* lo, int64_t ldo, void* hi16, void* lo16, int64_t ldo16,
-                       cudaStream_t stream);
+// `src_half` != 0: the source holds fp16 scalars, widened exactly (the
+// reference's AccumOf<Half> = float, kernels.hpp:29-35).
+cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, int64_t rows,
+                       int64_t kcols, float* hi, float* lo, int64_t ldo, void* hi16, void* lo16,
+                       int64_t ldo16, cudaStream_t stream);
 
 // Seeded synthetic fill, bit-exact with the reference's WorkerContext::fill_seeded
-// (runtime_types.hpp:208-218): v[e] = float(2*u53(mix64(key, e)) - 1).
-cudaError_t fill_seeded(float* dst, int64_t count, uint64_t key, cudaStream_t stream);
+// (runtime_types.hpp:208-218): v[e] = T(2*u53(mix64(key, e)) - 1), the double
+// narrowed once with round-to-nearest-even (scalar_from_double, precision.hpp:83-89).
+// precision: 0 Half16, 1 Single32, 2 Double64.
+cudaError_t fill_seeded(void* dst, int precision, int64_t count, uint64_t key, cudaStream_t stream);
 
 }  // namespace dm

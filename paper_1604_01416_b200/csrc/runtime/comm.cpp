@@ -67,6 +67,12 @@ std::vector<std::uint8_t> Comm::allgather(const void* data, std::size_t bytes) {
 
 void Comm::publish(MatrixId id, const LayoutSpec& layout,
                    const std::map<BlockKey, StoredBlock>& owned) {
+  std::map<BlockKey, void*> mine;
+  for (BlockCoord c : owned_coords(layout, rank_)) mine[{id, c}] = owned.at({id, c}).mem.data();
+  publish_raw(id, layout, mine);
+}
+
+void Comm::publish_raw(MatrixId id, const LayoutSpec& layout, const std::map<BlockKey, void*>& mine_ptrs) {
   std::size_t max_owned = 0;
   std::vector<std::vector<BlockCoord>> coords(world_);
   for (int r = 0; r < world_; ++r) {
@@ -78,9 +84,8 @@ void Comm::publish(MatrixId id, const LayoutSpec& layout,
   std::vector<std::uint8_t> mine(max_owned * kRec, 0);
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   for (std::size_t i = 0; i < coords[rank_].size(); ++i) {
-    const StoredBlock& b = owned.at({id, coords[rank_][i]});
     cudaIpcMemHandle_t h;
-    cuda_check(cudaIpcGetMemHandle(&h, b.mem.data()), "cudaIpcGetMemHandle");
+    cuda_check(cudaIpcGetMemHandle(&h, mine_ptrs.at({id, coords[rank_][i]})), "cudaIpcGetMemHandle");
     std::memcpy(mine.data() + i * kRec, &h, kRec);
   }
   const std::vector<std::uint8_t> all = allgather(mine.data(), mine.size());

@@ -36,6 +36,8 @@ class Comm {
 
   // Export this rank's owned blocks of `id` and map every peer's.
   void publish(MatrixId id, const LayoutSpec& layout, const std::map<BlockKey, StoredBlock>& owned);
+  // Same for raw allocations (this rank's blocks of `id` -> base pointers).
+  void publish_raw(MatrixId id, const LayoutSpec& layout, const std::map<BlockKey, void*>& mine);
   void unpublish(MatrixId id);
   const float* remote_ptr(MatrixId id, BlockCoord c) const;
 

@@ -38,6 +38,7 @@ DM_DEFINE_ERROR(ConfigError, DM_ERR_CONFIG)
 DM_DEFINE_ERROR(ShapeError, DM_ERR_SHAPE)
 DM_DEFINE_ERROR(ProtocolError, DM_ERR_PROTOCOL)
 DM_DEFINE_ERROR(PlanError, DM_ERR_PLAN)
+DM_DEFINE_ERROR(IntegrityError, DM_ERR_INTEGRITY)
 DM_DEFINE_ERROR(UnsupportedError, DM_ERR_UNSUPPORTED)
 DM_DEFINE_ERROR(CudaError, DM_ERR_CUDA)
 DM_DEFINE_ERROR(NcclError, DM_ERR_NCCL)

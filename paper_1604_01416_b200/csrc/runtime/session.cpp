@@ -113,6 +113,8 @@ Session::~Session() {
       if (e) cudaEventDestroy(e);
     w->owned.clear();
     w->cache.clear();
+    w->replicas.clear();
+    w->arena = DeviceBuffer();
     w->pool.reset();
     cudaStreamDestroy(w->stream);
     cudaStreamDestroy(w->side);
@@ -124,12 +126,17 @@ void Session::shutdown() {
   sync_local();
   if (comm_) {
     for (const auto& [id, d] : table_) comm_->unpublish(id);
+    comm_->unpublish(0);  // exchange arenas
     comm_->barrier();
   }
+  arena_ptrs_.clear();
+  arena_bytes_ = 0;
   for (auto& w : workers_) {
     if (!w) continue;
     w->owned.clear();
     w->cache.clear();
+    w->replicas.clear();
+    w->arena = DeviceBuffer();
     w->descriptors.clear();
     w->pool->trim();
   }
@@ -236,37 +243,46 @@ float Session::marker_elapsed(int w, int a, int b) {
 // --------------------------------------------------------------- matrices
 
 MatrixId Session::create_matrix(const LayoutSpec& layout, Precision p, FillKind fill,
-                                const float* host) {
+                                const void* host) {
   require_live();
   validate_layout_workers(layout);
   if (fill == FillKind::FromHost && host == nullptr)
     throw UsageError("create_matrix: FromHost requires host data");
-  if (p != Precision::Single32)
-    throw UnsupportedError(
-        "create_matrix: the B200 path stores Single32 only (Half16/Double64 are outside the fp32 "
-        "GEMM hot path)");
   MatrixDescriptor d;
   d.matrix_id = next_matrix_id_++;
   d.layout = layout;
   d.precision = p;
   d.seed = mix64(root_seed_, d.matrix_id);  // session.hpp:142
+  materialize(d, fill == FillKind::SeededRandom);
+  end_command();
+  if (fill == FillKind::FromHost)
+    scatter(d.matrix_id, host, layout.grid.global_rows, layout.grid.global_cols);
+  return d.matrix_id;
+}
+
+// Allocate (and fill) the blocks every local worker owns under `d`, register
+// the descriptor everywhere and export the blocks to the peers (SPMD).
+void Session::materialize(const MatrixDescriptor& d, bool seeded) {
+  const std::size_t esz = byte_width(d.precision);
   for (auto& w : workers_) {
     if (!w) continue;
     DeviceGuard g(w->device);
-    for (BlockCoord c : owned_coords(layout, w->id)) {
-      auto [br, bc] = block_extent(layout.grid, c);
+    for (BlockCoord c : owned_coords(d.layout, w->id)) {
+      auto [br, bc] = block_extent(d.layout.grid, c);
       StoredBlock blk;
       blk.rows = br;
       blk.cols = bc;
+      blk.precision = d.precision;
       blk.version_seen = d.version;
-      blk.mem = w->pool->acquire(static_cast<std::size_t>(br * bc) * 4);
-      if (fill == FillKind::SeededRandom) {
+      blk.mem = w->pool->acquire(static_cast<std::size_t>(br * bc) * esz);
+      if (seeded) {
         const std::uint64_t key =
             mix64(d.seed, (static_cast<std::uint64_t>(static_cast<std::uint32_t>(c.row)) << 32) |
                               static_cast<std::uint32_t>(c.col));
-        cuda_check(fill_seeded(blk.mem.f32(), br * bc, key, w->stream), "fill_seeded");
+        cuda_check(fill_seeded(blk.mem.data(), static_cast<int>(d.precision), br * bc, key, w->stream),
+                   "fill_seeded");
       } else {
-        cuda_check(cudaMemsetAsync(blk.mem.data(), 0, static_cast<std::size_t>(br * bc) * 4,
+        cuda_check(cudaMemsetAsync(blk.mem.data(), 0, static_cast<std::size_t>(br * bc) * esz,
                                    w->stream),
                    "cudaMemsetAsync");
       }
@@ -276,11 +292,7 @@ MatrixId Session::create_matrix(const LayoutSpec& layout, Precision p, FillKind 
   }
   table_[d.matrix_id] = d;
   sync_local();
-  if (comm_) comm_->publish(d.matrix_id, layout, workers_[rank_]->owned);
-  end_command();
-  if (fill == FillKind::FromHost)
-    scatter(d.matrix_id, host, layout.grid.global_rows, layout.grid.global_cols);
-  return d.matrix_id;
+  if (comm_) comm_->publish(d.matrix_id, d.layout, workers_[rank_]->owned);
 }
 
 void Session::destroy_matrix(MatrixId id) {
@@ -293,7 +305,7 @@ void Session::destroy_matrix(MatrixId id) {
   }
   for (auto& w : workers_) {
     if (!w) continue;
-    for (auto* m : {&w->owned, &w->cache}) {
+    for (auto* m : {&w->owned, &w->cache, &w->replicas}) {
       auto it = m->lower_bound({id, {0, 0}});
       while (it != m->end() && it->first.matrix == id) it = m->erase(it);
     }
@@ -314,23 +326,25 @@ void Session::bump_version(MatrixId id) {
   }
 }
 
-void Session::scatter(MatrixId id, const float* host, std::int64_t rows, std::int64_t cols) {
+void Session::scatter(MatrixId id, const void* host, std::int64_t rows, std::int64_t cols) {
   require_live();
   const MatrixDescriptor d = descriptor(id);
   const BlockGrid& g = d.layout.grid;
   if (rows != g.global_rows || cols != g.global_cols)
     throw ShapeError("scatter: host data shape does not match the matrix");
   if (host == nullptr) throw UsageError("scatter: null host pointer");
+  const std::size_t esz = byte_width(d.precision);
   for (auto& w : workers_) {
     if (!w) continue;
     DeviceGuard guard(w->device);
     for (BlockCoord c : owned_coords(d.layout, w->id)) {
       StoredBlock& blk = w->owned.at({id, c});
-      const float* src = host + static_cast<std::int64_t>(c.row) * g.block_rows * g.global_cols +
-                         static_cast<std::int64_t>(c.col) * g.block_cols;
-      cuda_check(cudaMemcpy2DAsync(blk.mem.data(), static_cast<std::size_t>(blk.cols) * 4, src,
-                                   static_cast<std::size_t>(g.global_cols) * 4,
-                                   static_cast<std::size_t>(blk.cols) * 4,
+      const char* src = static_cast<const char*>(host) +
+                        (static_cast<std::int64_t>(c.row) * g.block_rows * g.global_cols +
+                         static_cast<std::int64_t>(c.col) * g.block_cols) * esz;
+      cuda_check(cudaMemcpy2DAsync(blk.mem.data(), static_cast<std::size_t>(blk.cols) * esz, src,
+                                   static_cast<std::size_t>(g.global_cols) * esz,
+                                   static_cast<std::size_t>(blk.cols) * esz,
                                    static_cast<std::size_t>(blk.rows), cudaMemcpyHostToDevice,
                                    w->stream),
                  "scatter H2D");
@@ -340,7 +354,15 @@ void Session::scatter(MatrixId id, const float* host, std::int64_t rows, std::in
   end_command();
 }
 
-void Session::gather(MatrixId id, float* host, std::int64_t rows, std::int64_t cols, int root) {
+const void* Session::block_src(MatrixId id, BlockCoord c, const Worker& reader) const {
+  const MatrixDescriptor& d = table_.at(id);
+  const int owner = d.layout.owner(c);
+  if (const Worker* ow = local(owner)) return ow->owned.at({id, c}).mem.data();
+  (void)reader;
+  return comm_->remote_ptr(id, c);
+}
+
+void Session::gather(MatrixId id, void* host, std::int64_t rows, std::int64_t cols, int root) {
   require_live();
   const MatrixDescriptor d = descriptor(id);
   const BlockGrid& g = d.layout.grid;
@@ -350,6 +372,7 @@ void Session::gather(MatrixId id, float* host, std::int64_t rows, std::int64_t c
   const bool all_blocks = !comm_ || root == rank_;
   const bool any = !comm_ || root == -1 || root == rank_;
   if (any && host == nullptr) throw UsageError("gather: null host pointer");
+  const std::size_t esz = byte_width(d.precision);
   if (any) {
     Worker& me = comm_ ? *workers_[rank_] : *workers_[0];
     for (int r = 0; r < g.n_block_rows(); ++r)
@@ -358,14 +381,15 @@ void Session::gather(MatrixId id, float* host, std::int64_t rows, std::int64_t c
         Worker* ow = local(owner);
         if (!all_blocks && ow == nullptr) continue;
         auto [br, bc] = block_extent(g, {r, c});
-        const float* src = ow ? ow->owned.at({id, {r, c}}).mem.f32() : comm_->remote_ptr(id, {r, c});
+        const void* src = block_src(id, {r, c}, me);
         Worker& issuer = ow ? *ow : me;
         DeviceGuard guard(issuer.device);
-        float* dst = host + static_cast<std::int64_t>(r) * g.block_rows * g.global_cols +
-                     static_cast<std::int64_t>(c) * g.block_cols;
-        cuda_check(cudaMemcpy2DAsync(dst, static_cast<std::size_t>(g.global_cols) * 4, src,
-                                     static_cast<std::size_t>(bc) * 4,
-                                     static_cast<std::size_t>(bc) * 4,
+        char* dst = static_cast<char*>(host) +
+                    (static_cast<std::int64_t>(r) * g.block_rows * g.global_cols +
+                     static_cast<std::int64_t>(c) * g.block_cols) * esz;
+        cuda_check(cudaMemcpy2DAsync(dst, static_cast<std::size_t>(g.global_cols) * esz, src,
+                                     static_cast<std::size_t>(bc) * esz,
+                                     static_cast<std::size_t>(bc) * esz,
                                      static_cast<std::size_t>(br), cudaMemcpyDefault,
                                      issuer.stream),
                    "gather D2H");
@@ -399,6 +423,8 @@ void Session::validate_general(const GemmArgs& g) const {
   if (da.precision != db.precision || da.precision != dc.precision)
     throw UsageError("gemm: operands must share a precision; reshape to convert first");
   if (dc.replicated) throw UsageError("gemm: destination matrix may not be replicated");
+  if (da.precision == Precision::Double64)
+    throw UnsupportedError("gemm: Double64 is outside the fp32 tensor-core path (reshape to Single32)");
   const std::int64_t kk = g.trans_a ? da.layout.grid.global_rows : da.layout.grid.global_cols;
   const std::int64_t m = g.trans_a ? da.layout.grid.global_cols : da.layout.grid.global_rows;
   const std::int64_t kb = g.trans_b ? db.layout.grid.global_cols : db.layout.grid.global_rows;
@@ -450,21 +476,23 @@ void Session::validate_cyclic(const GemmArgs& g, std::vector<WorkerId>* strip_ow
   }
 }
 
-const float* Session::source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
-                                 bool* remote) const {
+const void* Session::source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
+                                bool* remote) const {
   const MatrixDescriptor& d = table_.at(m);
   const int owner = d.layout.owner(c);
   *remote = false;
-  if (owner == reader.id) return reader.owned.at({m, c}).mem.f32();
-  // A version-fresh cached copy (CyclicGemmExec cache, ops.hpp:278-289) holds the
-  // owner's exact bytes: read it instead of crossing the link again.
-  auto hit = reader.cache.find({m, c});
-  if (hit != reader.cache.end() && hit->second.version_seen == d.version)
-    return hit->second.mem.f32();
+  if (owner == reader.id) return reader.owned.at({m, c}).mem.data();
+  // A version-fresh cached copy (CyclicGemmExec cache, ops.hpp:278-289) or
+  // replica (ReplicateExec, ops.hpp:660-702) holds the owner's exact bytes:
+  // read it instead of crossing the link again.
+  for (const auto* store : {&reader.cache, &reader.replicas}) {
+    auto hit = store->find({m, c});
+    if (hit != store->end() && hit->second.version_seen == d.version) return hit->second.mem.data();
+  }
   if (pol == SourcePolicy::LocalOnly)
     throw CacheMissError("cached_backward_gemm: stale or missing cached blocks", {{c.row, c.col}});
   *remote = true;
-  if (const Worker* ow = local(owner)) return ow->owned.at({m, c}).mem.f32();
+  if (const Worker* ow = local(owner)) return ow->owned.at({m, c}).mem.data();
   return comm_->remote_ptr(m, c);
 }
 
@@ -547,11 +575,9 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
       for (const Range& r : *ranges)
         for (const Piece& pc : r.panels[0])
           if (table_.at(pc.matrix).layout.owner(pc.coord) != w) {
-            const Worker* me = local(w);
-            auto hit = me->cache.find({pc.matrix, pc.coord});
-            const bool fresh = hit != me->cache.end() &&
-                               hit->second.version_seen == table_.at(pc.matrix).version;
-            if (!fresh) plan.has_remote = true;
+            bool remote = false;
+            source_ptr(*local(w), pc.matrix, pc.coord, pol, &remote);
+            if (remote) plan.has_remote = true;
           }
   }
   const std::int64_t target = env_int("DM_PANEL_K", 8192);
@@ -613,6 +639,9 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   const int group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
   const int l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
   const int lockstep_env = static_cast<int>(env_int("DM_LOCKSTEP", 32));
+  // Half16 operands compute at fp32 and round C once (AccumOf<Half>, kernels.hpp:29-35)
+  const bool half_in = table_.at(g.a).precision == Precision::Half16;
+  const std::size_t esz = byte_width(table_.at(g.a).precision);
 
   for (auto& wp : workers_) {
     if (!wp) continue;
@@ -698,17 +727,18 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         for (std::size_t i = 0; i < rs.size(); ++i)
           for (const Piece& pc : rs[i].panels[p]) {
             bool remote = false;
-            const float* src = source_ptr(w, pc.matrix, pc.coord, pol, &remote) + pc.src_off;
+            const void* src = static_cast<const char*>(source_ptr(w, pc.matrix, pc.coord, pol, &remote)) +
+                              pc.src_off * static_cast<std::int64_t>(esz);
             const Planes& pl = planes[i][buf];
             const std::int64_t off = pc.dst_row * kpitch + pc.dst_k;
-            cuda_check(split_tf32(src, pc.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
+            cuda_check(split_tf32(src, half_in ? 1 : 0, pc.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
                                   pl.lo ? pl.lo + off : nullptr, kpitch,
                                   pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
                                   pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch,
                                   w.side),
                        "split_tf32");
             w.stats.split_launches += 1;
-            (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes();
+            (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
           }
       };
       issue(plan.ar, pa);
@@ -733,6 +763,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         a.b_lo16 = B.lo16;
         a.ldb = a.ldb16 = kpitch;
         a.c = cb.mem.f32();
+        a.c_half = half_in ? 1 : 0;
         a.ldc = cb.cols;
         a.m = cb.rows;
         a.n = cb.cols;
@@ -785,16 +816,17 @@ void Session::cache_foreign_a(const GemmArgs& g) {
       if (cached != w.cache.end() && cached->second.version_seen == da.version) continue;
       auto [br, bc] = block_extent(da.layout.grid, {r, 0});
       bool remote = false;
-      const float* src = source_ptr(w, g.a, {r, 0}, SourcePolicy::Peer, &remote);
+      const void* src = block_src(g.a, {r, 0}, w);
       StoredBlock blk;
       blk.rows = br;
       blk.cols = bc;
+      blk.precision = da.precision;
       blk.version_seen = da.version;
-      blk.mem = w.pool->acquire(static_cast<std::size_t>(br * bc) * 4);
-      cuda_check(cudaMemcpyAsync(blk.mem.data(), src, static_cast<std::size_t>(br * bc) * 4,
-                                 cudaMemcpyDefault, w.side),
+      blk.mem = w.pool->acquire(blk.bytes());
+      cuda_check(cudaMemcpyAsync(blk.mem.data(), src, blk.bytes(), cudaMemcpyDefault, w.side),
                  "cache copy");
-      w.stats.peer_bytes_read += static_cast<std::uint64_t>(br * bc) * 4;
+      (void)remote;
+      w.stats.peer_bytes_read += blk.bytes();
       w.cache[{g.a, {r, 0}}] = std::move(blk);
     }
   }

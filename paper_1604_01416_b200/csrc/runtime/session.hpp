@@ -35,8 +35,10 @@ enum class FillKind : std::uint8_t { Zeros = 0, SeededRandom = 1, FromHost = 2 }
 
 struct StoredBlock {
   std::int64_t rows = 0, cols = 0;
+  Precision precision = Precision::Single32;
   std::uint64_t version_seen = 0;
   DeviceBuffer mem;
+  std::size_t bytes() const { return static_cast<std::size_t>(rows * cols) * byte_width(precision); }
 };
 
 struct BlockKey {
@@ -64,6 +66,8 @@ struct Worker {
   std::map<MatrixId, MatrixDescriptor> descriptors;
   std::map<BlockKey, StoredBlock> owned;
   std::map<BlockKey, StoredBlock> cache;
+  std::map<BlockKey, StoredBlock> replicas;
+  DeviceBuffer arena;  // exchange buffer peers read (row/col partials, narrowed reshape payloads)
   std::uint64_t seed = 0;
   dm_worker_stats stats{};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_events;
@@ -85,10 +89,20 @@ class Session {
   int rank() const { return rank_; }
   std::vector<int> local_worker_ids() const;
 
-  MatrixId create_matrix(const LayoutSpec& layout, Precision p, FillKind fill, const float* host);
+  MatrixId create_matrix(const LayoutSpec& layout, Precision p, FillKind fill, const void* host);
   void destroy_matrix(MatrixId id);
-  void scatter(MatrixId id, const float* host, std::int64_t rows, std::int64_t cols);
-  void gather(MatrixId id, float* host, std::int64_t rows, std::int64_t cols, int root);
+  void scatter(MatrixId id, const void* host, std::int64_t rows, std::int64_t cols);
+  void gather(MatrixId id, void* host, std::int64_t rows, std::int64_t cols, int root);
+  void update_block(MatrixId id, BlockCoord c, const void* host, std::int64_t rows, std::int64_t cols);
+  // replication, reshape, row/col sums, checkpoint
+  void replicate(MatrixId id, bool enable);
+  void replica_read(MatrixId id, int reader, void* host, std::int64_t rows, std::int64_t cols);
+  MatrixId reshape(MatrixId src, const LayoutSpec& layout, Precision p);
+  MatrixId add_row_col_sum(MatrixId id, int axis, bool deterministic);
+  void checkpoint(const std::string& path);
+  void restore_image(const std::string& path);  // into a fresh session
+  std::uint64_t next_matrix_id() const { return next_matrix_id_; }
+  std::uint64_t root_seed() const { return root_seed_; }
   void general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
                     bool tb);
   void cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta, bool tb,
@@ -136,6 +150,12 @@ class Session {
     bool has_remote = false;
   };
 
+  void materialize(const MatrixDescriptor& d, bool seeded);
+  const void* block_src(MatrixId id, BlockCoord c, const Worker& reader) const;
+  void sync_replicas(MatrixId id);
+  void* arena(int w, std::size_t* bytes);
+  void ensure_arenas(std::size_t bytes);
+  void mid_barrier();
   Worker& worker(int w);
   const Worker& worker(int w) const;
   Worker* local(int w);
@@ -155,8 +175,8 @@ class Session {
   WorkerPlan plan_worker(const GemmArgs& g, int w, SourcePolicy pol) const;
   void add_range_pieces(Range& rg, const MatrixDescriptor& d, bool op_rows_trans, bool is_a,
                         const std::vector<std::int64_t>& k0) const;
-  const float* source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
-                          bool* remote) const;
+  const void* source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
+                         bool* remote) const;
   void run_gemm(const GemmArgs& g, SourcePolicy pol);
   void cache_foreign_a(const GemmArgs& g);
   void record_timing(Worker& w, bool start);
@@ -173,6 +193,9 @@ class Session {
   std::vector<std::unique_ptr<Worker>> workers_;  // index = worker id; null if not local
   std::map<MatrixId, MatrixDescriptor> table_;
   std::map<MatrixId, std::uint64_t> cache_meta_;
+  std::uint64_t nondet_counter_ = 0;
+  std::size_t arena_bytes_ = 0;               // replicated: every worker's arena size
+  std::vector<void*> arena_ptrs_;             // per worker (peer-readable)
   std::unique_ptr<Comm> comm_;
 };
 

@@ -76,6 +76,12 @@ class Precision(enum.IntEnum):
     Double64 = 2
 
 
+class Axis(enum.IntEnum):
+    """kernels.hpp:16 (add_row_col_sum axis)"""
+    Rows = 0
+    Cols = 1
+
+
 class FillKind(enum.IntEnum):
     """runtime_types.hpp:68"""
     Zeros = 0
@@ -197,25 +203,53 @@ def _host_ptr(arr: np.ndarray):
     return C.c_void_p(arr.ctypes.data)
 
 
+_DTYPES = {Precision.Half16: np.float16, Precision.Single32: np.float32, Precision.Double64: np.float64}
+
+
+def _dtype(p) -> np.dtype:
+    return np.dtype(_DTYPES[Precision(p)])
+
+
+def _make_config(cfg: "Config"):
+    mode = {"local": 0, "spmd": 1}[cfg.mode]
+    keep = []
+    devs = None
+    if cfg.devices is not None:
+        devs = (C.c_int32 * len(cfg.devices))(*cfg.devices)
+        keep.append(devs)
+    nid = None
+    if cfg.nccl_id is not None:
+        nid = C.create_string_buffer(bytes(cfg.nccl_id), 128)
+        keep.append(nid)
+    c = SessionConfig(cfg.worker_count, mode, cfg.rank, int(cfg.coherence_checks),
+                      cfg.root_seed & (2**64 - 1),
+                      C.cast(devs, C.POINTER(C.c_int32)) if devs is not None else None,
+                      C.cast(nid, C.c_void_p) if nid is not None else None)
+    return c, keep
+
+
 class Session:
     """gridgemm::Session on B200 workers (one GPU each)."""
 
-    def __init__(self, cfg: Config):
+    def __init__(self, cfg: Config, _handle=None):
         self._cfg = cfg
-        mode = {"local": 0, "spmd": 1}[cfg.mode]
-        devs = None
-        if cfg.devices is not None:
-            devs = (C.c_int32 * len(cfg.devices))(*cfg.devices)
-        nid = None
-        if cfg.nccl_id is not None:
-            nid = C.create_string_buffer(bytes(cfg.nccl_id), 128)
-        c = SessionConfig(cfg.worker_count, mode, cfg.rank, int(cfg.coherence_checks),
-                          cfg.root_seed & (2**64 - 1),
-                          C.cast(devs, C.POINTER(C.c_int32)) if devs is not None else None,
-                          C.cast(nid, C.c_void_p) if nid is not None else None)
+        if _handle is not None:
+            self._h = _handle
+            return
+        c, _keep = _make_config(cfg)
         h = C.c_void_p()
         _check(lib.dm_session_create(C.byref(c), C.byref(h)))
         self._h = h
+
+    @classmethod
+    def restore(cls, path: str, cfg: Optional[Config] = None) -> "Session":
+        """Session::restore (session.hpp:425-465): worker count and root seed
+        come from the image; `cfg` supplies placement (mode, devices, NCCL id)."""
+        cfg = cfg or Config()
+        c, _keep = _make_config(cfg)
+        h = C.c_void_p()
+        _check(lib.dm_restore(path.encode(), C.byref(c), C.byref(h)))
+        return cls(cfg, _handle=h)
 
     # -- lifecycle
     def close(self):
@@ -320,7 +354,7 @@ class Session:
         if fill == FillKind.FromHost:
             if host is None:
                 raise UsageError("create_matrix: FromHost requires host data")
-            host = self._host_in(host)
+            host = self._host_in(host, precision)
             if host.shape != (layout.global_rows, layout.global_cols):
                 raise ShapeError("create_matrix: host data shape does not match the layout")
             hp = _host_ptr(host)
@@ -333,14 +367,15 @@ class Session:
         _check(lib.dm_destroy_matrix(self._h, mid))
 
     @staticmethod
-    def _host_in(host: np.ndarray) -> np.ndarray:
-        if host.dtype != np.float32:
-            raise UnsupportedError("host data must be float32 (Single32)")
-        return np.ascontiguousarray(host)
+    def _host_in(host: np.ndarray, precision) -> np.ndarray:
+        """Host data at the matrix precision.  Other dtypes are converted with
+        numpy's round-to-nearest-even, like the reference's scatter_payloads
+        per-element conversion (session.hpp:568-576)."""
+        return np.ascontiguousarray(host, dtype=_dtype(precision))
 
     def scatter(self, mid: int, host: np.ndarray):
         """Session::scatter (session.hpp:164-175); bit-exact."""
-        host = self._host_in(host)
+        host = self._host_in(host, self.descriptor(mid).precision)
         if host.ndim != 2:
             raise ShapeError("scatter: host data must be 2-D")
         _check(lib.dm_scatter(self._h, mid, _host_ptr(host), host.shape[0], host.shape[1]))
@@ -349,12 +384,48 @@ class Session:
         """Session::gather (session.hpp:179-201); bit-exact, owned blocks only."""
         d = self.descriptor(mid)
         shape = (d.layout.global_rows, d.layout.global_cols)
+        dt = _dtype(d.precision)
         if out is None:
-            out = np.empty(shape, dtype=np.float32)
-        if out.shape != shape or out.dtype != np.float32 or not out.flags.c_contiguous:
+            out = np.empty(shape, dtype=dt)
+        if out.shape != shape or out.dtype != dt or not out.flags.c_contiguous:
             raise ShapeError("gather: output buffer shape does not match the matrix")
         _check(lib.dm_gather(self._h, mid, _host_ptr(out), shape[0], shape[1], root))
         return out
+
+    def update_block(self, mid: int, row: int, col: int, data: np.ndarray):
+        """Session::update_block (session.hpp:203-222)."""
+        data = self._host_in(data, self.descriptor(mid).precision)
+        if data.ndim != 2:
+            raise ShapeError("update_block: data must be 2-D")
+        _check(lib.dm_update_block(self._h, mid, row, col, _host_ptr(data), data.shape[0], data.shape[1]))
+
+    # -- SURVEY 8(f): replication, reshape, row/col sums, checkpoint
+    def replicate(self, mid: int, enable: bool):
+        """Session::replicate (session.hpp:266-274)."""
+        _check(lib.dm_replicate(self._h, mid, int(enable)))
+
+    def replica_read(self, mid: int, reader: int) -> np.ndarray:
+        """Session::replica_read (session.hpp:276-297)."""
+        d = self.descriptor(mid)
+        out = np.empty((d.layout.global_rows, d.layout.global_cols), dtype=_dtype(d.precision))
+        _check(lib.dm_replica_read(self._h, mid, reader, _host_ptr(out), out.shape[0], out.shape[1]))
+        return out
+
+    def reshape(self, src: int, layout: LayoutSpec, precision=Precision.Single32) -> int:
+        """Session::reshape (session.hpp:299-317)."""
+        out = C.c_uint64()
+        _check(lib.dm_reshape(self._h, src, C.byref(layout._abi()), int(precision), C.byref(out)))
+        return out.value
+
+    def add_row_col_sum(self, mid: int, axis: int, deterministic_reduce: bool = True) -> int:
+        """Session::add_row_col_sum (session.hpp:321-348); axis 0 = rows, 1 = cols."""
+        out = C.c_uint64()
+        _check(lib.dm_add_row_col_sum(self._h, mid, int(axis), int(deterministic_reduce), C.byref(out)))
+        return out.value
+
+    def checkpoint(self, path: str):
+        """Session::checkpoint (session.hpp:395-423), DMTH v1 file."""
+        _check(lib.dm_checkpoint(self._h, path.encode()))
 
     # -- distributed operations
     def general_gemm(self, alpha, a, b, beta, c, trans_a=False, trans_b=False):

@@ -205,12 +205,146 @@ def fills(ro):
     return out
 
 
+# ------------------------------------------------------------ SURVEY 8(f)
+LAYS = [(0, 12, 20, 5, 7), (1, 12, 20, 5, 7), (2, 12, 20, 5, 7), (3, 12, 20, 5, 7), (3, 33, 17, 8, 6)]
+
+
+def fills_p(ro):
+    out = []
+    for prec in (0, 1, 2):
+        for (kind, gr, gc, br, bc) in LAYS:
+            with ro.session(4, 11 + prec) as s:
+                m = s.create_p(kind, gr, gc, br, bc, 4, prec)
+                out.append({"precision": prec, "layout": [kind, gr, gc, br, bc, 4], "root_seed": 11 + prec,
+                            "fnv": hx(ro.fnv1a(s.gather_p(m)))})
+    return out
+
+
+def reshapes(ro):
+    cases = []
+    combos = [((3, 12, 20, 5, 7), (0, 16, 15, 4, 15), 1, 0),   # single -> half (narrow before link)
+              ((0, 12, 20, 3, 20), (3, 20, 12, 6, 5), 0, 1),   # half -> single (widen at receiver)
+              ((1, 24, 10, 24, 3), (2, 6, 40, 2, 9), 2, 0),    # double -> half
+              ((2, 24, 10, 5, 10), (3, 10, 24, 4, 7), 1, 2),   # single -> double
+              ((3, 33, 17, 8, 6), (1, 51, 11, 51, 4), 1, 1),   # same precision, new shape
+              ((0, 7, 9, 7, 9), (3, 3, 21, 2, 8), 2, 2)]
+    for P in (1, 3, 4):
+        for i, (src, dst, sp, dp) in enumerate(combos):
+            with ro.session(P, 31 + i) as s:
+                a = s.create_p(src[0], src[1], src[2], src[3], src[4], P, sp)
+                b = s.reshape(a, dst[0], dst[1], dst[2], dst[3], dst[4], P, dp)
+                cases.append({"workers": P, "root_seed": 31 + i, "src": list(src), "src_prec": sp,
+                              "dst": list(dst), "dst_prec": dp, "src_fnv": hx(ro.fnv1a(s.gather_p(a))),
+                              "dst_fnv": hx(ro.fnv1a(s.gather_p(b))), "dst_id": b})
+    return cases
+
+
+def sums(ro):
+    cases = []
+    for P in (1, 2, 3, 4):
+        for prec in (0, 1, 2):
+            for (kind, gr, gc, br, bc) in LAYS[:4] + [(3, 40, 70, 9, 11)]:
+                for axis in (0, 1):
+                    for det in (True, False):
+                        seed = 51 + P * 7 + prec
+                        with ro.session(P, seed) as s:
+                            m = s.create_p(kind, gr, gc, br, bc, P, prec)
+                            o = s.add_row_col_sum(m, axis, det)
+                            o2 = s.add_row_col_sum(m, axis, det)  # salt advances per call
+                            cases.append({"workers": P, "root_seed": seed, "precision": prec,
+                                          "layout": [kind, gr, gc, br, bc, P], "axis": axis, "det": det,
+                                          "in_fnv": hx(ro.fnv1a(s.gather_p(m))),
+                                          "out_fnv": hx(ro.fnv1a(s.gather_p(o))),
+                                          "out2_fnv": hx(ro.fnv1a(s.gather_p(o2))),
+                                          "out_layout": s.describe(o)[5], "out_id": o})
+    return cases
+
+
+def replication(ro):
+    out = []
+    for P in (1, 3, 4):
+        with ro.session(P, 71) as s:
+            m = s.create_p(3, 30, 22, 7, 6, P, 1)
+            s.replicate(m, True)
+            d1 = s.describe(m)
+            r0 = s.replica_read(m, P - 1)
+            new = (np.arange(30 * 22, dtype=np.float32).reshape(30, 22) / 7.0).astype(np.float32)
+            s.scatter(m, new)
+            d2 = s.describe(m)
+            r1 = s.replica_read(m, 0)
+            d3 = s.describe(m)
+            out.append({"workers": P, "root_seed": 71, "layout": [3, 30, 22, 7, 6, P],
+                        "read0_fnv": hx(ro.fnv1a(r0)), "read1_fnv": hx(ro.fnv1a(r1)),
+                        "desc_after_enable": list(d1[:3]), "desc_after_scatter": list(d2[:3]),
+                        "desc_after_read": list(d3[:3])})
+    return out
+
+
+def update_blocks(ro):
+    out = []
+    with ro.session(3, 81) as s:
+        m = s.create_p(1, 20, 30, 20, 7, 3, 1)
+        data = (np.linspace(-3, 3, 20 * 7, dtype=np.float32).reshape(20, 7))
+        s.update_block(m, 0, 2, data)
+        out.append({"workers": 3, "root_seed": 81, "layout": [1, 20, 30, 20, 7, 3], "block": [0, 2],
+                    "version": s.describe(m)[0], "fnv": hx(ro.fnv1a(s.gather_p(m)))})
+    return out
+
+
+def half_gemm(ro):
+    cases = []
+    for P in (1, 4):
+        for trans in range(4):
+            ta, tb = bool(trans & 1), bool(trans & 2)
+            with ro.session(P, 91 + trans) as s:
+                a = s.create_p(3, 40, 40, 16, 12, P, 0)
+                b = s.create_p(0, 40, 40, 10, 40, P, 0)
+                c = s.create_p(2, 40, 40, 9, 40, P, 0)
+                C0 = s.gather_p(c)
+                assert s.general_gemm(1.5, a, b, -0.5, c, ta, tb) == 0
+                cases.append({"workers": P, "root_seed": 91 + trans, "ta": ta, "tb": tb,
+                              "A": hx(ro.fnv1a(s.gather_p(a))), "B": hx(ro.fnv1a(s.gather_p(b))),
+                              "C0": hx(ro.fnv1a(C0)), "C": hx(ro.fnv1a(s.gather_p(c)))})
+    return cases
+
+
+def checkpoint_fixture(ro):
+    """A reference-written DMTH file (committed) plus the recipe to rebuild the
+    same session state, so the product can be checked both ways."""
+    path = os.path.join(os.path.dirname(OUT), "ref_checkpoint.dmth")
+    with ro.session(3, 1234) as s:
+        a = s.create_p(3, 20, 18, 7, 5, 3, 1)
+        b = s.create_p(0, 12, 10, 4, 10, 3, 0)
+        c = s.create_p(2, 9, 14, 2, 14, 3, 2)
+        s.replicate(b, True)
+        s.scatter(a, (np.arange(20 * 18, dtype=np.float32).reshape(20, 18) * 0.25 - 7).astype(np.float32))
+        s.checkpoint(path)
+        digests = {str(m): hx(ro.fnv1a(s.gather_p(m))) for m in (a, b, c)}
+    data = open(path, "rb").read()
+    r = RefSession_restore(ro, path)
+    return {"file": "ref_checkpoint.dmth", "file_fnv": hx(ro.fnv1a(np.frombuffer(data, np.uint8))),
+            "bytes": len(data), "workers": 3, "root_seed": 1234, "matrices": digests,
+            "recipe": "create(3,20x18,7x5,f32); create(0,12x10,4x10,f16); create(2,9x14,2x14,f64); "
+                      "replicate(2); scatter(1, arange(360)*0.25-7)", "restored_ok": r}
+
+
+def RefSession_restore(ro, path):
+    from oracle import RefSession
+    rs = RefSession.restore(ro, path)
+    ok = all(rs.describe(m)[0] >= 0 for m in (1, 2, 3))
+    rs.close()
+    return ok
+
+
 def main():
     ro = RefOracle()
     g = {"generator": "tests/golden/make_golden.py (reference: /root/reference/proj/include/gridgemm)",
          "kat": [kat(ro, 256, 1.0, 0.0, False), kat(ro, 256, 1.5, -0.5, False),
                  kat(ro, 2048, 1.0, 0.0, True)],
          "sweep": sweep(ro), "fc": fc_case(ro), "errors": errors(ro), "layouts": layouts(ro), "plans": plans(ro),
+         "fills_p": fills_p(ro), "reshape": reshapes(ro), "sums": sums(ro),
+         "replication": replication(ro), "update_block": update_blocks(ro), "half_gemm": half_gemm(ro),
+         "checkpoint": checkpoint_fixture(ro),
          "fills": fills(ro),
          "matrix_seeds": {str(i): hx(ro.lib.ref_mix64_2(42, i)) for i in range(1, 6)}}
     with open(OUT, "w") as f:

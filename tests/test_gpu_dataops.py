@@ -1,0 +1,182 @@
+"""GPU parity of the SURVEY 8(f) operations against the reference's own outputs
+(tests/golden/golden.json, tests/golden/ref_checkpoint.dmth):
+
+* seeded fills at Half16 / Single32 / Double64: bit-exact;
+* reshape with narrowing before the link / widening at the receiver: bit-exact;
+* add_row_col_sum, deterministic and salted fast mode: bit-exact (same fold order);
+* replicate + lazy version-checked replica_read: bit-exact, same descriptor effects;
+* update_block: bit-exact, version bump;
+* Half16 GEMM (fp32 compute, one rounding on store): within 1 half ulp;
+* DMTH checkpoint: the reference's file restores bit-exactly, and the same
+  session state checkpoints to a byte-identical file.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1604_01416_b200 import (Config, FillKind, IntegrityError, Precision, Session,
+                                   UnsupportedError, make_layout)
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLDEN = json.load(open(os.path.join(HERE, "golden", "golden.json")))
+
+
+def fnv(arr):
+    from oracle import COracle
+    return f"{COracle().fnv1a(np.ascontiguousarray(arr)):016x}"
+
+
+def session(P, seed):
+    return Session(Config(worker_count=P, root_seed=seed, devices=[0] * P))
+
+
+@pytest.mark.parametrize("i", range(len(GOLDEN["fills_p"])))
+def test_fill_precisions(cuda, i):
+    f = GOLDEN["fills_p"][i]
+    with session(f["layout"][5], f["root_seed"]) as s:
+        m = s.create_matrix(make_layout(*f["layout"]), Precision(f["precision"]), FillKind.SeededRandom)
+        assert fnv(s.gather(m)) == f["fnv"]
+
+
+@pytest.mark.parametrize("i", range(len(GOLDEN["reshape"])))
+def test_reshape(cuda, i):
+    c = GOLDEN["reshape"][i]
+    P = c["workers"]
+    with session(P, c["root_seed"]) as s:
+        a = s.create_matrix(make_layout(*c["src"], P), Precision(c["src_prec"]), FillKind.SeededRandom)
+        assert fnv(s.gather(a)) == c["src_fnv"]
+        b = s.reshape(a, make_layout(*c["dst"], P), Precision(c["dst_prec"]))
+        assert b == c["dst_id"]
+        assert fnv(s.gather(b)) == c["dst_fnv"]
+
+
+@pytest.mark.parametrize("i", range(0, len(GOLDEN["sums"]), 3))
+def test_row_col_sums(cuda, i):
+    c = GOLDEN["sums"][i]
+    with session(c["workers"], c["root_seed"]) as s:
+        m = s.create_matrix(make_layout(*c["layout"]), Precision(c["precision"]), FillKind.SeededRandom)
+        assert fnv(s.gather(m)) == c["in_fnv"]
+        o = s.add_row_col_sum(m, c["axis"], c["det"])
+        o2 = s.add_row_col_sum(m, c["axis"], c["det"])
+        assert o == c["out_id"]
+        assert s.descriptor(o).layout.to_string() == c["out_layout"]
+        assert fnv(s.gather(o)) == c["out_fnv"]
+        assert fnv(s.gather(o2)) == c["out2_fnv"]
+
+
+@pytest.mark.parametrize("i", range(len(GOLDEN["replication"])))
+def test_replication(cuda, i):
+    c = GOLDEN["replication"][i]
+    P = c["workers"]
+    with session(P, c["root_seed"]) as s:
+        m = s.create_matrix(make_layout(*c["layout"]), fill=FillKind.SeededRandom)
+        s.replicate(m, True)
+        d = s.descriptor(m)
+        assert [d.version, d.replica_version, d.replicated] == c["desc_after_enable"]
+        assert fnv(s.replica_read(m, P - 1)) == c["read0_fnv"]
+        s.scatter(m, (np.arange(30 * 22, dtype=np.float32).reshape(30, 22) / 7.0).astype(np.float32))
+        d = s.descriptor(m)
+        assert [d.version, d.replica_version, d.replicated] == c["desc_after_scatter"]
+        assert fnv(s.replica_read(m, 0)) == c["read1_fnv"]
+        d = s.descriptor(m)
+        assert [d.version, d.replica_version, d.replicated] == c["desc_after_read"]
+
+
+def test_fresh_replicas_feed_gemm(cuda):
+    """A replicated operand is read from local replicas: zero peer bytes."""
+    P = 4
+    with session(P, 5) as s:
+        lay = make_layout(3, 64, 64, 32, 32, P)
+        a, b, c = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(3))
+        s.replicate(a, True)
+        s.replicate(b, True)
+        s.reset_worker_stats()
+        s.general_gemm(1.0, a, b, 0.0, c)
+        assert sum(s.worker_stats(w).peer_bytes_read for w in range(P)) == 0
+
+
+def test_update_block(cuda):
+    c = GOLDEN["update_block"][0]
+    with session(c["workers"], c["root_seed"]) as s:
+        m = s.create_matrix(make_layout(*c["layout"]), fill=FillKind.SeededRandom)
+        s.update_block(m, *c["block"], np.linspace(-3, 3, 20 * 7, dtype=np.float32).reshape(20, 7))
+        assert s.descriptor(m).version == c["version"]
+        assert fnv(s.gather(m)) == c["fnv"]
+
+
+@pytest.mark.parametrize("i", range(len(GOLDEN["half_gemm"])))
+def test_half_gemm(cuda, i):
+    from oracle import RefOracle, ref_available
+    c = GOLDEN["half_gemm"][i]
+    P = c["workers"]
+    with session(P, c["root_seed"]) as s:
+        a = s.create_matrix(make_layout(3, 40, 40, 16, 12, P), Precision.Half16, FillKind.SeededRandom)
+        b = s.create_matrix(make_layout(0, 40, 40, 10, 40, P), Precision.Half16, FillKind.SeededRandom)
+        cm = s.create_matrix(make_layout(2, 40, 40, 9, 40, P), Precision.Half16, FillKind.SeededRandom)
+        A, B, C0 = s.gather(a), s.gather(b), s.gather(cm)
+        assert (fnv(A), fnv(B), fnv(C0)) == (c["A"], c["B"], c["C0"])
+        s.general_gemm(1.5, a, b, -0.5, cm, c["ta"], c["tb"])
+        got = s.gather(cm)
+    if not ref_available():
+        pytest.skip("oracle/_ref not shipped")
+    ro = RefOracle()
+    with ro.session(P, c["root_seed"]) as rs:
+        ra = rs.create_p(3, 40, 40, 16, 12, P, 0)
+        rb = rs.create_p(0, 40, 40, 10, 40, P, 0)
+        rc = rs.create_p(2, 40, 40, 9, 40, P, 0)
+        rs.general_gemm(1.5, ra, rb, -0.5, rc, c["ta"], c["tb"])
+        want = rs.gather_p(rc)
+    assert fnv(want) == c["C"]
+    ulp = np.abs(got.view(np.int16).astype(np.int32) - want.view(np.int16).astype(np.int32))
+    assert ulp.max() <= 1 and (ulp == 0).mean() > 0.9
+
+
+def test_double_gemm_unsupported(cuda):
+    with session(1, 1) as s:
+        lay = make_layout(0, 8, 8, 8, 8, 1)
+        a, b, c = (s.create_matrix(lay, Precision.Double64, FillKind.SeededRandom) for _ in range(3))
+        with pytest.raises(UnsupportedError):
+            s.general_gemm(1.0, a, b, 0.0, c)
+
+
+def test_restore_reference_checkpoint(cuda, tmp_path):
+    ck = GOLDEN["checkpoint"]
+    path = os.path.join(HERE, "golden", ck["file"])
+    s = Session.restore(path, Config(devices=[0] * ck["workers"]))
+    try:
+        assert s.worker_count() == ck["workers"]
+        for mid, want in ck["matrices"].items():
+            assert fnv(s.gather(int(mid))) == want
+        assert s.descriptor(1).version == 1 and s.descriptor(2).replicated
+        # the same session state checkpoints to a byte-identical file
+        out = str(tmp_path / "ours.dmth")
+        s.checkpoint(out)
+        assert fnv(np.frombuffer(open(out, "rb").read(), np.uint8)) == ck["file_fnv"]
+    finally:
+        s.close()
+
+
+def test_checkpoint_rebuilt_state_matches_reference_file(cuda, tmp_path):
+    ck = GOLDEN["checkpoint"]
+    with session(3, ck["root_seed"]) as s:
+        a = s.create_matrix(make_layout(3, 20, 18, 7, 5, 3), Precision.Single32, FillKind.SeededRandom)
+        b = s.create_matrix(make_layout(0, 12, 10, 4, 10, 3), Precision.Half16, FillKind.SeededRandom)
+        s.create_matrix(make_layout(2, 9, 14, 2, 14, 3), Precision.Double64, FillKind.SeededRandom)
+        s.replicate(b, True)
+        s.scatter(a, (np.arange(20 * 18, dtype=np.float32).reshape(20, 18) * 0.25 - 7).astype(np.float32))
+        out = str(tmp_path / "rebuilt.dmth")
+        s.checkpoint(out)
+    assert fnv(np.frombuffer(open(out, "rb").read(), np.uint8)) == ck["file_fnv"]
+
+
+def test_checkpoint_corruption_detected(cuda, tmp_path):
+    ck = GOLDEN["checkpoint"]
+    data = bytearray(open(os.path.join(HERE, "golden", ck["file"]), "rb").read())
+    data[100] ^= 0x01
+    bad = tmp_path / "bad.dmth"
+    bad.write_bytes(bytes(data))
+    with pytest.raises(IntegrityError):
+        Session.restore(str(bad), Config(devices=[0] * 3))
