@@ -113,6 +113,49 @@ def main():
         results["fc_bwd"] = orc.rel_frobenius(dXh, orc.local_gemm(1.0, Wh, False, dYh, False, 0.0))
     s.close()
 
+    # 4. SURVEY 8(f) ops over IPC: reshape (narrowing via exchange arenas),
+    #    row/col sums, replication, checkpoint -- digests must equal the
+    #    reference's (golden cases with this worker count)
+    ok = True
+    for c in [g for g in GOLDEN["reshape"] if g["workers"] == world][:6]:
+        s = session(c["root_seed"])
+        a = s.create_matrix(dm.make_layout(*c["src"], world), dm.Precision(c["src_prec"]), dm.FillKind.SeededRandom)
+        b = s.reshape(a, dm.make_layout(*c["dst"], world), dm.Precision(c["dst_prec"]))
+        got = s.gather(b)
+        if rank == 0:
+            ok &= f"{orc.fnv1a(got):016x}" == c["dst_fnv"]
+        s.close()
+    results["reshape_ok"] = ok
+    ok = True
+    for c in [g for g in GOLDEN["sums"] if g["workers"] == world][::5]:
+        s = session(c["root_seed"])
+        m = s.create_matrix(dm.make_layout(*c["layout"]), dm.Precision(c["precision"]), dm.FillKind.SeededRandom)
+        o = s.add_row_col_sum(m, c["axis"], c["det"])
+        got = s.gather(o)
+        if rank == 0:
+            ok &= f"{orc.fnv1a(got):016x}" == c["out_fnv"]
+        s.close()
+    results["sums_ok"] = ok
+    s = session(71)
+    m = s.create_matrix(dm.make_layout(3, 30, 22, 7, 6, world), fill=dm.FillKind.SeededRandom)
+    s.replicate(m, True)
+    full = s.gather(m)
+    rd = s.replica_read(m, world - 1)
+    at_reader = s.gather(m, root=world - 1)  # collective: every rank calls it
+    results[f"replica_ok_r{rank}"] = bool(rank != world - 1 or rd.tobytes() == at_reader.tobytes())
+    ck = os.path.join(ROOT, "gpurun_out", f"spmd_ck_{world}.dmth")
+    os.makedirs(os.path.dirname(ck), exist_ok=True)
+    s.checkpoint(ck)
+    s.close()
+    dist.barrier()
+    obj = [dm.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    r = dm.Session.restore(ck, dm.Config(mode="spmd", rank=rank, devices=[local], nccl_id=obj[0]))
+    back = r.gather(m)
+    if rank == 0:
+        results["checkpoint_roundtrip"] = bool(back.tobytes() == full.tobytes())
+    r.close()
+
     allres = [None] * world
     dist.all_gather_object(allres, results)
     if rank == 0:

@@ -49,3 +49,5 @@ def test_spmd_parity(cuda):
     assert res["sweep_worst"] <= 1e-5
     assert res["fc_fwd"] <= 1e-5 and res["fc_bwd"] <= 1e-5
     assert all(res[f"bwd_peer_bytes_r{r}"] == 0 for r in range(n))
+    assert res["reshape_ok"] and res["sums_ok"] and res["checkpoint_roundtrip"]
+    assert all(res[f"replica_ok_r{r}"] for r in range(n))
