@@ -208,6 +208,15 @@ int dm_descriptor_digest(dm_session* s, uint64_t* master, uint64_t* workers, int
 int dm_block_device_ptr(dm_session* s, dm_matrix_id id, int row, int col, void** ptr,
                         int* device);
 int dm_barrier(dm_session* s);
+/* Asynchronous command mode (on != 0): dm_scatter / dm_gather / dm_general_gemm
+ * enqueue stream-ordered work on copy-engine / compute / pull streams and
+ * return; per-matrix read/write events (and device-side NCCL barriers across
+ * ranks) keep them ordered, so H2D, tensor-core and D2H work overlap.  Host
+ * buffers passed to scatter/gather must stay valid and unmodified until
+ * dm_barrier() or dm_set_async(s, 0); other commands drain first and run
+ * synchronously.  The reference's calls are synchronous (session.hpp:585-605);
+ * this mode is the B200 extension of the same command stream. */
+int dm_set_async(dm_session* s, int on);
 /* Device-time markers on worker `worker`'s GEMM stream (bench timing):
  * record CUDA event `slot` (0..15); elapsed ms between two recorded slots. */
 int dm_marker_record(dm_session* s, int worker, int slot);

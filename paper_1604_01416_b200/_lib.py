@@ -90,6 +90,7 @@ def _load() -> C.CDLL:
         "dm_descriptor_digest": (C.c_int, [vp, P(u64), P(u64), C.c_int]),
         "dm_block_device_ptr": (C.c_int, [vp, u64, C.c_int, C.c_int, P(vp), P(C.c_int)]),
         "dm_barrier": (C.c_int, [vp]),
+        "dm_set_async": (C.c_int, [vp, C.c_int]),
         "dm_marker_record": (C.c_int, [vp, C.c_int, C.c_int]),
         "dm_marker_elapsed": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float)]),
         "dm_local_gemm_f32": (C.c_int, [f64, vp, i64, C.c_int, vp, i64, C.c_int, f64, vp, i64,
@@ -118,5 +119,5 @@ EXPORTED = [
     "dm_cached_backward_gemm", "dm_worker_count", "dm_local_workers", "dm_descriptor_get",
     "dm_pool_stats_get", "dm_pool_trim", "dm_worker_stats_get", "dm_worker_stats_reset",
     "dm_set_gemm_timing", "dm_worker_seed", "dm_descriptor_digest", "dm_block_device_ptr",
-    "dm_barrier", "dm_marker_record", "dm_marker_elapsed", "dm_local_gemm_f32", "dm_local_gemm_f32_ex", "dm_fill_seeded_f32",
+    "dm_barrier", "dm_set_async", "dm_marker_record", "dm_marker_elapsed", "dm_local_gemm_f32", "dm_local_gemm_f32_ex", "dm_fill_seeded_f32",
 ]

@@ -460,6 +460,8 @@ int dm_block_device_ptr(dm_session* s, dm_matrix_id id, int row, int col, void**
 
 int dm_barrier(dm_session* s) { return guarded([&] { S(s).barrier(); }); }
 
+int dm_set_async(dm_session* s, int on) { return guarded([&] { S(s).set_async(on != 0); }); }
+
 int dm_marker_record(dm_session* s, int worker, int slot) {
   return guarded([&] { S(s).marker_record(worker, slot); });
 }

@@ -24,6 +24,7 @@ Comm::Comm(int world, int rank, const void* nccl_id, int device)
   comm_ = c;
   dev_buf_bytes_ = 1 << 20;
   cuda_check(cudaMalloc(&dev_buf_, dev_buf_bytes_), "cudaMalloc(comm)");
+  cuda_check(cudaMalloc(&bar_buf_, 256), "cudaMalloc(barrier)");  // never reallocated
 }
 
 Comm::~Comm() {
@@ -33,16 +34,23 @@ Comm::~Comm() {
   opened_.clear();
   if (comm_) ncclCommDestroy(static_cast<ncclComm_t>(comm_));
   if (dev_buf_) cudaFree(dev_buf_);
+  if (bar_buf_) cudaFree(bar_buf_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
 void Comm::barrier() {
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
-  int* buf = static_cast<int*>(dev_buf_);
+  int* buf = static_cast<int*>(bar_buf_);
   nccl_check(ncclAllReduce(buf, buf + 1, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(comm_),
                            stream_),
              "ncclAllReduce(barrier)");
   cuda_check(cudaStreamSynchronize(stream_), "barrier sync");
+}
+
+void Comm::barrier_on(cudaStream_t s) {
+  int* buf = static_cast<int*>(bar_buf_);
+  nccl_check(ncclAllReduce(buf + 2, buf + 3, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(comm_), s),
+             "ncclAllReduce(device barrier)");
 }
 
 std::vector<std::uint8_t> Comm::allgather(const void* data, std::size_t bytes) {

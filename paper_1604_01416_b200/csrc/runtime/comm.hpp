@@ -31,6 +31,9 @@ class Comm {
   // Stream-ordered all-reduce of one int followed by a host wait: returns
   // once every rank has reached the same point.
   void barrier();
+  // Same collective enqueued on `s` without a host wait: work issued on `s`
+  // afterwards starts only once every rank's `s` reached this point.
+  void barrier_on(cudaStream_t s);
   // Fixed-size all-gather of host bytes; result is world * bytes.
   std::vector<std::uint8_t> allgather(const void* data, std::size_t bytes);
 
@@ -46,6 +49,7 @@ class Comm {
   int world_ = 1, rank_ = 0, device_ = 0;
   cudaStream_t stream_ = nullptr;
   void* dev_buf_ = nullptr;
+  void* bar_buf_ = nullptr;
   std::size_t dev_buf_bytes_ = 0;
   struct Mapping {
     void* ptr = nullptr;

@@ -62,6 +62,8 @@ Session::Session(const dm_session_config& cfg) {
     wk->device = dev;
     cuda_check(cudaStreamCreateWithFlags(&wk->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&wk->side, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&wk->h2d, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&wk->d2h, cudaStreamNonBlocking), "cudaStreamCreate");
     wk->pool = std::make_unique<DevicePool>(dev);
     wk->seed = mix64(root_seed_, static_cast<std::uint64_t>(w));  // exec_seed, ops.hpp:1140
     workers_[w] = std::move(wk);
@@ -115,14 +117,21 @@ Session::~Session() {
     w->cache.clear();
     w->replicas.clear();
     w->arena = DeviceBuffer();
+    w->inflight.clear();
+    for (auto* v : {&w->event_pool, &w->events_used})
+      for (cudaEvent_t e : *v) cudaEventDestroy(e);
     w->pool.reset();
     cudaStreamDestroy(w->stream);
     cudaStreamDestroy(w->side);
+    cudaStreamDestroy(w->h2d);
+    cudaStreamDestroy(w->d2h);
   }
 }
 
 void Session::shutdown() {
   if (!live_) return;
+  if (async_) drain();
+  async_ = false;
   sync_local();
   if (comm_) {
     for (const auto& [id, d] : table_) comm_->unpublish(id);
@@ -186,12 +195,117 @@ void Session::sync_local() {
   for (auto& w : workers_) {
     if (!w) continue;
     DeviceGuard g(w->device);
-    cuda_check(cudaStreamSynchronize(w->side), "stream sync");
-    cuda_check(cudaStreamSynchronize(w->stream), "stream sync");
+    for (cudaStream_t st : {w->h2d, w->side, w->stream, w->d2h})
+      cuda_check(cudaStreamSynchronize(st), "stream sync");
   }
 }
 
+// ------------------------------------------------------ asynchronous mode
+
+cudaEvent_t Session::ev_get(Worker& w) {
+  cudaEvent_t e;
+  if (w.event_pool.empty()) {
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+  } else {
+    e = w.event_pool.back();
+    w.event_pool.pop_back();
+  }
+  w.events_used.push_back(e);
+  return e;
+}
+
+void Session::mark_write(Worker& w, cudaStream_t s, MatrixId id) {
+  Track& t = w.tracks[id];
+  t.write = ev_get(w);
+  cuda_check(cudaEventRecord(t.write, s), "cudaEventRecord");
+  t.reads.clear();
+}
+
+void Session::mark_read(Worker& w, cudaStream_t s, MatrixId id) {
+  cudaEvent_t e = ev_get(w);
+  cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+  w.tracks[id].reads.push_back(e);
+}
+
+// `s` waits for the last write of `id` on every local worker (cross-device
+// waits are legal inside one process).
+void Session::wait_writes(cudaStream_t s, MatrixId id) {
+  for (auto& v : workers_) {
+    if (!v) continue;
+    auto it = v->tracks.find(id);
+    if (it != v->tracks.end() && it->second.write)
+      cuda_check(cudaStreamWaitEvent(s, it->second.write, 0), "cudaStreamWaitEvent");
+  }
+}
+
+// ... and for every read of `id` issued since (before overwriting it).
+void Session::wait_all(cudaStream_t s, MatrixId id) {
+  wait_writes(s, id);
+  for (auto& v : workers_) {
+    if (!v) continue;
+    auto it = v->tracks.find(id);
+    if (it == v->tracks.end()) continue;
+    for (cudaEvent_t e : it->second.reads) cuda_check(cudaStreamWaitEvent(s, e, 0), "cudaStreamWaitEvent");
+  }
+}
+
+// SPMD: every rank's work issued on `s` so far completes before anything
+// issued on `s` afterwards (NCCL all-reduce on the stream, no host wait).
+void Session::device_barrier(cudaStream_t s) {
+  if (comm_) comm_->barrier_on(s);
+}
+
+void Session::reap_inflight(Worker& w) {
+  while (!w.inflight.empty() && cudaEventQuery(w.inflight.front().done) == cudaSuccess) {
+    for (cudaEvent_t e : w.inflight.front().events) cudaEventDestroy(e);
+    w.inflight.pop_front();
+  }
+  cudaGetLastError();  // cudaErrorNotReady is not an error here
+}
+
+// Complete every outstanding asynchronous command on every rank.
+void Session::drain() {
+  sync_local();
+  for (auto& w : workers_) {
+    if (!w) continue;
+    DeviceGuard g(w->device);
+    for (auto& f : w->inflight)
+      for (cudaEvent_t e : f.events) cudaEventDestroy(e);
+    w->inflight.clear();
+    w->tracks.clear();
+    w->event_pool.insert(w->event_pool.end(), w->events_used.begin(), w->events_used.end());
+    w->events_used.clear();
+  }
+  collect_timing();
+  if (comm_) comm_->barrier();
+}
+
+SyncScope::SyncScope(Session* ss) : s(ss), prev(ss != nullptr && ss->async_mode()) {
+  if (prev) s->set_async(false);
+}
+SyncScope::~SyncScope() {
+  if (prev) {
+    try {
+      s->set_async(true);
+    } catch (...) {
+    }
+  }
+}
+
+void Session::set_async(bool on) {
+  require_live();
+  if (async_ && !on) {
+    drain();
+    async_ = false;
+    end_command();  // coherence check of everything issued asynchronously
+    return;
+  }
+  if (!async_ && on) sync_local();
+  async_ = on;
+}
+
 void Session::end_command() {
+  if (async_) return;  // stream-ordered; completed by barrier()/drain()
   sync_local();
   collect_timing();
   if (comm_) {
@@ -217,6 +331,10 @@ void Session::end_command() {
 }
 
 void Session::barrier() {
+  if (async_) {
+    drain();
+    return;
+  }
   sync_local();
   if (comm_) comm_->barrier();
 }
@@ -245,6 +363,7 @@ float Session::marker_elapsed(int w, int a, int b) {
 MatrixId Session::create_matrix(const LayoutSpec& layout, Precision p, FillKind fill,
                                 const void* host) {
   require_live();
+  SyncScope scope(this);
   validate_layout_workers(layout);
   if (fill == FillKind::FromHost && host == nullptr)
     throw UsageError("create_matrix: FromHost requires host data");
@@ -297,6 +416,7 @@ void Session::materialize(const MatrixDescriptor& d, bool seeded) {
 
 void Session::destroy_matrix(MatrixId id) {
   require_live();
+  SyncScope scope(this);
   descriptor(id);
   sync_local();
   if (comm_) {
@@ -337,6 +457,15 @@ void Session::scatter(MatrixId id, const void* host, std::int64_t rows, std::int
   for (auto& w : workers_) {
     if (!w) continue;
     DeviceGuard guard(w->device);
+    cudaStream_t st = w->stream;
+    if (async_) {
+      // copy engine stream; wait until nobody (here or on a peer) still reads
+      // or writes the blocks we are about to overwrite
+      reap_inflight(*w);
+      st = w->h2d;
+      wait_all(st, id);
+      device_barrier(st);
+    }
     for (BlockCoord c : owned_coords(d.layout, w->id)) {
       StoredBlock& blk = w->owned.at({id, c});
       const char* src = static_cast<const char*>(host) +
@@ -346,9 +475,10 @@ void Session::scatter(MatrixId id, const void* host, std::int64_t rows, std::int
                                    static_cast<std::size_t>(g.global_cols) * esz,
                                    static_cast<std::size_t>(blk.cols) * esz,
                                    static_cast<std::size_t>(blk.rows), cudaMemcpyHostToDevice,
-                                   w->stream),
+                                   st),
                  "scatter H2D");
     }
+    if (async_) mark_write(*w, st, id);
   }
   bump_version(id);  // runtime_types.hpp:289-292
   end_command();
@@ -369,6 +499,8 @@ void Session::gather(MatrixId id, void* host, std::int64_t rows, std::int64_t co
   if (rows != g.global_rows || cols != g.global_cols)
     throw ShapeError("gather: host buffer shape does not match the matrix");
   if (root < -1 || root >= P_) throw UsageError("gather: root out of range");
+  // SPMD gathers to a root read peer blocks through IPC: run synchronously
+  SyncScope scope(async_ && comm_ && root != -1 ? this : nullptr);
   const bool all_blocks = !comm_ || root == rank_;
   const bool any = !comm_ || root == -1 || root == rank_;
   if (any && host == nullptr) throw UsageError("gather: null host pointer");
@@ -384,15 +516,20 @@ void Session::gather(MatrixId id, void* host, std::int64_t rows, std::int64_t co
         const void* src = block_src(id, {r, c}, me);
         Worker& issuer = ow ? *ow : me;
         DeviceGuard guard(issuer.device);
+        cudaStream_t st = issuer.stream;
+        if (async_) {
+          st = issuer.d2h;
+          wait_writes(st, id);
+        }
         char* dst = static_cast<char*>(host) +
                     (static_cast<std::int64_t>(r) * g.block_rows * g.global_cols +
                      static_cast<std::int64_t>(c) * g.block_cols) * esz;
         cuda_check(cudaMemcpy2DAsync(dst, static_cast<std::size_t>(g.global_cols) * esz, src,
                                      static_cast<std::size_t>(bc) * esz,
                                      static_cast<std::size_t>(bc) * esz,
-                                     static_cast<std::size_t>(br), cudaMemcpyDefault,
-                                     issuer.stream),
+                                     static_cast<std::size_t>(br), cudaMemcpyDefault, st),
                    "gather D2H");
+        if (async_) mark_read(issuer, st, id);
       }
   }
   end_command();
@@ -648,6 +785,15 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     Worker& w = *wp;
     DeviceGuard guard(w.device);
     WorkerPlan plan = plan_worker(g, w.id, pol);
+    if (async_) {
+      // pulls start once A and B are written everywhere; C is overwritten only
+      // after its previous writes and reads (e.g. an async gather) finished
+      reap_inflight(w);
+      wait_writes(w.side, g.a);
+      wait_writes(w.side, g.b);
+      device_barrier(w.side);  // every rank, even one without C blocks
+      wait_all(w.stream, g.c);
+    }
     if (plan.tasks.empty()) continue;
     Live& lv = live[w.id];
     // Producer lockstep needs the GEMM's CTAs co-resident: off when another
@@ -794,7 +940,21 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
       }
       cuda_check(cudaEventRecord(gemm_done[buf], w.stream), "event");
     }
+    if (async_) {
+      mark_write(w, w.stream, g.c);
+      mark_read(w, w.side, g.a);
+      mark_read(w, w.side, g.b);
+      // panel planes live until the last GEMM of this command has run
+      Worker::Inflight f;
+      cuda_check(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(f.done, w.stream), "event");
+      f.bufs = std::move(lv.bufs);
+      f.events = std::move(lv.events);
+      f.events.push_back(f.done);
+      w.inflight.push_back(std::move(f));
+    }
   }
+  if (async_) return;
   sync_local();
   for (auto& wp : workers_) {
     if (!wp) continue;
@@ -846,6 +1006,7 @@ void Session::general_gemm(double alpha, MatrixId a, MatrixId b, double beta, Ma
 void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
                           bool tb, bool cache_a) {
   require_live();
+  SyncScope scope(this);
   GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, cache_a);
   validate_cyclic(g, nullptr);
   run_gemm(g, SourcePolicy::Peer);
@@ -866,6 +1027,7 @@ void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, Mat
 
 void Session::cached_backward_gemm(MatrixId w_id, MatrixId dy, MatrixId dx) {
   require_live();
+  SyncScope scope(this);
   GemmArgs g = gemm_command(1.0, w_id, dy, 0.0, dx, false, false, false);
   std::vector<WorkerId> strip_owners;
   validate_cyclic(g, &strip_owners);

@@ -20,6 +20,7 @@
 
 #include <cuda_runtime.h>
 
+#include <deque>
 #include <map>
 #include <memory>
 #include <set>
@@ -57,11 +58,28 @@ struct GemmArgs {
 
 enum class SourcePolicy { Peer, LocalOnly };
 
+// Outstanding device work on one matrix (asynchronous command mode): the last
+// write and the reads issued since, as events on whichever stream ran them.
+struct Track {
+  cudaEvent_t write = nullptr;
+  std::vector<cudaEvent_t> reads;
+};
+
 struct Worker {
   int id = 0;
   int device = 0;
   cudaStream_t stream = nullptr;  // GEMM stream
   cudaStream_t side = nullptr;    // pull/split stream
+  cudaStream_t h2d = nullptr;     // copy engine, host -> device (async scatter)
+  cudaStream_t d2h = nullptr;     // copy engine, device -> host (async gather)
+  std::map<MatrixId, Track> tracks;
+  std::vector<cudaEvent_t> event_pool, events_used;
+  struct Inflight {  // buffers of an asynchronous GEMM, released once `done` fires
+    cudaEvent_t done = nullptr;
+    std::vector<DeviceBuffer> bufs;
+    std::vector<cudaEvent_t> events;
+  };
+  std::deque<Inflight> inflight;
   std::unique_ptr<DevicePool> pool;
   std::map<MatrixId, MatrixDescriptor> descriptors;
   std::map<BlockKey, StoredBlock> owned;
@@ -122,6 +140,12 @@ class Session {
   std::vector<std::uint64_t> worker_digests() const;
   void* block_device_ptr(MatrixId id, BlockCoord c, int* device) const;
   void barrier();
+  // Asynchronous command mode: create/scatter/gather/general_gemm enqueue
+  // stream-ordered work and return; dependencies are tracked per matrix with
+  // events (device-side NCCL barriers between ranks in SPMD).  Host buffers
+  // must stay valid and unmodified until barrier()/set_async(false).
+  void set_async(bool on);
+  bool async_mode() const { return async_; }
   void marker_record(int w, int slot);
   float marker_elapsed(int w, int a, int b);
 
@@ -156,6 +180,14 @@ class Session {
   void* arena(int w, std::size_t* bytes);
   void ensure_arenas(std::size_t bytes);
   void mid_barrier();
+  void drain();
+  void reap_inflight(Worker& w);
+  cudaEvent_t ev_get(Worker& w);
+  void mark_write(Worker& w, cudaStream_t s, MatrixId id);
+  void mark_read(Worker& w, cudaStream_t s, MatrixId id);
+  void wait_writes(cudaStream_t s, MatrixId id);
+  void wait_all(cudaStream_t s, MatrixId id);
+  void device_barrier(cudaStream_t s);
   Worker& worker(int w);
   const Worker& worker(int w) const;
   Worker* local(int w);
@@ -188,6 +220,7 @@ class Session {
   bool coherence_ = true;
   bool live_ = false;
   bool timing_ = false;
+  bool async_ = false;
   std::uint64_t root_seed_ = 0;
   std::uint64_t next_matrix_id_ = 1;
   std::vector<std::unique_ptr<Worker>> workers_;  // index = worker id; null if not local
@@ -197,6 +230,17 @@ class Session {
   std::size_t arena_bytes_ = 0;               // replicated: every worker's arena size
   std::vector<void*> arena_ptrs_;             // per worker (peer-readable)
   std::unique_ptr<Comm> comm_;
+};
+
+// Commands without an asynchronous form drain outstanding work first and run
+// synchronously (their end_command syncs and checks coherence).
+struct SyncScope {
+  Session* s;
+  bool prev;
+  explicit SyncScope(Session* ss);
+  ~SyncScope();
+  SyncScope(const SyncScope&) = delete;
+  SyncScope& operator=(const SyncScope&) = delete;
 };
 
 }  // namespace dm

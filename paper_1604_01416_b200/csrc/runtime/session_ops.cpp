@@ -101,6 +101,7 @@ void* Session::arena(int w, std::size_t* bytes) {
 void Session::update_block(MatrixId id, BlockCoord c, const void* host, std::int64_t rows,
                            std::int64_t cols) {
   require_live();
+  SyncScope scope(this);
   const MatrixDescriptor d = descriptor(id);
   auto [br, bc] = block_extent(d.layout.grid, c);
   if (rows != br || cols != bc)
@@ -150,6 +151,7 @@ void Session::sync_replicas(MatrixId id) {
 // ReplicateExec (ops.hpp:660-702) + descriptor effects (runtime_types.hpp:302-307).
 void Session::replicate(MatrixId id, bool enable) {
   require_live();
+  SyncScope scope(this);
   descriptor(id);
   if (enable && P_ > 1) sync_replicas(id);
   if (!enable)
@@ -173,6 +175,7 @@ void Session::replicate(MatrixId id, bool enable) {
 void Session::replica_read(MatrixId id, int reader, void* host, std::int64_t rows,
                            std::int64_t cols) {
   require_live();
+  SyncScope scope(this);
   const MatrixDescriptor d0 = descriptor(id);
   if (!d0.replicated) throw UsageError("replica_read: matrix is not replicated");
   if (reader < 0 || reader >= P_) throw UsageError("unknown worker id");
@@ -216,6 +219,7 @@ void Session::replica_read(MatrixId id, int reader, void* host, std::int64_t row
 // narrower precision), widening at the receiver.
 MatrixId Session::reshape(MatrixId src, const LayoutSpec& layout, Precision p) {
   require_live();
+  SyncScope scope(this);
   const MatrixDescriptor sd = descriptor(src);
   validate_layout_workers(layout);
   const BlockGrid& gs = sd.layout.grid;
@@ -302,6 +306,7 @@ MatrixId Session::reshape(MatrixId src, const LayoutSpec& layout, Precision p) {
 // permutation (fast mode), so both modes are bit-exact with the reference.
 MatrixId Session::add_row_col_sum(MatrixId id, int axis, bool deterministic) {
   require_live();
+  SyncScope scope(this);
   const MatrixDescriptor d = descriptor(id);
   const BlockGrid& g = d.layout.grid;
   const bool rows_axis = axis == 0;
@@ -418,6 +423,7 @@ std::vector<int> checkpoint_block_order(const LayoutSpec& layout) {
 // SPMD rank 0 reads every peer block through its IPC mapping and writes.
 void Session::checkpoint(const std::string& path) {
   require_live();
+  SyncScope scope(this);
   const bool writer = !comm_ || rank_ == 0;
   if (writer) {
     std::vector<unsigned char> out;

@@ -335,7 +335,17 @@ class Session:
         return p.value, d.value
 
     def barrier(self):
+        """Complete all outstanding (asynchronous) work on every worker/rank."""
         _check(lib.dm_barrier(self._h))
+        self._async_keep = []
+
+    def set_async(self, on: bool):
+        """Asynchronous command mode (dm_set_async): scatter / gather /
+        general_gemm return once enqueued; host buffers must stay alive and
+        unmodified until barrier() or set_async(False)."""
+        _check(lib.dm_set_async(self._h, int(on)))
+        if not on:
+            self._async_keep = []
 
     def marker_record(self, worker: int, slot: int):
         """Record device-time marker `slot` on the worker's GEMM stream."""
@@ -366,6 +376,13 @@ class Session:
     def destroy_matrix(self, mid: int):
         _check(lib.dm_destroy_matrix(self._h, mid))
 
+    def _keep_host(self, arr):
+        """Async mode: keep converted host arrays alive until the next barrier."""
+        keep = getattr(self, "_async_keep", None)
+        if keep is None:
+            keep = self._async_keep = []
+        keep.append(arr)
+
     @staticmethod
     def _host_in(host: np.ndarray, precision) -> np.ndarray:
         """Host data at the matrix precision.  Other dtypes are converted with
@@ -378,6 +395,7 @@ class Session:
         host = self._host_in(host, self.descriptor(mid).precision)
         if host.ndim != 2:
             raise ShapeError("scatter: host data must be 2-D")
+        self._keep_host(host)
         _check(lib.dm_scatter(self._h, mid, _host_ptr(host), host.shape[0], host.shape[1]))
 
     def gather(self, mid: int, out: Optional[np.ndarray] = None, root: int = 0) -> np.ndarray:

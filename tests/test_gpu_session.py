@@ -183,3 +183,38 @@ def test_fresh_cache_serves_repeated_forward(cuda):
         s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
         assert sum(s.worker_stats(w).peer_bytes_read for w in range(P)) > 0
         assert relfro(s.gather(Y), ref_gemm(1.0, np.ones((fin, fout), np.float32), True, s.gather(X), False, 0.0, None)) <= TOL
+
+
+@pytest.mark.parametrize("P", [1, 4])
+def test_async_pipeline_double_buffered(cuda, P):
+    """Asynchronous mode: scatter -> gemm -> gather steps enqueue and return;
+    double-buffered matrices let H2D, GEMM and D2H of different steps overlap.
+    Results must equal the synchronous path bit for bit (same kernels, same
+    order of operations per output element)."""
+    n = 384
+    rng = np.random.default_rng(P)
+    hosts = [(rng.standard_normal((n, n)).astype(np.float32), rng.standard_normal((n, n)).astype(np.float32))
+             for _ in range(4)]
+    with Session(Config(worker_count=P, root_seed=1, devices=[0] * P)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
+        mats = [[s.create_matrix(lay) for _ in range(3)] for _ in range(2)]
+        sync_out = []
+        for A, B in hosts:
+            a, b, c = mats[0]
+            s.scatter(a, A)
+            s.scatter(b, B)
+            s.general_gemm(1.0, a, b, 0.0, c)
+            sync_out.append(s.gather(c))
+        outs = [np.empty((n, n), np.float32) for _ in hosts]
+        s.set_async(True)
+        for i, (A, B) in enumerate(hosts):
+            a, b, c = mats[i % 2]
+            s.scatter(a, A)
+            s.scatter(b, B)
+            s.general_gemm(1.0, a, b, 0.0, c)
+            s.gather(c, outs[i])
+        s.barrier()
+        s.set_async(False)
+        for got, want in zip(outs, sync_out):
+            assert got.tobytes() == want.tobytes()
+        assert s.descriptor(mats[0][2]).version == 2 + 4  # 4 sync + 2 async GEMMs on set 0
