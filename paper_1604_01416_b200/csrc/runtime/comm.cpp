@@ -22,6 +22,14 @@ Comm::Comm(int world, int rank, const void* nccl_id, int device)
   ncclComm_t c = nullptr;
   nccl_check(ncclCommInitRank(&c, world_, id, rank_), "ncclCommInitRank");
   comm_ = c;
+  // one extra communicator per device-barrier channel: NCCL orders the
+  // collectives of one communicator, so barriers on the copy and pull streams
+  // must not share one (that would chain the streams together)
+  for (auto& ch : channels_) {
+    ncclComm_t d = nullptr;
+    nccl_check(ncclCommSplit(c, 0, rank_, &d, nullptr), "ncclCommSplit");
+    ch = d;
+  }
   dev_buf_bytes_ = 1 << 20;
   cuda_check(cudaMalloc(&dev_buf_, dev_buf_bytes_), "cudaMalloc(comm)");
   cuda_check(cudaMalloc(&bar_buf_, 256), "cudaMalloc(barrier)");  // never reallocated
@@ -32,6 +40,8 @@ Comm::~Comm() {
   for (auto& [h, m] : opened_)
     if (m.ptr) cudaIpcCloseMemHandle(m.ptr);
   opened_.clear();
+  for (void* ch : channels_)
+    if (ch) ncclCommDestroy(static_cast<ncclComm_t>(ch));
   if (comm_) ncclCommDestroy(static_cast<ncclComm_t>(comm_));
   if (dev_buf_) cudaFree(dev_buf_);
   if (bar_buf_) cudaFree(bar_buf_);
@@ -47,9 +57,10 @@ void Comm::barrier() {
   cuda_check(cudaStreamSynchronize(stream_), "barrier sync");
 }
 
-void Comm::barrier_on(cudaStream_t s) {
-  int* buf = static_cast<int*>(bar_buf_);
-  nccl_check(ncclAllReduce(buf + 2, buf + 3, 1, ncclInt32, ncclSum, static_cast<ncclComm_t>(comm_), s),
+void Comm::barrier_on(cudaStream_t s, int channel) {
+  int* buf = static_cast<int*>(bar_buf_) + 4 * (channel + 1);
+  nccl_check(ncclAllReduce(buf, buf + 1, 1, ncclInt32, ncclSum,
+                           static_cast<ncclComm_t>(channels_.at(channel)), s),
              "ncclAllReduce(device barrier)");
 }
 

@@ -11,6 +11,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <map>
 #include <string>
@@ -33,7 +34,8 @@ class Comm {
   void barrier();
   // Same collective enqueued on `s` without a host wait: work issued on `s`
   // afterwards starts only once every rank's `s` reached this point.
-  void barrier_on(cudaStream_t s);
+  // `channel` selects a dedicated communicator (0: copy-in stream, 1: pulls).
+  void barrier_on(cudaStream_t s, int channel);
   // Fixed-size all-gather of host bytes; result is world * bytes.
   std::vector<std::uint8_t> allgather(const void* data, std::size_t bytes);
 
@@ -46,6 +48,7 @@ class Comm {
 
  private:
   void* comm_ = nullptr;  // ncclComm_t
+  std::array<void*, 2> channels_{};
   int world_ = 1, rank_ = 0, device_ = 0;
   cudaStream_t stream_ = nullptr;
   void* dev_buf_ = nullptr;

@@ -251,8 +251,8 @@ void Session::wait_all(cudaStream_t s, MatrixId id) {
 
 // SPMD: every rank's work issued on `s` so far completes before anything
 // issued on `s` afterwards (NCCL all-reduce on the stream, no host wait).
-void Session::device_barrier(cudaStream_t s) {
-  if (comm_) comm_->barrier_on(s);
+void Session::device_barrier(cudaStream_t s, int channel) {
+  if (comm_) comm_->barrier_on(s, channel);
 }
 
 void Session::reap_inflight(Worker& w) {
@@ -464,7 +464,7 @@ void Session::scatter(MatrixId id, const void* host, std::int64_t rows, std::int
       reap_inflight(*w);
       st = w->h2d;
       wait_all(st, id);
-      device_barrier(st);
+      device_barrier(st, 0);
     }
     for (BlockCoord c : owned_coords(d.layout, w->id)) {
       StoredBlock& blk = w->owned.at({id, c});
@@ -791,7 +791,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
       reap_inflight(w);
       wait_writes(w.side, g.a);
       wait_writes(w.side, g.b);
-      device_barrier(w.side);  // every rank, even one without C blocks
+      device_barrier(w.side, 1);  // every rank, even one without C blocks
       wait_all(w.stream, g.c);
     }
     if (plan.tasks.empty()) continue;

@@ -187,7 +187,7 @@ class Session {
   void mark_read(Worker& w, cudaStream_t s, MatrixId id);
   void wait_writes(cudaStream_t s, MatrixId id);
   void wait_all(cudaStream_t s, MatrixId id);
-  void device_barrier(cudaStream_t s);
+  void device_barrier(cudaStream_t s, int channel);
   Worker& worker(int w);
   const Worker& worker(int w) const;
   Worker* local(int w);
