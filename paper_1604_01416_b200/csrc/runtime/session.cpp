@@ -728,6 +728,26 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     plan.k0.push_back(K);
     for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
     for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
+    // If even the least-remote panel must cross a link, cut a narrow lead
+    // panel off it: only that sliver's pull is exposed before the first GEMM,
+    // the rest streams behind compute.
+    const std::int64_t lead = env_int("DM_LEAD_PANEL_K", 1024);
+    const int np0 = static_cast<int>(plan.k0.size()) - 1;
+    std::vector<std::uint64_t> rb(np0, 0);
+    for (int p = 0; p < np0; ++p)
+      for (const auto* ranges : {&plan.ar, &plan.br})
+        for (const Range& r : *ranges)
+          for (const Piece& pc : r.panels[p]) {
+            bool remote = false;
+            source_ptr(*local(w), pc.matrix, pc.coord, pol, &remote);
+            if (remote) rb[p] += pc.bytes();
+          }
+    const int best = static_cast<int>(std::min_element(rb.begin(), rb.end()) - rb.begin());
+    if (lead > 0 && rb[best] > 0 && plan.k0[best + 1] - plan.k0[best] > 2 * lead) {
+      plan.k0.insert(plan.k0.begin() + best + 1, plan.k0[best] + lead);
+      for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
+      for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
+    }
   }
   return plan;
 }
