@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -95,6 +96,7 @@ Session::Session(const dm_session_config& cfg) {
   } else {
     throw ConfigError("init: unknown session mode");
   }
+  if (const char* t = std::getenv("DM_TRACE")) trace_path_ = t;
   live_ = true;
 }
 
@@ -781,6 +783,43 @@ void Session::collect_timing() {
   }
 }
 
+cudaEvent_t Session::trace_event(cudaStream_t s) {
+  cudaEvent_t e;
+  cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+  cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+  return e;
+}
+
+// Append the recorded timeline of the last command as JSON lines (one per
+// record: worker, what, panel, start/end ms relative to the command start).
+void Session::flush_trace(const char* op) {
+  if (!tracing()) return;
+  ++trace_cmd_;
+  FILE* f = std::fopen(trace_path_.c_str(), "a");
+  for (auto& wp : workers_) {
+    if (!wp || !wp->trace_t0) continue;
+    Worker& w = *wp;
+    DeviceGuard g(w.device);
+    for (auto& r : w.trace) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, w.trace_t0, r.a);
+      cudaEventElapsedTime(&b, w.trace_t0, r.b);
+      if (f)
+        std::fprintf(f,
+                     "{\"cmd\":%llu,\"op\":\"%s\",\"rank\":%d,\"worker\":%d,\"what\":\"%s\","
+                     "\"panel\":%d,\"t0_ms\":%.4f,\"t1_ms\":%.4f,\"bytes\":%llu,\"flops\":%.6g}\n",
+                     static_cast<unsigned long long>(trace_cmd_), op, rank_, w.id, r.what.c_str(), r.panel,
+                     a, b, static_cast<unsigned long long>(r.bytes), r.flops);
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    w.trace.clear();
+    cudaEventDestroy(w.trace_t0);
+    w.trace_t0 = nullptr;
+  }
+  if (f) std::fclose(f);
+}
+
 void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   struct Live {
     std::vector<DeviceBuffer> bufs;
@@ -816,6 +855,8 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     }
     if (plan.tasks.empty()) continue;
     Live& lv = live[w.id];
+    const bool trace = tracing() && !async_;
+    if (trace) w.trace_t0 = trace_event(w.stream);
     // Producer lockstep needs the GEMM's CTAs co-resident: off when another
     // local worker shares this device (its GEMMs run concurrently).
     int sharing = 0;
@@ -907,11 +948,18 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
             (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
           }
       };
+      const std::uint64_t pulled0 = w.stats.peer_bytes_read + w.stats.local_bytes_read;
+      cudaEvent_t ta = trace ? trace_event(w.side) : nullptr;
       issue(plan.ar, pa);
       issue(plan.br, pb);
+      if (trace)
+        w.trace.push_back({"pull+split", p, w.stats.peer_bytes_read + w.stats.local_bytes_read - pulled0, 0.0,
+                           ta, trace_event(w.side)});
       cuda_check(cudaEventRecord(split_done[buf], w.side), "event");
       cuda_check(cudaStreamWaitEvent(w.stream, split_done[buf], 0), "wait");
       const std::int64_t kw = plan.k0[p + 1] - plan.k0[p];
+      cudaEvent_t tg = trace ? trace_event(w.stream) : nullptr;
+      const double flops0 = w.stats.gemm_flops;
       for (const Task& t : plan.tasks) {
         StoredBlock& cb = w.owned.at({g.c, t.c});
         Tf32x3Args a;
@@ -958,6 +1006,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         w.stats.gemm_launches += 1;
         w.stats.gemm_flops += 2.0 * static_cast<double>(a.m) * a.n * a.k;
       }
+      if (trace) w.trace.push_back({"gemm", p, 0, w.stats.gemm_flops - flops0, tg, trace_event(w.stream)});
       cuda_check(cudaEventRecord(gemm_done[buf], w.stream), "event");
     }
     if (async_) {
@@ -1021,6 +1070,7 @@ void Session::general_gemm(double alpha, MatrixId a, MatrixId b, double beta, Ma
   run_gemm(g, SourcePolicy::Peer);
   bump_version(c);  // runtime_types.hpp:296-301
   end_command();
+  flush_trace("general_gemm");
 }
 
 void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,

@@ -80,6 +80,15 @@ struct Worker {
     std::vector<cudaEvent_t> events;
   };
   std::deque<Inflight> inflight;
+  struct TraceRec {  // device timeline of one command (DM_TRACE)
+    std::string what;
+    int panel = -1;
+    std::uint64_t bytes = 0;
+    double flops = 0;
+    cudaEvent_t a = nullptr, b = nullptr;
+  };
+  std::vector<TraceRec> trace;
+  cudaEvent_t trace_t0 = nullptr;
   std::unique_ptr<DevicePool> pool;
   std::map<MatrixId, MatrixDescriptor> descriptors;
   std::map<BlockKey, StoredBlock> owned;
@@ -213,6 +222,10 @@ class Session {
   void cache_foreign_a(const GemmArgs& g);
   void record_timing(Worker& w, bool start);
   void collect_timing();
+  // device timeline (DM_TRACE=<file>): events around each panel's pulls and GEMMs
+  bool tracing() const { return !trace_path_.empty(); }
+  cudaEvent_t trace_event(cudaStream_t s);
+  void flush_trace(const char* op);
 
   int P_ = 1;
   int mode_ = DM_MODE_LOCAL;
@@ -221,6 +234,8 @@ class Session {
   bool live_ = false;
   bool timing_ = false;
   bool async_ = false;
+  std::string trace_path_;
+  std::uint64_t trace_cmd_ = 0;
   std::uint64_t root_seed_ = 0;
   std::uint64_t next_matrix_id_ = 1;
   std::vector<std::unique_ptr<Worker>> workers_;  // index = worker id; null if not local
