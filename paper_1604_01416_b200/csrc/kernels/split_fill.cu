@@ -89,6 +89,103 @@ __global__ void split_trans_kernel(const T* __restrict__ src, int64_t lds, int64
   }
 }
 
+// ---- vectorised fp32 variants: 4 consecutive elements per access, 4 accesses
+// in flight per thread.  They run concurrently with the persistent GEMM (one
+// resident block per SM at most), so bytes in flight per thread, not thread
+// count, sets their bandwidth.
+__device__ __forceinline__ void split_store4(float4 x, const Planes& p, int64_t r, int64_t k) {
+  const float v[4] = {x.x, x.y, x.z, x.w};
+  float h[4], l[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    h[u] = tf32_rne(v[u]);
+    l[u] = v[u] - h[u];
+  }
+  *reinterpret_cast<float4*>(p.hi + r * p.ldo + k) = make_float4(h[0], h[1], h[2], h[3]);
+  if (p.lo)
+    *reinterpret_cast<float4*>(p.lo + r * p.ldo + k) =
+        make_float4(tf32_rne(l[0]), tf32_rne(l[1]), tf32_rne(l[2]), tf32_rne(l[3]));
+  if (p.hi16) {
+    __nv_bfloat162 a0 = __floats2bfloat162_rn(h[0], h[1]), a1 = __floats2bfloat162_rn(h[2], h[3]);
+    __nv_bfloat162 b0 = __floats2bfloat162_rn(l[0], l[1]), b1 = __floats2bfloat162_rn(l[2], l[3]);
+    uint2 hv, lv;
+    hv.x = *reinterpret_cast<uint32_t*>(&a0);
+    hv.y = *reinterpret_cast<uint32_t*>(&a1);
+    lv.x = *reinterpret_cast<uint32_t*>(&b0);
+    lv.y = *reinterpret_cast<uint32_t*>(&b1);
+    *reinterpret_cast<uint2*>(p.hi16 + r * p.ldo16 + k) = hv;
+    *reinterpret_cast<uint2*>(p.lo16 + r * p.ldo16 + k) = lv;
+  }
+}
+
+// 32 rows x 128 k per block (32 x 8 threads); requires 16-B aligned rows.
+__global__ void split_direct_vec4_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
+                                         int64_t kcols, Planes p) {
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x * 4;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  if (k >= kcols) return;
+  float4 v[4];
+  const bool full = k + 4 <= kcols;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + threadIdx.y + 8 * i;
+    if (r < rows && full) v[i] = __ldg(reinterpret_cast<const float4*>(src + r * lds + k));
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + threadIdx.y + 8 * i;
+    if (r >= rows) continue;
+    if (full) {
+      split_store4(v[i], p, r, k);
+    } else {
+      for (int64_t kk = k; kk < kcols; ++kk) split_store(__ldg(src + r * lds + kk), p, r, kk);
+    }
+  }
+}
+
+// out[r][k] = src[k][r]: 32 k x 128 r per block through shared memory.
+__global__ void split_trans_vec4_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
+                                        int64_t kcols, Planes p) {
+  __shared__ float tile[32][128 + 4];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 128;
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  const int64_t r = r0 + threadIdx.x * 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int kl = threadIdx.y + 8 * i;
+    const int64_t k = k0 + kl;
+    if (k >= kcols) continue;
+    if (r + 4 <= rows) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + k * lds + r));
+      tile[kl][threadIdx.x * 4 + 0] = v.x;
+      tile[kl][threadIdx.x * 4 + 1] = v.y;
+      tile[kl][threadIdx.x * 4 + 2] = v.z;
+      tile[kl][threadIdx.x * 4 + 3] = v.w;
+    } else {
+      for (int u = 0; u < 4; ++u)
+        if (r + u < rows) tile[kl][threadIdx.x * 4 + u] = __ldg(src + k * lds + r + u);
+    }
+  }
+  __syncthreads();
+  // 128 r x 32 k out: thread -> one row, 16 consecutive k (4 x float4)
+  const int rl = t >> 1;
+  const int64_t ro = r0 + rl;
+  if (ro >= rows) return;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int kl = (t & 1) * 16 + 4 * j;
+    const int64_t k = k0 + kl;
+    if (k >= kcols) continue;
+    if (k + 4 <= kcols) {
+      split_store4(make_float4(tile[kl][rl], tile[kl + 1][rl], tile[kl + 2][rl], tile[kl + 3][rl]), p,
+                   ro, k);
+    } else {
+      for (int u = 0; k + u < kcols; ++u) split_store(tile[kl + u][rl], p, ro, k + u);
+    }
+  }
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ULL;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
@@ -125,6 +222,24 @@ cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, in
     else split_direct_kernel<<<grid, block, 0, stream>>>(s16, lds, rows, kcols, p);
   } else {
     const float* s32 = static_cast<const float*>(src);
+    auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    auto a8 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; };
+    // vector path: 16-B aligned source rows and destination rows
+    const bool vec = a16(s32) && (lds & 3) == 0 && a16(hi) && (ldo & 3) == 0 &&
+                     (lo == nullptr || a16(lo)) &&
+                     (hi16 == nullptr || (a8(hi16) && a8(lo16) && (ldo16 & 3) == 0));
+    if (vec) {
+      if (trans) {
+        dim3 g(static_cast<unsigned>((kcols + 31) / 32), static_cast<unsigned>((rows + 127) / 128));
+        if (g.y > 65535u) return cudaErrorInvalidConfiguration;
+        split_trans_vec4_kernel<<<g, block, 0, stream>>>(s32, lds, rows, kcols, p);
+      } else {
+        dim3 g(static_cast<unsigned>((kcols + 127) / 128), static_cast<unsigned>((rows + 31) / 32));
+        if (g.y > 65535u) return cudaErrorInvalidConfiguration;
+        split_direct_vec4_kernel<<<g, block, 0, stream>>>(s32, lds, rows, kcols, p);
+      }
+      return cudaGetLastError();
+    }
     if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(s32, lds, rows, kcols, p);
     else split_direct_kernel<<<grid, block, 0, stream>>>(s32, lds, rows, kcols, p);
   }

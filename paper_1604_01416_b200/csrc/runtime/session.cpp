@@ -65,6 +65,7 @@ Session::Session(const dm_session_config& cfg) {
     cuda_check(cudaStreamCreateWithFlags(&wk->side, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&wk->h2d, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&wk->d2h, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&wk->pull, cudaStreamNonBlocking), "cudaStreamCreate");
     wk->pool = std::make_unique<DevicePool>(dev);
     wk->seed = mix64(root_seed_, static_cast<std::uint64_t>(w));  // exec_seed, ops.hpp:1140
     workers_[w] = std::move(wk);
@@ -127,6 +128,7 @@ Session::~Session() {
     cudaStreamDestroy(w->side);
     cudaStreamDestroy(w->h2d);
     cudaStreamDestroy(w->d2h);
+    cudaStreamDestroy(w->pull);
   }
 }
 
@@ -197,7 +199,7 @@ void Session::sync_local() {
   for (auto& w : workers_) {
     if (!w) continue;
     DeviceGuard g(w->device);
-    for (cudaStream_t st : {w->h2d, w->side, w->stream, w->d2h})
+    for (cudaStream_t st : {w->h2d, w->pull, w->side, w->stream, w->d2h})
       cuda_check(cudaStreamSynchronize(st), "stream sync");
   }
 }
@@ -926,19 +928,111 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
                        [&](int x, int y) { return remote_bytes[x] < remote_bytes[y]; });
     }
 
+    // Pieces that live on another GPU cross NVLink on a copy engine into a
+    // local landing buffer (no SMs taken from the concurrently running GEMM);
+    // the split then reads local HBM.  Landing buffers are double-buffered so
+    // the copy of panel s+1 overlaps the split and GEMM of panel s.
+    const bool use_ce = env_int("DM_PULL_CE", 1) != 0;
+    auto resolve = [&](const Piece& pc, bool* remote, bool* cross) {
+      const void* src = static_cast<const char*>(source_ptr(w, pc.matrix, pc.coord, pol, remote)) +
+                        pc.src_off * static_cast<std::int64_t>(esz);
+      *cross = false;
+      if (*remote && use_ce) {
+        const Worker* ow = local(table_.at(pc.matrix).layout.owner(pc.coord));
+        *cross = ow == nullptr || ow->device != w.device;
+      }
+      return src;
+    };
+    // landing rectangle of a piece: source rows (op-k rows when transposed)
+    auto land_width = [](const Piece& pc) { return pc.trans ? pc.rows : pc.kcols; };
+    auto land_height = [](const Piece& pc) { return pc.trans ? pc.kcols : pc.rows; };
+    auto land_pitch = [&](const Piece& pc) { return (land_width(pc) + 7) / 8 * 8; };
+    auto land_bytes = [&](const Piece& pc) {
+      return static_cast<std::size_t>((land_pitch(pc) * land_height(pc) * static_cast<std::int64_t>(esz) + 255) /
+                                      256 * 256);
+    };
+    std::size_t land_max = 0;
+    for (int p = 0; p < np; ++p) {
+      std::size_t tot = 0;
+      for (const auto* ranges : {&plan.ar, &plan.br})
+        for (const Range& r : *ranges)
+          for (const Piece& pc : r.panels[p]) {
+            bool remote, cross;
+            resolve(pc, &remote, &cross);
+            if (cross) tot += land_bytes(pc);
+          }
+      land_max = std::max(land_max, tot);
+    }
+    char* landing[2] = {nullptr, nullptr};
+    cudaEvent_t landed[2] = {nullptr, nullptr};
+    if (land_max > 0) {
+      for (int b = 0; b < nbuf; ++b) {
+        lv.bufs.push_back(w.pool->acquire(land_max));
+        landing[b] = static_cast<char*>(lv.bufs.back().data());
+        cuda_check(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming), "event");
+        lv.events.push_back(landed[b]);
+      }
+      // the copy stream starts where the split stream is (after the operand
+      // waits / device barrier above)
+      cuda_check(cudaEventRecord(landed[0], w.side), "event");
+      cuda_check(cudaStreamWaitEvent(w.pull, landed[0], 0), "wait");
+    }
+
     for (int step = 0; step < np; ++step) {
       const int p = order[step];
       const int buf = step % nbuf;
-      if (step >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_done[buf], 0), "wait");
+      // effective source of every piece of this panel, in issue order
+      std::vector<std::pair<const void*, std::int64_t>> eff;
+      std::vector<char> eff_remote;
+      {
+        std::size_t loff = 0;
+        const std::uint64_t landed0 = w.stats.peer_bytes_read;
+        cudaEvent_t tp = nullptr;
+        bool any = false;
+        for (const auto* ranges : {&plan.ar, &plan.br})
+          for (const Range& r : *ranges)
+            for (const Piece& pc : r.panels[p]) {
+              bool remote, cross;
+              const void* src = resolve(pc, &remote, &cross);
+              eff_remote.push_back(remote ? 1 : 0);
+              if (!cross) {
+                eff.push_back({src, pc.lds});
+                continue;
+              }
+              if (!any) {
+                any = true;
+                // landing[buf] is free once the split of panel step-nbuf ran
+                if (step >= nbuf) cuda_check(cudaStreamWaitEvent(w.pull, split_done[buf], 0), "wait");
+                if (trace) tp = trace_event(w.pull);
+              }
+              char* dst = landing[buf] + loff;
+              cuda_check(cudaMemcpy2DAsync(dst, land_pitch(pc) * esz, src, pc.lds * esz, land_width(pc) * esz,
+                                           land_height(pc), cudaMemcpyDefault, w.pull),
+                         "cudaMemcpy2DAsync(peer)");
+              eff.push_back({dst, land_pitch(pc)});
+              loff += land_bytes(pc);
+              w.stats.peer_bytes_read += pc.bytes() / 4 * esz;
+            }
+        if (any) {
+          cuda_check(cudaEventRecord(landed[buf], w.pull), "event");
+          if (trace)
+            w.trace.push_back({"pull", p, w.stats.peer_bytes_read - landed0, 0.0, tp, trace_event(w.pull)});
+        }
+        w.stats.peer_bytes_read = landed0;  // counted once below, with the split
+        if (step >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_done[buf], 0), "wait");
+        if (any) cuda_check(cudaStreamWaitEvent(w.side, landed[buf], 0), "wait");
+      }
+      std::size_t next = 0;
       auto issue = [&](const std::vector<Range>& rs, const std::vector<std::array<Planes, 2>>& planes) {
         for (std::size_t i = 0; i < rs.size(); ++i)
           for (const Piece& pc : rs[i].panels[p]) {
-            bool remote = false;
-            const void* src = static_cast<const char*>(source_ptr(w, pc.matrix, pc.coord, pol, &remote)) +
-                              pc.src_off * static_cast<std::int64_t>(esz);
+            const bool remote = eff_remote[next] != 0;
+            const void* src = eff[next].first;
+            const std::int64_t lds = eff[next].second;
+            ++next;
             const Planes& pl = planes[i][buf];
             const std::int64_t off = pc.dst_row * kpitch + pc.dst_k;
-            cuda_check(split_tf32(src, half_in ? 1 : 0, pc.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
+            cuda_check(split_tf32(src, half_in ? 1 : 0, lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
                                   pl.lo ? pl.lo + off : nullptr, kpitch,
                                   pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
                                   pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch,

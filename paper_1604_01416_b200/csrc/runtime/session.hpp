@@ -69,7 +69,8 @@ struct Worker {
   int id = 0;
   int device = 0;
   cudaStream_t stream = nullptr;  // GEMM stream
-  cudaStream_t side = nullptr;    // pull/split stream
+  cudaStream_t side = nullptr;    // split stream
+  cudaStream_t pull = nullptr;    // copy engine, peer -> local landing buffers
   cudaStream_t h2d = nullptr;     // copy engine, host -> device (async scatter)
   cudaStream_t d2h = nullptr;     // copy engine, device -> host (async gather)
   std::map<MatrixId, Track> tracks;
