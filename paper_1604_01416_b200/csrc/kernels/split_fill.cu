@@ -13,37 +13,18 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
+#include "split_common.cuh"
 #include "tf32x3_gemm.h"
 
 namespace dm {
 
 namespace {
 
-__device__ __forceinline__ float tf32_rne(float x) {
-  uint32_t u = __float_as_uint(x);
-  if ((u & 0x7f800000u) != 0x7f800000u) u += 0xFFFu + ((u >> 13) & 1u);
-  return __uint_as_float(u & 0xFFFFE000u);
-}
-
-struct Planes {
-  float* hi;
-  float* lo;            // tf32 lo (kModeTf32x3) or null
-  __nv_bfloat16* hi16;  // bf16(hi) (kModeMixed) or null
-  __nv_bfloat16* lo16;
-  int64_t ldo, ldo16;
-};
-
-__device__ __forceinline__ void split_store(float x, const Planes& p, int64_t r, int64_t k) {
-  const float h = tf32_rne(x);
-  const float l = x - h;  // exact
-  p.hi[r * p.ldo + k] = h;
-  if (p.lo) p.lo[r * p.ldo + k] = tf32_rne(l);
-  if (p.hi16) {
-    p.hi16[r * p.ldo16 + k] = __float2bfloat16_rn(h);
-    p.lo16[r * p.ldo16 + k] = __float2bfloat16_rn(l);
-  }
-}
+using splitdev::Planes;
+using splitdev::split_store;
+using splitdev::split_store4;
 
 constexpr int kT = 32;  // tile edge
 constexpr int kRowsPerPass = 8;
@@ -90,50 +71,27 @@ __global__ void split_trans_kernel(const T* __restrict__ src, int64_t lds, int64
 }
 
 // ---- vectorised fp32 variants: 4 consecutive elements per access, 4 accesses
-// in flight per thread.  They run concurrently with the persistent GEMM (one
-// resident block per SM at most), so bytes in flight per thread, not thread
-// count, sets their bandwidth.
-__device__ __forceinline__ void split_store4(float4 x, const Planes& p, int64_t r, int64_t k) {
-  const float v[4] = {x.x, x.y, x.z, x.w};
-  float h[4], l[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    h[u] = tf32_rne(v[u]);
-    l[u] = v[u] - h[u];
-  }
-  *reinterpret_cast<float4*>(p.hi + r * p.ldo + k) = make_float4(h[0], h[1], h[2], h[3]);
-  if (p.lo)
-    *reinterpret_cast<float4*>(p.lo + r * p.ldo + k) =
-        make_float4(tf32_rne(l[0]), tf32_rne(l[1]), tf32_rne(l[2]), tf32_rne(l[3]));
-  if (p.hi16) {
-    __nv_bfloat162 a0 = __floats2bfloat162_rn(h[0], h[1]), a1 = __floats2bfloat162_rn(h[2], h[3]);
-    __nv_bfloat162 b0 = __floats2bfloat162_rn(l[0], l[1]), b1 = __floats2bfloat162_rn(l[2], l[3]);
-    uint2 hv, lv;
-    hv.x = *reinterpret_cast<uint32_t*>(&a0);
-    hv.y = *reinterpret_cast<uint32_t*>(&a1);
-    lv.x = *reinterpret_cast<uint32_t*>(&b0);
-    lv.y = *reinterpret_cast<uint32_t*>(&b1);
-    *reinterpret_cast<uint2*>(p.hi16 + r * p.ldo16 + k) = hv;
-    *reinterpret_cast<uint2*>(p.lo16 + r * p.ldo16 + k) = lv;
-  }
-}
-
-// 32 rows x 128 k per block (32 x 8 threads); requires 16-B aligned rows.
-__global__ void split_direct_vec4_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
-                                         int64_t kcols, Planes p) {
+// in flight per thread.
+// (4*WY) rows x 128 k per block (32 x WY threads); requires 16-B aligned rows.
+// <= 40 registers so blocks fit beside a resident GEMM CTA (320 threads x
+// 168 registers leave 11.7 K of the SM's 64 K).
+template <int WY>
+__global__ void __launch_bounds__(32 * WY, 48 / WY) split_direct_vec4_kernel(const float* __restrict__ src,
+                                                                            int64_t lds, int64_t rows,
+                                                                            int64_t kcols, Planes p) {
   const int64_t k = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x * 4;
-  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * (4 * WY);
   if (k >= kcols) return;
   float4 v[4];
   const bool full = k + 4 <= kcols;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + threadIdx.y + 8 * i;
+    const int64_t r = r0 + threadIdx.y + WY * i;
     if (r < rows && full) v[i] = __ldg(reinterpret_cast<const float4*>(src + r * lds + k));
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int64_t r = r0 + threadIdx.y + 8 * i;
+    const int64_t r = r0 + threadIdx.y + WY * i;
     if (r >= rows) continue;
     if (full) {
       split_store4(v[i], p, r, k);
@@ -144,16 +102,18 @@ __global__ void split_direct_vec4_kernel(const float* __restrict__ src, int64_t 
 }
 
 // out[r][k] = src[k][r]: 32 k x 128 r per block through shared memory.
-__global__ void split_trans_vec4_kernel(const float* __restrict__ src, int64_t lds, int64_t rows,
-                                        int64_t kcols, Planes p) {
+template <int WY>
+__global__ void __launch_bounds__(32 * WY, 48 / WY) split_trans_vec4_kernel(const float* __restrict__ src,
+                                                                           int64_t lds, int64_t rows,
+                                                                           int64_t kcols, Planes p) {
   __shared__ float tile[32][128 + 4];
   const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 128;
   const int t = threadIdx.y * 32 + threadIdx.x;
   const int64_t r = r0 + threadIdx.x * 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int kl = threadIdx.y + 8 * i;
+#pragma unroll 4
+  for (int i = 0; i < 32 / WY; ++i) {
+    const int kl = threadIdx.y + WY * i;
     const int64_t k = k0 + kl;
     if (k >= kcols) continue;
     if (r + 4 <= rows) {
@@ -168,22 +128,45 @@ __global__ void split_trans_vec4_kernel(const float* __restrict__ src, int64_t l
     }
   }
   __syncthreads();
-  // 128 r x 32 k out: thread -> one row, 16 consecutive k (4 x float4)
-  const int rl = t >> 1;
-  const int64_t ro = r0 + rl;
-  if (ro >= rows) return;
+  // 128 r x 32 k out: a thread pair per row, 16 consecutive k each (4 x float4)
+  for (int rl = t >> 1; rl < 128; rl += 16 * WY) {
+    const int64_t ro = r0 + rl;
+    if (ro >= rows) break;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int kl = (t & 1) * 16 + 4 * j;
-    const int64_t k = k0 + kl;
-    if (k >= kcols) continue;
-    if (k + 4 <= kcols) {
-      split_store4(make_float4(tile[kl][rl], tile[kl + 1][rl], tile[kl + 2][rl], tile[kl + 3][rl]), p,
-                   ro, k);
-    } else {
-      for (int u = 0; k + u < kcols; ++u) split_store(tile[kl + u][rl], p, ro, k + u);
+    for (int j = 0; j < 4; ++j) {
+      const int kl = (t & 1) * 16 + 4 * j;
+      const int64_t k = k0 + kl;
+      if (k >= kcols) continue;
+      if (k + 4 <= kcols) {
+        split_store4(make_float4(tile[kl][rl], tile[kl + 1][rl], tile[kl + 2][rl], tile[kl + 3][rl]), p,
+                     ro, k);
+      } else {
+        for (int u = 0; k + u < kcols; ++u) split_store(tile[kl + u][rl], p, ro, k + u);
+      }
     }
   }
+}
+
+template <int WY>
+void launch_split_vec4(const float* s32, int64_t lds, int trans, int64_t rows, int64_t kcols, const Planes& p,
+                       cudaStream_t stream) {
+  const dim3 block(32, WY);
+  if (trans) {
+    const dim3 g(static_cast<unsigned>((kcols + 31) / 32), static_cast<unsigned>((rows + 127) / 128));
+    split_trans_vec4_kernel<WY><<<g, block, 0, stream>>>(s32, lds, rows, kcols, p);
+  } else {
+    const dim3 g(static_cast<unsigned>((kcols + 127) / 128), static_cast<unsigned>((rows + 4 * WY - 1) / (4 * WY)));
+    split_direct_vec4_kernel<WY><<<g, block, 0, stream>>>(s32, lds, rows, kcols, p);
+  }
+}
+
+int split_warps() {
+  static const int w = [] {
+    const char* e = std::getenv("DM_SPLIT_WARPS");
+    const int v = e ? std::atoi(e) : 8;
+    return (v == 2 || v == 4) ? v : 8;
+  }();
+  return w;
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -229,14 +212,11 @@ cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, in
                      (lo == nullptr || a16(lo)) &&
                      (hi16 == nullptr || (a8(hi16) && a8(lo16) && (ldo16 & 3) == 0));
     if (vec) {
-      if (trans) {
-        dim3 g(static_cast<unsigned>((kcols + 31) / 32), static_cast<unsigned>((rows + 127) / 128));
-        if (g.y > 65535u) return cudaErrorInvalidConfiguration;
-        split_trans_vec4_kernel<<<g, block, 0, stream>>>(s32, lds, rows, kcols, p);
-      } else {
-        dim3 g(static_cast<unsigned>((kcols + 127) / 128), static_cast<unsigned>((rows + 31) / 32));
-        if (g.y > 65535u) return cudaErrorInvalidConfiguration;
-        split_direct_vec4_kernel<<<g, block, 0, stream>>>(s32, lds, rows, kcols, p);
+      if ((rows + 7) / 8 > 65535) return cudaErrorInvalidConfiguration;
+      switch (split_warps()) {
+        case 2: launch_split_vec4<2>(s32, lds, trans, rows, kcols, p, stream); break;
+        case 4: launch_split_vec4<4>(s32, lds, trans, rows, kcols, p, stream); break;
+        default: launch_split_vec4<8>(s32, lds, trans, rows, kcols, p, stream); break;
       }
       return cudaGetLastError();
     }

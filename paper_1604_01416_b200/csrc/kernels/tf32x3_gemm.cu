@@ -30,6 +30,7 @@
 #include <cstdio>
 
 #include "ptx.cuh"
+#include "split_common.cuh"
 #include "tf32x3_gemm.h"
 
 namespace dm {
@@ -49,9 +50,12 @@ struct Cfg {
   static constexpr int kTmemCols = 2 * kAccCols;             // double-buffered chunks
   static constexpr int kEpiWarps = 8;                        // 2 per TMEM lane quadrant
   static constexpr int kColsPerThread = kAccCols / 2;        // master accumulator registers
-  static constexpr int kThreads = 64 + 32 * kEpiWarps;
+  static constexpr int kSplitWarps = 2;                      // fused split of the next panel
+  static constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kSplitWarps;
   static constexpr int kGroupM = 8;                          // rasterisation group
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSplitTileBytes = 32 * (128 + 4) * 4;  // transposed split tile
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kSplitTileBytes;
 };
 
 struct EpiParams {
@@ -78,6 +82,103 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
   nt = r / gsize;
 }
 
+// ---------------------------------------------------------------- split warps
+// The kernel's two split warps run split jobs for the next K panel (see
+// SplitJob) while the producer / MMA / epilogue warps run this panel: the
+// split then needs no SM time of its own (a separate split kernel cannot be
+// co-resident with this one -- the GEMM's warps leave too few registers in
+// every SM sub-partition), and no launch between the panels' GEMMs.
+// Tiles: direct 32 rows x 128 k (16 float4 loads in flight per thread),
+// transposed 32 k x 128 rows through a shared-memory tile.
+__device__ __forceinline__ void split_bar() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
+
+__device__ __noinline__ void run_split_jobs(const SplitJobs& sj, float (*tile)[128 + 4], int st) {
+  using splitdev::Planes;
+  const int lane = st & 31, wy = st >> 5;
+  uint32_t ready = 0;  // jobs whose landing flag was seen
+  for (int64_t t = sj.t_begin + blockIdx.x; t < sj.t_end; t += gridDim.x) {
+    int j = 0;
+    while (j + 1 < sj.n && t >= sj.job[j + 1].t0) ++j;
+    const SplitJob& jb = sj.job[j];
+    if (jb.flag != nullptr && !(ready & (1u << j))) {
+      const long long t0 = clock64();
+      while (true) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(jb.flag) : "memory");
+        if (static_cast<int>(v - jb.flag_val) >= 0) break;
+        __nanosleep(256);
+        if (clock64() - t0 > (1ll << 36)) __trap();  // landing copy never signalled
+      }
+      ready |= 1u << j;
+    }
+    const Planes p{jb.hi, jb.lo, static_cast<__nv_bfloat16*>(jb.hi16), static_cast<__nv_bfloat16*>(jb.lo16),
+                   jb.ldo, jb.ldo16};
+    const int64_t lt = t - jb.t0;
+    if (!jb.trans) {
+      const int64_t tiles_k = (jb.kcols + 127) / 128;
+      const int64_t k = (lt % tiles_k) * 128 + lane * 4;
+      const int64_t r0 = (lt / tiles_k) * 32 + wy;
+      if (k >= jb.kcols) continue;
+      const bool full = k + 4 <= jb.kcols;
+      float4 v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int64_t r = r0 + 2 * i;
+        if (r < jb.rows && full) v[i] = __ldcs(reinterpret_cast<const float4*>(jb.src + r * jb.lds + k));
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int64_t r = r0 + 2 * i;
+        if (r >= jb.rows) break;
+        if (full) {
+          splitdev::split_store4(v[i], p, r, k);
+        } else {
+          for (int64_t kk = k; kk < jb.kcols; ++kk) splitdev::split_store(__ldcs(jb.src + r * jb.lds + kk), p, r, kk);
+        }
+      }
+    } else {
+      const int64_t tiles_k = (jb.kcols + 31) / 32;
+      const int64_t k0 = (lt % tiles_k) * 32;
+      const int64_t rb = (lt / tiles_k) * 128;
+      const int64_t r = rb + lane * 4;
+      split_bar();  // previous tile fully read
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int kl = wy + 2 * i;
+        const int64_t k = k0 + kl;
+        if (k >= jb.kcols) break;
+        if (r + 4 <= jb.rows) {
+          const float4 x = __ldcs(reinterpret_cast<const float4*>(jb.src + k * jb.lds + r));
+          tile[kl][lane * 4 + 0] = x.x;
+          tile[kl][lane * 4 + 1] = x.y;
+          tile[kl][lane * 4 + 2] = x.z;
+          tile[kl][lane * 4 + 3] = x.w;
+        } else {
+          for (int u = 0; u < 4; ++u)
+            if (r + u < jb.rows) tile[kl][lane * 4 + u] = __ldcs(jb.src + k * jb.lds + r + u);
+        }
+      }
+      split_bar();
+      for (int rl = st >> 1; rl < 128; rl += 32) {
+        const int64_t ro = rb + rl;
+        if (ro >= jb.rows) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int kl = (st & 1) * 16 + 4 * q;
+          const int64_t k = k0 + kl;
+          if (k >= jb.kcols) break;
+          if (k + 4 <= jb.kcols) {
+            splitdev::split_store4(make_float4(tile[kl][rl], tile[kl + 1][rl], tile[kl + 2][rl], tile[kl + 3][rl]),
+                                   p, ro, k);
+          } else {
+            for (int u = 0; k + u < jb.kcols; ++u) splitdev::split_store(tile[kl + u][rl], p, ro, k + u);
+          }
+        }
+      }
+    }
+  }
+}
+
 // Numerics note.  The tensor core adds each MMA's products into the fp32
 // accumulator with truncation (round toward zero), so the relative error of
 // one TMEM accumulator grows linearly with the number of MMAs issued into it
@@ -96,7 +197,8 @@ struct Maps {
 
 template <int CG, int MODE>
 __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
-    tf32x3_gemm_kernel(const __grid_constant__ Maps maps, int K, int kc_blocks, EpiParams ep) {
+    tf32x3_gemm_kernel(const __grid_constant__ Maps maps, int K, int kc_blocks, EpiParams ep,
+                       const __grid_constant__ SplitJobs sj) {
   using C = Cfg<CG>;
   using namespace ptx;
 
@@ -272,6 +374,11 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
         }
       }
     }
+  } else if (warp >= 2 + C::kEpiWarps) {
+    // ------------------------------------------------------------ split warps
+    if (sj.n > 0)
+      run_split_jobs(sj, reinterpret_cast<float(*)[128 + 4]>(smem + C::kStages * C::kStageBytes + 256),
+                     threadIdx.x - 32 * (2 + C::kEpiWarps));
   } else {
     // ------------------------------------------------------------ epilogue
     const int e = warp - 2;
@@ -326,30 +433,42 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       }
       float* crow = ep.c + static_cast<int64_t>(row) * ep.ldc + c0;
       const bool vec_ok = ((ep.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(ep.c) & 15) == 0);
+      // C is read in groups of kEpiGroup float4 issued back to back (one
+      // round trip per group, not per float4): with beta != 0 the epilogue
+      // must not hold the chunk buffers longer than the MMA's two-chunk slack.
+      constexpr int kEpiGroup = 4;
 #pragma unroll
-      for (int j = 0; j < C::kColsPerThread / 4; ++j) {
-        const int cc = c0 + 4 * j;
-        if (cc >= ep.n) break;
-        float o[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) o[u] = __fmul_rn(ep.alpha, master[4 * j + u]);
-        if (vec_ok && cc + 4 <= ep.n) {
-          float4* dst = reinterpret_cast<float4*>(crow + 4 * j);
+      for (int j0 = 0; j0 < C::kColsPerThread / 4; j0 += kEpiGroup) {
+        const int cc0 = c0 + 4 * j0;
+        if (cc0 >= ep.n) break;
+        if (vec_ok && cc0 + 4 * kEpiGroup <= ep.n) {
+          float4 cv[kEpiGroup];
           if (ep.read_c) {
-            const float4 cv = *dst;
-            o[0] = __fadd_rn(o[0], __fmul_rn(ep.beta, cv.x));
-            o[1] = __fadd_rn(o[1], __fmul_rn(ep.beta, cv.y));
-            o[2] = __fadd_rn(o[2], __fmul_rn(ep.beta, cv.z));
-            o[3] = __fadd_rn(o[3], __fmul_rn(ep.beta, cv.w));
+#pragma unroll
+            for (int u = 0; u < kEpiGroup; ++u) cv[u] = __ldcs(reinterpret_cast<const float4*>(crow + 4 * (j0 + u)));
           }
-          *dst = make_float4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+          for (int u = 0; u < kEpiGroup; ++u) {
+            const int j = j0 + u;
+            float o[4];
+#pragma unroll
+            for (int q2 = 0; q2 < 4; ++q2) o[q2] = __fmul_rn(ep.alpha, master[4 * j + q2]);
+            if (ep.read_c) {
+              o[0] = __fadd_rn(o[0], __fmul_rn(ep.beta, cv[u].x));
+              o[1] = __fadd_rn(o[1], __fmul_rn(ep.beta, cv[u].y));
+              o[2] = __fadd_rn(o[2], __fmul_rn(ep.beta, cv[u].z));
+              o[3] = __fadd_rn(o[3], __fmul_rn(ep.beta, cv[u].w));
+            }
+            __stcs(reinterpret_cast<float4*>(crow + 4 * j), make_float4(o[0], o[1], o[2], o[3]));
+          }
         } else {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            if (cc + u < ep.n) {
-              float v = o[u];
-              if (ep.read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, crow[4 * j + u]));
-              crow[4 * j + u] = v;
+          for (int jj = 0; jj < 4 * kEpiGroup; ++jj) {
+            const int cc = cc0 + jj;
+            if (cc < ep.n) {
+              float v = __fmul_rn(ep.alpha, master[4 * j0 + jj]);
+              if (ep.read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, crow[4 * j0 + jj]));
+              crow[4 * j0 + jj] = v;
             }
           }
         }
@@ -483,11 +602,40 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int kc_blocks = a.flush_k > 0 ? static_cast<int>((a.flush_k + C::kBK - 1) / C::kBK) : 8;
+  SplitJobs sj;
+  if (a.split != nullptr) sj = *a.split;
   return cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG, MODE>, maps, static_cast<int>(a.k),
-                            kc_blocks, ep);
+                            kc_blocks, ep, sj);
 }
 
 }  // namespace
+
+cudaError_t stream_write_flag(cudaStream_t stream, unsigned* addr, unsigned value) {
+  using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WriteValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<WriteValueFn>(nullptr);
+    return reinterpret_cast<WriteValueFn>(p);
+  }();
+  if (fn == nullptr) return cudaErrorNotSupported;
+  return fn(stream, reinterpret_cast<CUdeviceptr>(addr), value, 0) == CUDA_SUCCESS ? cudaSuccess
+                                                                                    : cudaErrorUnknown;
+}
+
+int64_t split_job_tiles(const SplitJob& j) {
+  if (j.rows <= 0 || j.kcols <= 0) return 0;
+  return j.trans ? ((j.kcols + 31) / 32) * ((j.rows + 127) / 128) : ((j.rows + 31) / 32) * ((j.kcols + 127) / 128);
+}
+
+bool split_job_fusable(const SplitJob& j) {
+  auto al = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
+  return j.src != nullptr && al(j.src, 16) && (j.lds & 3) == 0 && j.hi != nullptr && al(j.hi, 16) &&
+         (j.ldo & 3) == 0 && (j.lo == nullptr || al(j.lo, 16)) &&
+         (j.hi16 == nullptr || (al(j.hi16, 8) && al(j.lo16, 8) && (j.ldo16 & 3) == 0));
+}
 
 size_t tf32x3_sync_bytes(const Tf32x3Args& a) {
   if (a.lockstep <= 0 || a.m <= 0 || a.n <= 0 || a.k <= 0) return 0;
@@ -498,6 +646,8 @@ size_t tf32x3_sync_bytes(const Tf32x3Args& a) {
 }
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
+  if (a.split != nullptr && a.split->n > 0 && (a.m <= 0 || a.n <= 0 || a.k <= 0))
+    return cudaErrorInvalidValue;  // fused split work needs a real GEMM launch to ride on
   if (a.m <= 0 || a.n <= 0) return cudaSuccess;
   if (a.k <= 0) {
     const int64_t total = a.m * a.n;

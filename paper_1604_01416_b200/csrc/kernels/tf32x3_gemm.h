@@ -16,6 +16,36 @@ namespace dm {
 constexpr int kModeTf32x3 = 0;
 constexpr int kModeMixed = 1;
 
+// One split job fused into a GEMM launch: the split_tf32 of an fp32 piece
+// (16-B aligned rows and planes) for the NEXT K panel, executed by the
+// kernel's two split warps while its tensor-core pipeline runs.  With `flag`
+// set, the job's source is a landing buffer filled by copy-engine transfers:
+// the warps wait until (int)(*flag - flag_val) >= 0 before reading it.
+struct SplitJob {
+  const float* src = nullptr;
+  int64_t lds = 0;
+  int trans = 0;
+  int64_t rows = 0, kcols = 0;
+  float* hi = nullptr;
+  float* lo = nullptr;
+  void* hi16 = nullptr;
+  void* lo16 = nullptr;
+  int64_t ldo = 0, ldo16 = 0;
+  const unsigned* flag = nullptr;
+  unsigned flag_val = 0;
+  int64_t t0 = 0;  // first tile of this job in the launch's concatenated tile space
+};
+constexpr int kMaxSplitJobs = 16;
+struct SplitJobs {
+  SplitJob job[kMaxSplitJobs];
+  int n = 0;
+  int64_t t_begin = 0, t_end = 0;  // tile range this launch processes
+};
+// tiles of one job (direct: 32 rows x 128 k; transposed: 32 k x 128 rows)
+int64_t split_job_tiles(const SplitJob& j);
+// can the GEMM's split warps run this job (fp32, aligned)?
+bool split_job_fusable(const SplitJob& j);
+
 // C[m x n] (row pitch ldc) <- alpha * A B^T + beta * C, where A and B are
 // given as K-major splits: A planes [m x k] (fp32 containers pitch lda, bf16
 // planes pitch lda16), B planes [n x k] (i.e. op(B) transposed).
@@ -46,6 +76,7 @@ struct Tf32x3Args {
   int lockstep = 0;     // >0: producers stay within this many k-blocks of each other
   unsigned* sync = nullptr;  // lockstep counters (>= tf32x3_sync_bytes), private to this launch
   size_t sync_bytes = 0;
+  const SplitJobs* split = nullptr;  // fused split work for this launch (may be null)
 };
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);
@@ -66,6 +97,11 @@ size_t tf32x3_sync_bytes(const Tf32x3Args& args);
 cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, int64_t rows,
                        int64_t kcols, float* hi, float* lo, int64_t ldo, void* hi16, void* lo16,
                        int64_t ldo16, cudaStream_t stream);
+
+// Stream-ordered 32-bit store without an SM (a stream memory operation):
+// *addr = value once the stream's earlier work (e.g. copy-engine transfers)
+// completed; pairs with SplitJob::flag.
+cudaError_t stream_write_flag(cudaStream_t stream, unsigned* addr, unsigned value);
 
 // Seeded synthetic fill, bit-exact with the reference's WorkerContext::fill_seeded
 // (runtime_types.hpp:208-218): v[e] = T(2*u53(mix64(key, e)) - 1), the double

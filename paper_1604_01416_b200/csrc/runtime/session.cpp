@@ -120,6 +120,7 @@ Session::~Session() {
     w->cache.clear();
     w->replicas.clear();
     w->arena = DeviceBuffer();
+    w->pull_flag = DeviceBuffer();
     w->inflight.clear();
     for (auto* v : {&w->event_pool, &w->events_used})
       for (cudaEvent_t e : *v) cudaEventDestroy(e);
@@ -150,6 +151,7 @@ void Session::shutdown() {
     w->cache.clear();
     w->replicas.clear();
     w->arena = DeviceBuffer();
+    w->pull_flag = DeviceBuffer();
     w->descriptors.clear();
     w->pool->trim();
   }
@@ -722,7 +724,7 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
           }
   }
   const std::int64_t target = env_int("DM_PANEL_K", 8192);
-  if (plan.has_remote && K > 2 * 256 && target > 0) {
+  if ((plan.has_remote || env_int("DM_PANEL_LOCAL", 0) != 0) && K > 2 * 256 && target > 0) {
     std::int64_t np = std::max<std::int64_t>(2, (K + target - 1) / target);
     np = std::min<std::int64_t>(np, K / 256);
     std::int64_t width = (K + np - 1) / np;
@@ -897,17 +899,15 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     std::vector<std::array<Planes, 2>> pa, pb;
     alloc_planes(plan.ar, pa);
     alloc_planes(plan.br, pb);
-    cudaEvent_t split_done[2], gemm_done[2];
-    for (int b = 0; b < 2; ++b) {
-      cuda_check(cudaEventCreateWithFlags(&split_done[b], cudaEventDisableTiming), "event");
-      cuda_check(cudaEventCreateWithFlags(&gemm_done[b], cudaEventDisableTiming), "event");
-      lv.events.push_back(split_done[b]);
-      lv.events.push_back(gemm_done[b]);
-    }
     // operands of this worker's GEMMs were written by earlier commands on
-    // its own streams; order the side stream after the compute stream.
-    cuda_check(cudaEventRecord(gemm_done[1], w.stream), "event");
-    cuda_check(cudaStreamWaitEvent(w.side, gemm_done[1], 0), "wait");
+    // its own streams; order the split stream after the compute stream.
+    {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      lv.events.push_back(e);
+      cuda_check(cudaEventRecord(e, w.stream), "event");
+      cuda_check(cudaStreamWaitEvent(w.side, e, 0), "wait");
+    }
 
     // Panels with the fewest peer bytes first: the GEMM starts on local data
     // while the first remote pulls are still in flight (K order does not
@@ -964,97 +964,178 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
       land_max = std::max(land_max, tot);
     }
     char* landing[2] = {nullptr, nullptr};
-    cudaEvent_t landed[2] = {nullptr, nullptr};
     if (land_max > 0) {
       for (int b = 0; b < nbuf; ++b) {
         lv.bufs.push_back(w.pool->acquire(land_max));
         landing[b] = static_cast<char*>(lv.bufs.back().data());
-        cuda_check(cudaEventCreateWithFlags(&landed[b], cudaEventDisableTiming), "event");
-        lv.events.push_back(landed[b]);
       }
-      // the copy stream starts where the split stream is (after the operand
-      // waits / device barrier above)
-      cuda_check(cudaEventRecord(landed[0], w.side), "event");
-      cuda_check(cudaStreamWaitEvent(w.pull, landed[0], 0), "wait");
+      if (!w.pull_flag.data()) {
+        w.pull_flag = w.pool->acquire(256);
+        cuda_check(cudaMemset(w.pull_flag.data(), 0, 256), "cudaMemset(flag)");
+        w.pull_seq = 0;
+      }
     }
+    unsigned* flag = static_cast<unsigned*>(w.pull_flag.data());
+    auto new_event = [&]() {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+      lv.events.push_back(e);
+      return e;
+    };
+    // Per panel step: landed (copies done), consumed (landing buffer read by
+    // the split), split (planes written), gemm (planes read).
+    std::vector<cudaEvent_t> landed_ev(np, nullptr), consumed_ev(np, nullptr), split_ev(np, nullptr),
+        gemm_ev(np, nullptr);
+    // The copy stream starts where the split stream is (after the operand
+    // waits / device barrier above).
+    if (land_max > 0) {
+      cudaEvent_t e = new_event();
+      cuda_check(cudaEventRecord(e, w.side), "event");
+      cuda_check(cudaStreamWaitEvent(w.pull, e, 0), "wait");
+    }
+    const bool fuse = env_int("DM_FUSE_SPLIT", 1) != 0 && !half_in;
 
+    // One split item per piece: effective source (landing buffer for pieces
+    // that crossed a link), target planes, and whether it waits on the flag.
+    struct Item {
+      const void* src;
+      std::int64_t lds;
+      const Piece* pc;
+      const Planes* pl;
+      bool landed;
+    };
+    std::vector<std::vector<Item>> items(np);
+    std::vector<unsigned> seq(np, 0);
+    // Issue the copy-engine pulls of step s and build its split items.
+    auto prepare = [&](int s) {
+      const int p = order[s];
+      const int buf = s % nbuf;
+      std::size_t loff = 0;
+      std::uint64_t pulled = 0;
+      cudaEvent_t tp = nullptr;
+      bool any = false;
+      for (int side_ab = 0; side_ab < 2; ++side_ab) {
+        const std::vector<Range>& rs = side_ab == 0 ? plan.ar : plan.br;
+        const std::vector<std::array<Planes, 2>>& planes = side_ab == 0 ? pa : pb;
+        for (std::size_t i = 0; i < rs.size(); ++i)
+          for (const Piece& pc : rs[i].panels[p]) {
+            bool remote, cross;
+            const void* src = resolve(pc, &remote, &cross);
+            (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
+            if (!cross) {
+              items[s].push_back({src, pc.lds, &pc, &planes[i][buf], false});
+              continue;
+            }
+            if (!any) {
+              any = true;
+              // landing[buf] was last read by the split of step s - nbuf
+              if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.pull, consumed_ev[s - nbuf], 0), "wait");
+              if (trace) tp = trace_event(w.pull);
+            }
+            char* dst = landing[buf] + loff;
+            cuda_check(cudaMemcpy2DAsync(dst, land_pitch(pc) * esz, src, pc.lds * esz, land_width(pc) * esz,
+                                         land_height(pc), cudaMemcpyDefault, w.pull),
+                       "cudaMemcpy2DAsync(peer)");
+            items[s].push_back({dst, land_pitch(pc), &pc, &planes[i][buf], true});
+            loff += land_bytes(pc);
+            pulled += pc.bytes() / 4 * esz;
+          }
+      }
+      if (any) {
+        landed_ev[s] = new_event();
+        seq[s] = ++w.pull_seq;
+        cuda_check(stream_write_flag(w.pull, flag, seq[s]), "cuStreamWriteValue32");
+        cuda_check(cudaEventRecord(landed_ev[s], w.pull), "event");
+        if (trace) w.trace.push_back({"pull", p, pulled, 0.0, tp, trace_event(w.pull)});
+      }
+    };
+    auto plane_off = [&](const Item& it) { return it.pc->dst_row * kpitch + it.pc->dst_k; };
+    // Split step s with its own kernels on the split stream.
+    auto split_separate = [&](int s) {
+      const int p = order[s];
+      if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_ev[s - nbuf], 0), "wait");  // planes free
+      if (landed_ev[s]) cuda_check(cudaStreamWaitEvent(w.side, landed_ev[s], 0), "wait");
+      cudaEvent_t ta = trace ? trace_event(w.side) : nullptr;
+      std::uint64_t bytes = 0;
+      for (const Item& it : items[s]) {
+        const Piece& pc = *it.pc;
+        const Planes& pl = *it.pl;
+        const std::int64_t off = plane_off(it);
+        cuda_check(split_tf32(it.src, half_in ? 1 : 0, it.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
+                              pl.lo ? pl.lo + off : nullptr, kpitch,
+                              pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
+                              pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch, w.side),
+                   "split_tf32");
+        w.stats.split_launches += 1;
+        bytes += pc.bytes() / 4 * esz;
+      }
+      if (trace) w.trace.push_back({"split", p, bytes, 0.0, ta, trace_event(w.side)});
+      split_ev[s] = new_event();
+      cuda_check(cudaEventRecord(split_ev[s], w.side), "event");
+      consumed_ev[s] = split_ev[s];
+    };
+    // Split jobs of step s for the split warps of step s-1's GEMM launches.
+    // Fused only when the carrying GEMM is long enough to hide the split: two
+    // warps per SM split ~150 GB/s of input beside a ~300 TFLOP/s GEMM (a
+    // narrow lead panel cannot hide a full panel's split -- that one runs as
+    // its own full-machine kernels instead).
+    auto fused_jobs = [&](int s, SplitJobs* out) {
+      if (!fuse || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs)) return false;
+      double bytes_in = 0, flops = 0;
+      for (const Item& it : items[s]) bytes_in += static_cast<double>(it.pc->bytes());
+      for (const Task& t : plan.tasks) {
+        auto [mb, nb] = block_extent(table_.at(g.c).layout.grid, t.c);
+        flops += 2.0 * mb * nb * static_cast<double>(plan.k0[order[s - 1] + 1] - plan.k0[order[s - 1]]);
+      }
+      if (bytes_in / 150e9 > flops / 300e12) return false;
+      out->n = 0;
+      std::int64_t t = 0;
+      for (const Item& it : items[s]) {
+        const Piece& pc = *it.pc;
+        const Planes& pl = *it.pl;
+        const std::int64_t off = plane_off(it);
+        SplitJob& j = out->job[out->n++];
+        j = SplitJob{};
+        j.src = static_cast<const float*>(it.src);
+        j.lds = it.lds;
+        j.trans = pc.trans;
+        j.rows = pc.rows;
+        j.kcols = pc.kcols;
+        j.hi = pl.hi + off;
+        j.lo = pl.lo ? pl.lo + off : nullptr;
+        j.hi16 = pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr;
+        j.lo16 = pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr;
+        j.ldo = j.ldo16 = kpitch;
+        j.flag = it.landed ? flag : nullptr;
+        j.flag_val = it.landed ? seq[s] : 0;
+        j.t0 = t;
+        if (!split_job_fusable(j)) return false;
+        t += split_job_tiles(j);
+      }
+      out->t_begin = 0;
+      out->t_end = t;
+      return true;
+    };
+
+    prepare(0);
+    split_separate(0);
     for (int step = 0; step < np; ++step) {
       const int p = order[step];
       const int buf = step % nbuf;
-      // effective source of every piece of this panel, in issue order
-      std::vector<std::pair<const void*, std::int64_t>> eff;
-      std::vector<char> eff_remote;
-      {
-        std::size_t loff = 0;
-        const std::uint64_t landed0 = w.stats.peer_bytes_read;
-        cudaEvent_t tp = nullptr;
-        bool any = false;
-        for (const auto* ranges : {&plan.ar, &plan.br})
-          for (const Range& r : *ranges)
-            for (const Piece& pc : r.panels[p]) {
-              bool remote, cross;
-              const void* src = resolve(pc, &remote, &cross);
-              eff_remote.push_back(remote ? 1 : 0);
-              if (!cross) {
-                eff.push_back({src, pc.lds});
-                continue;
-              }
-              if (!any) {
-                any = true;
-                // landing[buf] is free once the split of panel step-nbuf ran
-                if (step >= nbuf) cuda_check(cudaStreamWaitEvent(w.pull, split_done[buf], 0), "wait");
-                if (trace) tp = trace_event(w.pull);
-              }
-              char* dst = landing[buf] + loff;
-              cuda_check(cudaMemcpy2DAsync(dst, land_pitch(pc) * esz, src, pc.lds * esz, land_width(pc) * esz,
-                                           land_height(pc), cudaMemcpyDefault, w.pull),
-                         "cudaMemcpy2DAsync(peer)");
-              eff.push_back({dst, land_pitch(pc)});
-              loff += land_bytes(pc);
-              w.stats.peer_bytes_read += pc.bytes() / 4 * esz;
-            }
-        if (any) {
-          cuda_check(cudaEventRecord(landed[buf], w.pull), "event");
-          if (trace)
-            w.trace.push_back({"pull", p, w.stats.peer_bytes_read - landed0, 0.0, tp, trace_event(w.pull)});
-        }
-        w.stats.peer_bytes_read = landed0;  // counted once below, with the split
-        if (step >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_done[buf], 0), "wait");
-        if (any) cuda_check(cudaStreamWaitEvent(w.side, landed[buf], 0), "wait");
+      SplitJobs jobs;
+      bool fused_next = false;
+      if (step + 1 < np) {
+        prepare(step + 1);
+        fused_next = fused_jobs(step + 1, &jobs);
+        if (!fused_next) split_separate(step + 1);
       }
-      std::size_t next = 0;
-      auto issue = [&](const std::vector<Range>& rs, const std::vector<std::array<Planes, 2>>& planes) {
-        for (std::size_t i = 0; i < rs.size(); ++i)
-          for (const Piece& pc : rs[i].panels[p]) {
-            const bool remote = eff_remote[next] != 0;
-            const void* src = eff[next].first;
-            const std::int64_t lds = eff[next].second;
-            ++next;
-            const Planes& pl = planes[i][buf];
-            const std::int64_t off = pc.dst_row * kpitch + pc.dst_k;
-            cuda_check(split_tf32(src, half_in ? 1 : 0, lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
-                                  pl.lo ? pl.lo + off : nullptr, kpitch,
-                                  pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
-                                  pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch,
-                                  w.side),
-                       "split_tf32");
-            w.stats.split_launches += 1;
-            (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
-          }
-      };
-      const std::uint64_t pulled0 = w.stats.peer_bytes_read + w.stats.local_bytes_read;
-      cudaEvent_t ta = trace ? trace_event(w.side) : nullptr;
-      issue(plan.ar, pa);
-      issue(plan.br, pb);
-      if (trace)
-        w.trace.push_back({"pull+split", p, w.stats.peer_bytes_read + w.stats.local_bytes_read - pulled0, 0.0,
-                           ta, trace_event(w.side)});
-      cuda_check(cudaEventRecord(split_done[buf], w.side), "event");
-      cuda_check(cudaStreamWaitEvent(w.stream, split_done[buf], 0), "wait");
+      if (split_ev[step]) cuda_check(cudaStreamWaitEvent(w.stream, split_ev[step], 0), "wait");
       const std::int64_t kw = plan.k0[p + 1] - plan.k0[p];
       cudaEvent_t tg = trace ? trace_event(w.stream) : nullptr;
       const double flops0 = w.stats.gemm_flops;
-      for (const Task& t : plan.tasks) {
+      const std::int64_t ntask = static_cast<std::int64_t>(plan.tasks.size());
+      for (std::int64_t ti = 0; ti < ntask; ++ti) {
+        const Task& t = plan.tasks[ti];
         StoredBlock& cb = w.owned.at({g.c, t.c});
         Tf32x3Args a;
         a.mode = gemm_mode;
@@ -1094,19 +1175,36 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
           a.sync = sync;
           a.sync_bytes = sync_bytes;
         }
+        if (fused_next) {
+          // the next panel's split tiles, spread evenly over this step's launches
+          const std::int64_t total = jobs.job[jobs.n - 1].t0 + split_job_tiles(jobs.job[jobs.n - 1]);
+          jobs.t_begin = total * ti / ntask;
+          jobs.t_end = total * (ti + 1) / ntask;
+          a.split = &jobs;
+        }
         record_timing(w, true);
         cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");
         record_timing(w, false);
         w.stats.gemm_launches += 1;
         w.stats.gemm_flops += 2.0 * static_cast<double>(a.m) * a.n * a.k;
       }
-      if (trace) w.trace.push_back({"gemm", p, 0, w.stats.gemm_flops - flops0, tg, trace_event(w.stream)});
-      cuda_check(cudaEventRecord(gemm_done[buf], w.stream), "event");
+      if (trace)
+        w.trace.push_back({fused_next ? "gemm+split" : "gemm", p, 0, w.stats.gemm_flops - flops0, tg,
+                           trace_event(w.stream)});
+      gemm_ev[step] = new_event();
+      cuda_check(cudaEventRecord(gemm_ev[step], w.stream), "event");
+      if (fused_next) {
+        split_ev[step + 1] = nullptr;  // written inside this step's GEMM launches
+        consumed_ev[step + 1] = gemm_ev[step];
+      }
     }
     if (async_) {
       mark_write(w, w.stream, g.c);
-      mark_read(w, w.side, g.a);
-      mark_read(w, w.side, g.b);
+      // A and B are read by the split stream and by the GEMMs' fused split warps
+      for (cudaStream_t st : {w.side, w.stream}) {
+        mark_read(w, st, g.a);
+        mark_read(w, st, g.b);
+      }
       // panel planes live until the last GEMM of this command has run
       Worker::Inflight f;
       cuda_check(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming), "event");

@@ -95,6 +95,8 @@ struct Worker {
   std::map<BlockKey, StoredBlock> owned;
   std::map<BlockKey, StoredBlock> cache;
   std::map<BlockKey, StoredBlock> replicas;
+  DeviceBuffer pull_flag;  // landing-copy sequence number (written by the pull stream)
+  unsigned pull_seq = 0;
   DeviceBuffer arena;  // exchange buffer peers read (row/col partials, narrowed reshape payloads)
   std::uint64_t seed = 0;
   dm_worker_stats stats{};
