@@ -98,6 +98,13 @@ class DevicePool {
       cudaGetDevice(&prev);
       cudaSetDevice(device_);
       cudaError_t e = cudaMalloc(&p, cls);
+      if (e == cudaErrorMemoryAllocation && stats_.bytes_pooled > 0) {
+        // out of memory with idle pooled blocks of other classes: return them
+        // to the driver and retry once (the reference's host pool would page)
+        cudaGetLastError();
+        release_pooled_locked();
+        e = cudaMalloc(&p, cls);
+      }
       if (prev >= 0) cudaSetDevice(prev);
       if (e != cudaSuccess) {
         cudaGetLastError();
@@ -131,13 +138,19 @@ class DevicePool {
   // Frees every pooled buffer; live buffers stay live (pool.hpp:110-115).
   std::uint64_t trim() {
     std::lock_guard<std::mutex> lk(mu_);
-    std::uint64_t freed = stats_.bytes_pooled;
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(device_);
+    const std::uint64_t freed = release_pooled_locked();
+    if (prev >= 0) cudaSetDevice(prev);
+    return freed;
+  }
+
+  // (mu_ held, device_ current) free every idle pooled block
+  std::uint64_t release_pooled_locked() {
+    const std::uint64_t freed = stats_.bytes_pooled;
     for (auto& [cls, list] : free_lists_)
       for (void* p : list) cudaFree(p);
-    if (prev >= 0) cudaSetDevice(prev);
     free_lists_.clear();
     stats_.bytes_pooled = 0;
     ++generation_;

@@ -269,6 +269,19 @@ void Session::reap_inflight(Worker& w) {
   cudaGetLastError();  // cudaErrorNotReady is not an error here
 }
 
+void Session::bound_inflight(Worker& w) {
+  reap_inflight(w);
+  // Bound the device memory held by queued GEMMs' panel planes: at most
+  // DM_MAX_INFLIGHT (default 2) commands in flight per worker.  Waiting here
+  // cannot deadlock: every rank already issued the older command waited on.
+  const std::size_t cap = static_cast<std::size_t>(std::max<std::int64_t>(1, env_int("DM_MAX_INFLIGHT", 2)));
+  while (w.inflight.size() >= cap) {
+    cuda_check(cudaEventSynchronize(w.inflight.front().done), "cudaEventSynchronize(inflight)");
+    for (cudaEvent_t e : w.inflight.front().events) cudaEventDestroy(e);
+    w.inflight.pop_front();
+  }
+}
+
 // Complete every outstanding asynchronous command on every rank.
 void Session::drain() {
   sync_local();
@@ -724,7 +737,26 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
           }
   }
   const std::int64_t target = env_int("DM_PANEL_K", 8192);
-  if ((plan.has_remote || env_int("DM_PANEL_LOCAL", 0) != 0) && K > 2 * 256 && target > 0) {
+  const std::int64_t local_lead = env_int("DM_PANEL_LOCAL", 0);
+  if (!plan.has_remote && local_lead > 0 && K >= 4 * local_lead) {
+    // All operands local: geometric panels.  Only the narrow lead panel's
+    // split is exposed; every later panel is split by the previous panel's
+    // GEMM (a GEMM of width w hides the split of ~3.7 w, tf32x3_gemm.cu).
+    const std::int64_t growth = std::max<std::int64_t>(2, env_int("DM_PANEL_GROWTH", 3));
+    plan.k0.clear();
+    std::int64_t k = 0, w = (local_lead + 31) / 32 * 32;
+    while (k < K) {
+      plan.k0.push_back(k);
+      if (K - k < w + w * growth / 2) break;  // last panel absorbs a short tail
+      k += w;
+      w *= growth;
+    }
+    plan.k0.push_back(K);
+    for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
+    for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
+    return plan;
+  }
+  if (plan.has_remote && K > 2 * 256 && target > 0) {
     std::int64_t np = std::max<std::int64_t>(2, (K + target - 1) / target);
     np = std::min<std::int64_t>(np, K / 256);
     std::int64_t width = (K + np - 1) / np;
@@ -851,7 +883,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     if (async_) {
       // pulls start once A and B are written everywhere; C is overwritten only
       // after its previous writes and reads (e.g. an async gather) finished
-      reap_inflight(w);
+      bound_inflight(w);
       wait_writes(w.side, g.a);
       wait_writes(w.side, g.b);
       device_barrier(w.side, 1);  // every rank, even one without C blocks
@@ -993,7 +1025,9 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
       cuda_check(cudaEventRecord(e, w.side), "event");
       cuda_check(cudaStreamWaitEvent(w.pull, e, 0), "wait");
     }
-    const bool fuse = env_int("DM_FUSE_SPLIT", 1) != 0 && !half_in;
+    // DM_FUSE_SPLIT: 0 never, 1 when the carrying GEMM hides the split, 2 always
+    const std::int64_t fuse_mode = env_int("DM_FUSE_SPLIT", 1);
+    const bool fuse = fuse_mode != 0 && !half_in;
 
     // One split item per piece: effective source (landing buffer for pieces
     // that crossed a link), target planes, and whether it waits on the flag.
@@ -1087,7 +1121,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         auto [mb, nb] = block_extent(table_.at(g.c).layout.grid, t.c);
         flops += 2.0 * mb * nb * static_cast<double>(plan.k0[order[s - 1] + 1] - plan.k0[order[s - 1]]);
       }
-      if (bytes_in / 150e9 > flops / 300e12) return false;
+      if (fuse_mode == 1 && bytes_in / 150e9 > flops / 300e12) return false;
       out->n = 0;
       std::int64_t t = 0;
       for (const Item& it : items[s]) {

@@ -194,6 +194,7 @@ class Session {
   void mid_barrier();
   void drain();
   void reap_inflight(Worker& w);
+  void bound_inflight(Worker& w);  // reap, then wait while >= DM_MAX_INFLIGHT GEMMs queued
   cudaEvent_t ev_get(Worker& w);
   void mark_write(Worker& w, cudaStream_t s, MatrixId id);
   void mark_read(Worker& w, cudaStream_t s, MatrixId id);

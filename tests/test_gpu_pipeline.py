@@ -1,0 +1,91 @@
+"""The K-panel pipeline of general_gemm under every schedule it can take.
+
+The distributed GEMM streams op(A)/op(B) in K panels (session.cpp run_gemm):
+the first panel is split by its own kernels, later panels either by the
+previous panel's GEMM launch (two fused split warps, DM_FUSE_SPLIT=1) or by
+separate split kernels; pieces on another GPU land through copy engines first.
+Whatever the schedule, the result must match the oracle within the
+reference's fp32 bound (tests/acceptance.cpp:66-72: relFro <= 1e-5), with the
+reference's transposes and alpha/beta (tests/test_dist_ops.cpp:136-147, 267-282).
+"""
+import numpy as np
+import pytest
+
+from paper_1604_01416_b200 import Config, FillKind, LayoutKind, Session, make_layout
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+def relfro(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    return float(np.linalg.norm(got - want) / np.linalg.norm(want))
+
+
+def ref_gemm(alpha, A, ta, B, tb, beta, C0):
+    a, b = A.astype(np.float64), B.astype(np.float64)
+    return alpha * ((a.T if ta else a) @ (b.T if tb else b)) + beta * C0.astype(np.float64)
+
+
+def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77):
+    ta, tb = bool(trans & 1), bool(trans & 2)
+    with Session(Config(worker_count=P, root_seed=seed + trans, devices=[0] * P)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, n, n, blk[0], blk[1], P)
+        a, b, c = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(3))
+        A, B, C0 = s.gather(a), s.gather(b), s.gather(c)
+        s.reset_worker_stats()
+        s.general_gemm(alpha, a, b, beta, c, ta, tb)
+        got = s.gather(c)
+        splits = sum(s.worker_stats(w).split_launches for w in range(P))
+        return relfro(got, ref_gemm(alpha, A, ta, B, tb, beta, C0)), splits
+
+
+@pytest.mark.parametrize("trans", [0, 1, 2, 3])
+@pytest.mark.parametrize("lead", [0, 128])
+def test_panels_fused_vs_separate(cuda, monkeypatch, trans, lead):
+    monkeypatch.setenv("DM_PANEL_K", "512")
+    monkeypatch.setenv("DM_LEAD_PANEL_K", str(lead))
+    res = {}
+    for fuse in (2, 0):  # 2: fuse even where the GEMM is too short to hide it
+        monkeypatch.setenv("DM_FUSE_SPLIT", str(fuse))
+        res[fuse] = run_case(4, 1536, (768, 768), trans)
+        assert res[fuse][0] <= TOL, (fuse, res[fuse])
+    # fused panels are split inside the GEMM launches: fewer split kernels
+    assert res[2][1] < res[0][1]
+
+
+@pytest.mark.parametrize("trans", [0, 3])
+def test_unaligned_pieces_fall_back(cuda, monkeypatch, trans):
+    # odd block pitches (233 / 175 columns) are not 16-B aligned: the fused
+    # split refuses them and the panel is split by its own kernels
+    monkeypatch.setenv("DM_PANEL_K", "256")
+    monkeypatch.setenv("DM_FUSE_SPLIT", "2")
+    err, _ = run_case(3, 700, (233, 175), trans)
+    assert err <= TOL
+
+
+@pytest.mark.parametrize("trans", [0, 1, 2, 3])
+def test_geometric_local_panels(cuda, monkeypatch, trans):
+    # one worker, all operands local: geometric panels (lead 256, x3)
+    monkeypatch.setenv("DM_PANEL_LOCAL", "256")
+    monkeypatch.setenv("DM_FUSE_SPLIT", "2")
+    err, _ = run_case(1, 1280, (1280, 1280), trans)
+    assert err <= TOL
+
+
+def test_beta_zero_ignores_garbage_c_across_panels(cuda, monkeypatch):
+    # beta == 0 never reads C on the first panel (kernels.hpp:69-71); later
+    # panels accumulate into the C the first one wrote
+    monkeypatch.setenv("DM_PANEL_K", "512")
+    n = 1024
+    with Session(Config(worker_count=4, root_seed=3, devices=[0] * 4)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, n, n, 512, 512, 4)
+        a, b = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(2))
+        garbage = np.full((n, n), np.nan, np.float32)
+        c = s.create_matrix(lay, fill=FillKind.FromHost, host=garbage)
+        A, B = s.gather(a), s.gather(b)
+        s.general_gemm(1.0, a, b, 0.0, c)
+        got = s.gather(c)
+        assert np.isfinite(got).all()
+        assert relfro(got, A.astype(np.float64) @ B.astype(np.float64)) <= TOL
