@@ -769,7 +769,7 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     // If even the least-remote panel must cross a link, cut a narrow lead
     // panel off it: only that sliver's pull is exposed before the first GEMM,
     // the rest streams behind compute.
-    const std::int64_t lead = env_int("DM_LEAD_PANEL_K", 1024);
+    const std::int64_t lead = env_int("DM_LEAD_PANEL_K", 0);
     const int np0 = static_cast<int>(plan.k0.size()) - 1;
     std::vector<std::uint64_t> rb(np0, 0);
     for (int p = 0; p < np0; ++p)
@@ -782,7 +782,12 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
           }
     const int best = static_cast<int>(std::min_element(rb.begin(), rb.end()) - rb.begin());
     if (lead > 0 && rb[best] > 0 && plan.k0[best + 1] - plan.k0[best] > 2 * lead) {
-      plan.k0.insert(plan.k0.begin() + best + 1, plan.k0[best] + lead);
+      // Ramp: lead, lead, 2 lead, 4 lead, ... so each sub-panel's GEMM is long
+      // enough to hide the pull and fused split of the next one.
+      const std::int64_t start = plan.k0[best], end = plan.k0[best + 1];
+      std::vector<std::int64_t> cuts;
+      for (std::int64_t c = lead; start + c < end && end - (start + c) >= lead; c *= 2) cuts.push_back(start + c);
+      plan.k0.insert(plan.k0.begin() + best + 1, cuts.begin(), cuts.end());
       for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
       for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
     }
