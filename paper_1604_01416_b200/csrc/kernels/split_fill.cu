@@ -73,8 +73,8 @@ __global__ void split_trans_kernel(const T* __restrict__ src, int64_t lds, int64
 // ---- vectorised fp32 variants: 4 consecutive elements per access, 4 accesses
 // in flight per thread.
 // (4*WY) rows x 128 k per block (32 x WY threads); requires 16-B aligned rows.
-// <= 40 registers so blocks fit beside a resident GEMM CTA (320 threads x
-// 168 registers leave 11.7 K of the SM's 64 K).
+// (Measured 6.6 TB/s of HBM traffic at 1 GiB input; later K panels are split
+// by the GEMM's own split warps instead, see tf32x3_gemm.cu.)
 template <int WY>
 __global__ void __launch_bounds__(32 * WY, 48 / WY) split_direct_vec4_kernel(const float* __restrict__ src,
                                                                             int64_t lds, int64_t rows,
@@ -101,40 +101,50 @@ __global__ void __launch_bounds__(32 * WY, 48 / WY) split_direct_vec4_kernel(con
   }
 }
 
-// out[r][k] = src[k][r]: 32 k x 128 r per block through shared memory.
+// out[r][k] = src[k][r]: 64 k x 128 r per block through shared memory.
+// Reads: 512-B row segments, all of a thread's float4 loads in flight before
+// the smem stores.  Writes: a thread pair per output row, the pair's float4s
+// interleaved by 4 k (conflict-free smem reads), 32 B sectors complete.
+constexpr int kTransK = 64;
 template <int WY>
-__global__ void __launch_bounds__(32 * WY, 48 / WY) split_trans_vec4_kernel(const float* __restrict__ src,
+__global__ void __launch_bounds__(32 * WY, 24 / WY) split_trans_vec4_kernel(const float* __restrict__ src,
                                                                            int64_t lds, int64_t rows,
                                                                            int64_t kcols, Planes p) {
-  __shared__ float tile[32][128 + 4];
-  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 32;
+  __shared__ __align__(16) float tile[kTransK][128 + 4];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kTransK;
   const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 128;
   const int t = threadIdx.y * 32 + threadIdx.x;
   const int64_t r = r0 + threadIdx.x * 4;
-#pragma unroll 4
-  for (int i = 0; i < 32 / WY; ++i) {
-    const int kl = threadIdx.y + WY * i;
-    const int64_t k = k0 + kl;
-    if (k >= kcols) continue;
-    if (r + 4 <= rows) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(src + k * lds + r));
-      tile[kl][threadIdx.x * 4 + 0] = v.x;
-      tile[kl][threadIdx.x * 4 + 1] = v.y;
-      tile[kl][threadIdx.x * 4 + 2] = v.z;
-      tile[kl][threadIdx.x * 4 + 3] = v.w;
-    } else {
-      for (int u = 0; u < 4; ++u)
-        if (r + u < rows) tile[kl][threadIdx.x * 4 + u] = __ldg(src + k * lds + r + u);
+  constexpr int kLoads = kTransK / WY;
+  constexpr int kBatch = kLoads < 8 ? kLoads : 8;
+  const bool full_r = r + 4 <= rows;
+#pragma unroll
+  for (int i0 = 0; i0 < kLoads; i0 += kBatch) {
+    float4 v[kBatch];
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int64_t k = k0 + threadIdx.y + WY * (i0 + i);
+      if (k < kcols && full_r) v[i] = __ldcs(reinterpret_cast<const float4*>(src + k * lds + r));
+    }
+#pragma unroll
+    for (int i = 0; i < kBatch; ++i) {
+      const int kl = threadIdx.y + WY * (i0 + i);
+      if (k0 + kl >= kcols) continue;
+      if (full_r) {
+        *reinterpret_cast<float4*>(&tile[kl][threadIdx.x * 4]) = v[i];
+      } else {
+        for (int u = 0; u < 4; ++u)
+          if (r + u < rows) tile[kl][threadIdx.x * 4 + u] = __ldcs(src + (k0 + kl) * lds + r + u);
+      }
     }
   }
   __syncthreads();
-  // 128 r x 32 k out: a thread pair per row, 16 consecutive k each (4 x float4)
   for (int rl = t >> 1; rl < 128; rl += 16 * WY) {
     const int64_t ro = r0 + rl;
     if (ro >= rows) break;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int kl = (t & 1) * 16 + 4 * j;
+    for (int j = 0; j < kTransK / 8; ++j) {
+      const int kl = 8 * j + 4 * (t & 1);
       const int64_t k = k0 + kl;
       if (k >= kcols) continue;
       if (k + 4 <= kcols) {
@@ -152,7 +162,7 @@ void launch_split_vec4(const float* s32, int64_t lds, int trans, int64_t rows, i
                        cudaStream_t stream) {
   const dim3 block(32, WY);
   if (trans) {
-    const dim3 g(static_cast<unsigned>((kcols + 31) / 32), static_cast<unsigned>((rows + 127) / 128));
+    const dim3 g(static_cast<unsigned>((kcols + kTransK - 1) / kTransK), static_cast<unsigned>((rows + 127) / 128));
     split_trans_vec4_kernel<WY><<<g, block, 0, stream>>>(s32, lds, rows, kcols, p);
   } else {
     const dim3 g(static_cast<unsigned>((kcols + 127) / 128), static_cast<unsigned>((rows + 4 * WY - 1) / (4 * WY)));
