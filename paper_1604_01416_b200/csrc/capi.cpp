@@ -131,6 +131,12 @@ int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const flo
     args.beta = static_cast<float>(beta);
     args.read_c = beta != 0.0 ? 1 : 0;
     args.cta_group = cta_group;
+    dm::DeviceBuffer ws;
+    if (const size_t wsn = dm::tf32x3_splitk_bytes(args)) {
+      ws = pool.acquire(wsn);
+      args.ws = ws.f32();
+      args.ws_bytes = ws.capacity();
+    }
     dm::cuda_check(dm::tf32x3_gemm(args, st), "tf32x3_gemm");
     // scratch goes back to the pool: make the seam synchronous on its stream
     dm::cuda_check(cudaStreamSynchronize(st), "local_gemm sync");

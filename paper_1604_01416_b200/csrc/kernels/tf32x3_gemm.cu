@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 
 #include "ptx.cuh"
@@ -69,7 +70,20 @@ struct EpiParams {
   int l2_policy;        // 0 evict_normal, 1 evict_last, 2 evict_first (TMA cache hint)
   int lockstep;         // >0: producers of a wave stay within `lockstep` k-blocks
   unsigned* sync;       // lockstep counters [waves * epochs], zeroed per launch
+  int ksplit;           // >1: split-K; item (s, tile) writes its fp32 partial to ws[s]
+  float* ws;            // [ksplit][m][n] partial tiles (ksplit > 1)
 };
+
+// Work item t of a launch: tile t % tiles of K-split t / tiles, whose k-blocks
+// are [kb_lo, kb_hi) (empty ranges still store a zero partial).
+__device__ __forceinline__ void item_range(int t, int total_tiles, int num_kb, int ksplit, int& tile, int& split,
+                                           int& kb_lo, int& kb_hi) {
+  split = t / total_tiles;
+  tile = t - split * total_tiles;
+  const int per = (num_kb + ksplit - 1) / ksplit;
+  kb_lo = min(num_kb, split * per);
+  kb_hi = min(num_kb, kb_lo + per);
+}
 
 template <int CG>
 __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int G, int& mt, int& nt) {
@@ -221,10 +235,10 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   const int tiles_m = (ep.m + C::kUmmaM - 1) / C::kUmmaM;
   const int tiles_n = (ep.n + C::kUmmaN - 1) / C::kUmmaN;
   const int total_tiles = tiles_m * tiles_n;
+  const int total_items = total_tiles * ep.ksplit;
   const int unit = blockIdx.x / CG;
   const int num_units = gridDim.x / CG;
   const int num_kb = (K + C::kBK - 1) / C::kBK;
-  const int num_chunks = (num_kb + kc_blocks - 1) / kc_blocks;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -254,14 +268,15 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
                                                : policy_evict_normal();
       const int epochs = ep.lockstep > 0 ? (num_kb + ep.lockstep - 1) / ep.lockstep : 0;
       int wave = 0;
-      for (int t = unit; t < total_tiles; t += num_units, ++wave) {
+      for (int t = unit; t < total_items; t += num_units, ++wave) {
         // CTAs of this wave (the last wave may be partial)
-        const int wave_ctas = CG * min(num_units, total_tiles - wave * num_units);
-        int mt, nt;
-        tile_coords<CG>(t, tiles_m, tiles_n, ep.group_m, mt, nt);
+        const int wave_ctas = CG * min(num_units, total_items - wave * num_units);
+        int tile, split, kb_lo, kb_hi, mt, nt;
+        item_range(t, total_tiles, num_kb, ep.ksplit, tile, split, kb_lo, kb_hi);
+        tile_coords<CG>(tile, tiles_m, tiles_n, ep.group_m, mt, nt);
         const int arow = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta;
         const int brow = nt * C::kUmmaN + static_cast<int>(cta_rank) * C::kRowsPerCta;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb_lo; kb < kb_hi; ++kb) {
           if (epochs > 0 && kb % ep.lockstep == 0) {
             // Software lockstep: CTAs sharing A/B tiles read the same k-slices
             // at about the same time, so L2 serves the sharers instead of DRAM.
@@ -318,14 +333,17 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0;
-      for (int t = unit; t < total_tiles; t += num_units) {
+      for (int t = unit; t < total_items; t += num_units) {
+        int tile, split, kb_lo, kb_hi;
+        item_range(t, total_tiles, num_kb, ep.ksplit, tile, split, kb_lo, kb_hi);
+        const int num_chunks = (kb_hi - kb_lo + kc_blocks - 1) / kc_blocks;
         for (int ch = 0; ch < num_chunks; ++ch, ++chunk_ctr) {
           const int buf = chunk_ctr & 1;
           mbar_wait(smem_u32(&cempty_bar[buf]), ((chunk_ctr >> 1) & 1) ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(buf * C::kAccCols);
-          const int kb0 = ch * kc_blocks;
-          const int kb1 = min(num_kb, kb0 + kc_blocks);
+          const int kb0 = kb_lo + ch * kc_blocks;
+          const int kb1 = min(kb_hi, kb0 + kc_blocks);
           for (int kb = kb0; kb < kb1; ++kb) {
             mbar_wait(smem_u32(&full_bar[stage]), phase);
             tc_fence_after();
@@ -387,9 +405,11 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     const int col_off = half * C::kColsPerThread;
     const uint32_t lane_addr = static_cast<uint32_t>(q * 32) << 16;
     uint32_t chunk_ctr = 0;
-    for (int t = unit; t < total_tiles; t += num_units) {
-      int mt, nt;
-      tile_coords<CG>(t, tiles_m, tiles_n, ep.group_m, mt, nt);
+    for (int t = unit; t < total_items; t += num_units) {
+      int tile, split, kb_lo, kb_hi, mt, nt;
+      item_range(t, total_tiles, num_kb, ep.ksplit, tile, split, kb_lo, kb_hi);
+      tile_coords<CG>(tile, tiles_m, tiles_n, ep.group_m, mt, nt);
+      const int num_chunks = (kb_hi - kb_lo + kc_blocks - 1) / kc_blocks;
       float master[C::kColsPerThread];
 #pragma unroll
       for (int j = 0; j < C::kColsPerThread; ++j) master[j] = 0.0f;
@@ -413,26 +433,32 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           else mbar_arrive_cluster(smem_u32(&cempty_bar[buf]), 0);
         }
       }
-      // alpha / beta epilogue straight from the master registers
+      // alpha / beta epilogue straight from the master registers; a split-K
+      // item stores its raw partial (alpha = 1, no C) to its workspace slice
+      const bool part = ep.ksplit > 1;
+      float* const cbase = part ? ep.ws + static_cast<int64_t>(split) * ep.m * ep.n : ep.c;
+      const int64_t ldc = part ? static_cast<int64_t>(ep.n) : ep.ldc;
+      const float alpha = part ? 1.0f : ep.alpha;
+      const int read_c = part ? 0 : ep.read_c;
       const int row = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta + q * 32 +
                       static_cast<int>(lane);
       if (row >= ep.m) continue;
       const int c0 = nt * C::kUmmaN + col_off;
-      if (ep.c_half) {
+      if (!part && ep.c_half) {
         // Half16 C: beta*C widened exactly, result rounded once (narrow_store)
-        __half* hrow = reinterpret_cast<__half*>(ep.c) + static_cast<int64_t>(row) * ep.ldc + c0;
+        __half* hrow = reinterpret_cast<__half*>(cbase) + static_cast<int64_t>(row) * ldc + c0;
 #pragma unroll
         for (int j = 0; j < C::kColsPerThread; ++j) {
           if (c0 + j < ep.n) {
-            float v = __fmul_rn(ep.alpha, master[j]);
-            if (ep.read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, __half2float(hrow[j])));
+            float v = __fmul_rn(alpha, master[j]);
+            if (read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, __half2float(hrow[j])));
             hrow[j] = __float2half_rn(v);
           }
         }
         continue;
       }
-      float* crow = ep.c + static_cast<int64_t>(row) * ep.ldc + c0;
-      const bool vec_ok = ((ep.ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(ep.c) & 15) == 0);
+      float* crow = cbase + static_cast<int64_t>(row) * ldc + c0;
+      const bool vec_ok = ((ldc & 3) == 0) && ((reinterpret_cast<uintptr_t>(cbase) & 15) == 0);
       // C is read in groups of kEpiGroup float4 issued back to back (one
       // round trip per group, not per float4): with beta != 0 the epilogue
       // must not hold the chunk buffers longer than the MMA's two-chunk slack.
@@ -443,7 +469,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
         if (cc0 >= ep.n) break;
         if (vec_ok && cc0 + 4 * kEpiGroup <= ep.n) {
           float4 cv[kEpiGroup];
-          if (ep.read_c) {
+          if (read_c) {
 #pragma unroll
             for (int u = 0; u < kEpiGroup; ++u) cv[u] = __ldcs(reinterpret_cast<const float4*>(crow + 4 * (j0 + u)));
           }
@@ -452,8 +478,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             const int j = j0 + u;
             float o[4];
 #pragma unroll
-            for (int q2 = 0; q2 < 4; ++q2) o[q2] = __fmul_rn(ep.alpha, master[4 * j + q2]);
-            if (ep.read_c) {
+            for (int q2 = 0; q2 < 4; ++q2) o[q2] = __fmul_rn(alpha, master[4 * j + q2]);
+            if (read_c) {
               o[0] = __fadd_rn(o[0], __fmul_rn(ep.beta, cv[u].x));
               o[1] = __fadd_rn(o[1], __fmul_rn(ep.beta, cv[u].y));
               o[2] = __fadd_rn(o[2], __fmul_rn(ep.beta, cv[u].z));
@@ -466,8 +492,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           for (int jj = 0; jj < 4 * kEpiGroup; ++jj) {
             const int cc = cc0 + jj;
             if (cc < ep.n) {
-              float v = __fmul_rn(ep.alpha, master[4 * j0 + jj]);
-              if (ep.read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, crow[4 * j0 + jj]));
+              float v = __fmul_rn(alpha, master[4 * j0 + jj]);
+              if (read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, crow[4 * j0 + jj]));
               crow[4 * j0 + jj] = v;
             }
           }
@@ -541,6 +567,55 @@ int make_operand_map(CUtensorMap* map, const void* base, int64_t rows, int64_t k
   return r == CUDA_SUCCESS ? 0 : -2;
 }
 
+int device_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+int pick_cta_group(const Tf32x3Args& a) {
+  if (a.cta_group != 0) return a.cta_group;
+  // Pairs pay off once there are enough 256x256 tiles to fill the machine.
+  const int64_t pair_tiles = ((a.m + 255) / 256) * ((a.n + 255) / 256);
+  return pair_tiles >= 74 ? 2 : 1;
+}
+
+// Split-K factor: when the tiles cannot fill the machine (tall-skinny C, e.g.
+// the FC layers' batch-wide strips), K is cut into S ranges of >= 512 so
+// tiles x S work items cover the SMs; partials are summed in fixed order.
+int pick_ksplit(const Tf32x3Args& a, int cg, int sms) {
+  if (a.ksplit == 1 || a.k <= 0) return 1;
+  const int64_t tiles = ((a.m + 128 * cg - 1) / (128 * cg)) * ((a.n + 128 * cg - 1) / (128 * cg));
+  const int64_t units = sms / cg;
+  const int64_t num_kb = (a.k + 31) / 32;
+  int64_t S = a.ksplit > 1 ? a.ksplit : (2 * tiles <= units ? std::min<int64_t>(units / tiles, num_kb / 16) : 1);
+  S = std::max<int64_t>(1, std::min<int64_t>(S, 32));
+  return static_cast<int>(S);
+}
+
+// out = alpha * sum_s ws[s] + beta * C, s ascending (deterministic).
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int m, int n, float* c, int c_half,
+                                     int64_t ldc, float alpha, float beta, int read_c) {
+  const int64_t total = static_cast<int64_t>(m) * n;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float acc = __ldcs(ws + i);
+    for (int sp = 1; sp < S; ++sp) acc = __fadd_rn(acc, __ldcs(ws + sp * total + i));
+    const int64_t r = i / n, cc = i % n;
+    float o = __fmul_rn(alpha, acc);
+    if (c_half) {
+      __half* h = reinterpret_cast<__half*>(c) + r * ldc + cc;
+      if (read_c) o = __fadd_rn(o, __fmul_rn(beta, __half2float(*h)));
+      *h = __float2half_rn(o);
+    } else {
+      float* f = c + r * ldc + cc;
+      if (read_c) o = __fadd_rn(o, __fmul_rn(beta, *f));
+      *f = o;
+    }
+  }
+}
+
 template <int CG, int MODE>
 cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   using C = Cfg<CG>;
@@ -573,13 +648,17 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   int sms = a.num_sms;
   if (sms <= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tiles = ((a.m + C::kUmmaM - 1) / C::kUmmaM) * ((a.n + C::kUmmaN - 1) / C::kUmmaN);
+  int ksplit = pick_ksplit(a, CG, sms);
+  if (ksplit > 1 && (a.ws == nullptr ||
+                     a.ws_bytes < static_cast<size_t>(ksplit) * static_cast<size_t>(a.m * a.n) * sizeof(float)))
+    ksplit = 1;  // no workspace: one item per tile
   int units = sms / CG;
-  if (units > tiles) units = tiles;
+  if (units > tiles * ksplit) units = tiles * ksplit;
   if (units < 1) units = 1;
 
   EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
-               a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr};
-  if (a.lockstep > 0 && a.sync != nullptr) {
+               a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws};
+  if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1) {
     const size_t need = tf32x3_sync_bytes(a);
     if (a.sync_bytes < need) return cudaErrorInvalidValue;
     ep.lockstep = a.lockstep;
@@ -604,8 +683,14 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   const int kc_blocks = a.flush_k > 0 ? static_cast<int>((a.flush_k + C::kBK - 1) / C::kBK) : 8;
   SplitJobs sj;
   if (a.split != nullptr) sj = *a.split;
-  return cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG, MODE>, maps, static_cast<int>(a.k),
-                            kc_blocks, ep, sj);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG, MODE>, maps, static_cast<int>(a.k),
+                                     kc_blocks, ep, sj);
+  if (e != cudaSuccess || ksplit == 1) return e;
+  const int64_t total = a.m * a.n;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * sms));
+  splitk_reduce_kernel<<<blocks, 256, 0, stream>>>(a.ws, ksplit, static_cast<int>(a.m), static_cast<int>(a.n),
+                                                   a.c, a.c_half, a.ldc, a.alpha, a.beta, a.read_c);
+  return cudaGetLastError();
 }
 
 }  // namespace
@@ -637,6 +722,14 @@ bool split_job_fusable(const SplitJob& j) {
          (j.hi16 == nullptr || (al(j.hi16, 8) && al(j.lo16, 8) && (j.ldo16 & 3) == 0));
 }
 
+size_t tf32x3_splitk_bytes(const Tf32x3Args& a) {
+  if (a.m <= 0 || a.n <= 0 || a.k <= 0) return 0;
+  const int cg = pick_cta_group(a);
+  const int sms = a.num_sms > 0 ? a.num_sms : device_sms();
+  const int S = pick_ksplit(a, cg, sms);
+  return S > 1 ? static_cast<size_t>(S) * static_cast<size_t>(a.m * a.n) * sizeof(float) : 0;
+}
+
 size_t tf32x3_sync_bytes(const Tf32x3Args& a) {
   if (a.lockstep <= 0 || a.m <= 0 || a.n <= 0 || a.k <= 0) return 0;
   const int64_t tiles = ((a.m + 127) / 128) * ((a.n + 127) / 128);  // upper bound (1-CTA tiles)
@@ -664,12 +757,7 @@ cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
   if (a.mode == kModeMixed && ((a.lda16 & 7) || (a.ldb16 & 7) || mis(a.a_hi16) || mis(a.a_lo16) ||
                                mis(a.b_hi16) || mis(a.b_lo16)))
     return cudaErrorMisalignedAddress;
-  int cg = a.cta_group;
-  if (cg == 0) {
-    // Pairs pay off once there are enough 256x256 tiles to fill the machine.
-    const int64_t pair_tiles = ((a.m + 255) / 256) * ((a.n + 255) / 256);
-    cg = pair_tiles >= 74 ? 2 : 1;
-  }
+  const int cg = pick_cta_group(a);
   if (a.mode == kModeMixed) return cg == 2 ? launch<2, kModeMixed>(a, stream) : launch<1, kModeMixed>(a, stream);
   return cg == 2 ? launch<2, kModeTf32x3>(a, stream) : launch<1, kModeTf32x3>(a, stream);
 }

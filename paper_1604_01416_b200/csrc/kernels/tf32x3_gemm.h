@@ -77,6 +77,9 @@ struct Tf32x3Args {
   unsigned* sync = nullptr;  // lockstep counters (>= tf32x3_sync_bytes), private to this launch
   size_t sync_bytes = 0;
   const SplitJobs* split = nullptr;  // fused split work for this launch (may be null)
+  int ksplit = 0;         // split-K: 0 auto (tiles cannot fill the SMs), 1 off, >1 forced
+  float* ws = nullptr;    // split-K partials (>= tf32x3_splitk_bytes); no workspace = no split
+  size_t ws_bytes = 0;
 };
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);
@@ -85,6 +88,9 @@ cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);
 // Lockstep requires every CTA of the launch to be co-resident: do not enable it
 // when other persistent kernels can share the device concurrently.
 size_t tf32x3_sync_bytes(const Tf32x3Args& args);
+
+// Workspace bytes for the split-K partials this launch would use (0: none).
+size_t tf32x3_splitk_bytes(const Tf32x3Args& args);
 
 // Elementwise split of a strided fp32 panel into K-major planes:
 //   x[r][k] = trans ? src[k*lds + r] : src[r*lds + k],  r < rows, k < kcols

@@ -756,7 +756,15 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
     return plan;
   }
-  if (plan.has_remote && K > 2 * 256 && target > 0) {
+  // Pipelining pays only when there is enough math to hide pulls behind;
+  // small GEMMs (latency-bound) take one panel.
+  double work = 0;
+  for (const Task& t : plan.tasks) {
+    auto [mb, nb] = block_extent(gc, t.c);
+    work += 2.0 * mb * nb * static_cast<double>(K);
+  }
+  const double min_work = static_cast<double>(env_int("DM_PIPELINE_MIN_GFLOP", 200)) * 1e9;
+  if (plan.has_remote && K > 2 * 256 && target > 0 && work >= min_work) {
     std::int64_t np = std::max<std::int64_t>(2, (K + target - 1) / target);
     np = std::min<std::int64_t>(np, K / 256);
     std::int64_t width = (K + np - 1) / np;
@@ -905,6 +913,8 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     const int lockstep = sharing == 1 ? lockstep_env : 0;
     unsigned* sync = nullptr;
     std::size_t sync_bytes = 0;
+    float* ksplit_ws = nullptr;  // split-K partials, shared by this worker's launches (stream-ordered)
+    std::size_t ksplit_ws_bytes = 0;
     const int np = static_cast<int>(plan.k0.size()) - 1;
     std::int64_t kmax = 0;
     for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
@@ -969,7 +979,11 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     // local landing buffer (no SMs taken from the concurrently running GEMM);
     // the split then reads local HBM.  Landing buffers are double-buffered so
     // the copy of panel s+1 overlaps the split and GEMM of panel s.
-    const bool use_ce = env_int("DM_PULL_CE", 1) != 0;
+    // Copy engines for remote pieces only when panels pipeline: there the
+    // transfer must not take SMs from the concurrently running GEMM.  A
+    // single-panel command has nothing to overlap, and one split kernel that
+    // reads peer memory directly moves the bytes once instead of twice.
+    const bool use_ce = env_int("DM_PULL_CE", 1) != 0 && np > 1;
     auto resolve = [&](const Piece& pc, bool* remote, bool* cross) {
       const void* src = static_cast<const char*>(source_ptr(w, pc.matrix, pc.coord, pol, remote)) +
                         pc.src_off * static_cast<std::int64_t>(esz);
@@ -1220,6 +1234,15 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
           jobs.t_begin = total * ti / ntask;
           jobs.t_end = total * (ti + 1) / ntask;
           a.split = &jobs;
+        }
+        if (const std::size_t need = tf32x3_splitk_bytes(a)) {
+          if (need > ksplit_ws_bytes) {
+            lv.bufs.push_back(w.pool->acquire(need));
+            ksplit_ws = lv.bufs.back().f32();
+            ksplit_ws_bytes = lv.bufs.back().capacity();
+          }
+          a.ws = ksplit_ws;
+          a.ws_bytes = ksplit_ws_bytes;
         }
         record_timing(w, true);
         cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");

@@ -41,19 +41,26 @@ def main():
     lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // pr, n // pc, world)
     a, b, c = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(3))
     A, B, C0 = s.gather(a), s.gather(b), s.gather(c)   # root 0 assembles (others untouched)
-    for trans in range(4):
-        ta, tb = bool(trans & 1), bool(trans & 2)
-        s.general_gemm(1.5, a, b, -0.5, c, ta, tb)
-        got = s.gather(c)
-        if rank == 0:
-            want = orc.local_gemm(1.5, A, ta, B, tb, -0.5, C0)
-            results[f"general_t{trans}"] = orc.rel_frobenius(got, want)
-            C0 = got  # next GEMM reads this C
-        else:
-            C0 = None
-        st = s.worker_stats(rank)
-        results[f"peer_bytes_r{rank}_t{trans}"] = int(st.peer_bytes_read)
-        s.reset_worker_stats()
+    # default schedule, then the K-panel pipeline forced on at this small size:
+    # copy-engine landing + stream flags + split warps fused into the GEMM
+    forced = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PANEL_K": "512", "DM_FUSE_SPLIT": "2"}
+    for tag, env in (("", {}), ("ce_", forced)):
+        os.environ.update(env)
+        for trans in range(4):
+            ta, tb = bool(trans & 1), bool(trans & 2)
+            s.general_gemm(1.5, a, b, -0.5, c, ta, tb)
+            got = s.gather(c)
+            if rank == 0:
+                want = orc.local_gemm(1.5, A, ta, B, tb, -0.5, C0)
+                results[f"general_{tag}t{trans}"] = orc.rel_frobenius(got, want)
+                C0 = got  # next GEMM reads this C
+            else:
+                C0 = None
+            st = s.worker_stats(rank)
+            results[f"peer_bytes_{tag}r{rank}_t{trans}"] = int(st.peer_bytes_read)
+            s.reset_worker_stats()
+        for k in env:
+            del os.environ[k]
     # inputs bit-exact with the reference's seeded fill (same layout, same ids)
     if rank == 0:
         results["A_bitexact"] = bool(A.tobytes() == orc.seeded_matrix(42, 1, 3, n, n, n // pr, n // pc).tobytes())

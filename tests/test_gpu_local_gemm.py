@@ -87,3 +87,25 @@ def test_large_k_accuracy(cuda, mode, cg, k):
     truncating TMEM accumulator near 1e-4).  The reference's own fp32
     k-ascending loop is ~3e-6 from exact at K=32768."""
     assert _run(cuda, 512, 512, k, False, False, 1.0, 0.0, cg, seed=7) <= 3e-6
+
+
+@pytest.mark.parametrize("trans", [0, 1, 2, 3])
+@pytest.mark.parametrize("m,n,k", [(128, 128, 8192), (4096, 64, 9216), (200, 72, 3000), (64, 1024, 4096)])
+def test_split_k_shapes(cuda, mode, trans, m, n, k):
+    # few output tiles, long K: split-K work items, partials summed in fixed order
+    ta, tb = bool(trans & 1), bool(trans & 2)
+    assert _run(cuda, m, n, k, ta, tb, 1.5, -0.5, 0, seed=trans) <= TOL
+
+
+def test_split_k_deterministic(cuda):
+    import torch
+    from paper_1604_01416_b200 import local_gemm
+    g = torch.Generator(device="cpu").manual_seed(3)
+    A = (torch.rand((256, 8192), generator=g) * 2 - 1).to(cuda)
+    B = (torch.rand((8192, 96), generator=g) * 2 - 1).to(cuda)
+    outs = []
+    for _ in range(3):
+        C = torch.zeros((256, 96), device=cuda)
+        local_gemm(1.0, A, False, B, False, 0.0, C)
+        outs.append(C.cpu())
+    assert all(torch.equal(outs[0], o) for o in outs[1:])

@@ -28,6 +28,12 @@ def ref_gemm(alpha, A, ta, B, tb, beta, C0):
     return alpha * ((a.T if ta else a) @ (b.T if tb else b)) + beta * C0.astype(np.float64)
 
 
+@pytest.fixture(autouse=True)
+def _pipeline_on(monkeypatch):
+    # these sizes are below the work threshold that turns the K pipeline on
+    monkeypatch.setenv("DM_PIPELINE_MIN_GFLOP", "0")
+
+
 def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77):
     ta, tb = bool(trans & 1), bool(trans & 2)
     with Session(Config(worker_count=P, root_seed=seed + trans, devices=[0] * P)) as s:

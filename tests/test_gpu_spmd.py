@@ -37,6 +37,7 @@ def test_spmd_parity(cuda):
     res = json.loads(line[len("SPMD_RESULTS "):])
     for t in range(4):
         assert res[f"general_t{t}"] <= 1e-5
+        assert res[f"general_ce_t{t}"] <= 1e-5  # copy-engine landing + fused split pipeline
     assert res["A_bitexact"]
     assert all(res[f"own_blocks_r{r}"] for r in range(n))
     # 2-D pull: every rank reads exactly its off-owner A row panel + B column panel
@@ -46,6 +47,7 @@ def test_spmd_parity(cuda):
         N = 1536
         want = 4 * (N // pr) * (N - N // pc) + 4 * (N // pc) * (N - N // pr)
         assert all(res[f"peer_bytes_r{r}_t0"] == want for r in range(n))
+        assert all(res[f"peer_bytes_ce_r{r}_t0"] == want for r in range(n))
     assert res["sweep_worst"] <= 1e-5
     assert res["fc_fwd"] <= 1e-5 and res["fc_bwd"] <= 1e-5
     assert all(res[f"bwd_peer_bytes_r{r}"] == 0 for r in range(n))
