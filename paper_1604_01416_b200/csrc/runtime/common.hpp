@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -17,6 +18,25 @@
 #include "../../../include/dmath_b200.h"
 
 namespace dm {
+
+// Current-device scope (restores the caller's device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
+// Integer tuning knob from the environment (read per call, so tests and
+// benches can flip schedules between commands).
+inline std::int64_t env_int(const char* name, std::int64_t dflt) {
+  const char* v = std::getenv(name);
+  if (v == nullptr || *v == 0) return dflt;
+  return std::strtoll(v, nullptr, 10);
+}
 
 class Error : public std::runtime_error {
  public:
@@ -55,6 +75,11 @@ inline void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
     throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
                     ")");
+}
+
+inline DeviceGuard::DeviceGuard(int dev) {
+  cudaGetDevice(&prev);
+  cuda_check(cudaSetDevice(dev), "cudaSetDevice");
 }
 
 // FNV-1a 64 (descriptor digests; checksums of gathered matrices in tests).

@@ -15,23 +15,6 @@ namespace dm {
 
 namespace {
 
-std::int64_t env_int(const char* name, std::int64_t dflt) {
-  const char* v = std::getenv(name);
-  if (v == nullptr || *v == 0) return dflt;
-  return std::strtoll(v, nullptr, 10);
-}
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    cuda_check(cudaSetDevice(dev), "cudaSetDevice");
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
 std::uint64_t table_digest(const std::map<MatrixId, MatrixDescriptor>& t) {
   Fnv1a h;
   for (const auto& [id, d] : t) hash_descriptor(h, d);
@@ -867,424 +850,6 @@ void Session::flush_trace(const char* op) {
     w.trace_t0 = nullptr;
   }
   if (f) std::fclose(f);
-}
-
-void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
-  struct Live {
-    std::vector<DeviceBuffer> bufs;
-    std::vector<cudaEvent_t> events;
-  };
-  std::vector<Live> live(P_);
-  const float alpha = static_cast<float>(g.alpha);
-  const float beta = static_cast<float>(g.beta);
-  const bool read_c0 = g.beta != 0.0;  // kernels.hpp:69-71: beta == 0 never reads C
-  const int cta_group = static_cast<int>(env_int("DM_CTA_GROUP", 0));
-  const std::int64_t flush_k = env_int("DM_FLUSH_K", 0);
-  const int gemm_mode = env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed;
-  const int group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
-  const int l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
-  const int lockstep_env = static_cast<int>(env_int("DM_LOCKSTEP", 32));
-  // Half16 operands compute at fp32 and round C once (AccumOf<Half>, kernels.hpp:29-35)
-  const bool half_in = table_.at(g.a).precision == Precision::Half16;
-  const std::size_t esz = byte_width(table_.at(g.a).precision);
-
-  for (auto& wp : workers_) {
-    if (!wp) continue;
-    Worker& w = *wp;
-    DeviceGuard guard(w.device);
-    WorkerPlan plan = plan_worker(g, w.id, pol);
-    if (async_) {
-      // pulls start once A and B are written everywhere; C is overwritten only
-      // after its previous writes and reads (e.g. an async gather) finished
-      bound_inflight(w);
-      wait_writes(w.side, g.a);
-      wait_writes(w.side, g.b);
-      device_barrier(w.side, 1);  // every rank, even one without C blocks
-      wait_all(w.stream, g.c);
-    }
-    if (plan.tasks.empty()) continue;
-    Live& lv = live[w.id];
-    const bool trace = tracing() && !async_;
-    if (trace) w.trace_t0 = trace_event(w.stream);
-    // Producer lockstep needs the GEMM's CTAs co-resident: off when another
-    // local worker shares this device (its GEMMs run concurrently).
-    int sharing = 0;
-    for (auto& o : workers_) sharing += (o && o->device == w.device) ? 1 : 0;
-    const int lockstep = sharing == 1 ? lockstep_env : 0;
-    unsigned* sync = nullptr;
-    std::size_t sync_bytes = 0;
-    float* ksplit_ws = nullptr;  // split-K partials, shared by this worker's launches (stream-ordered)
-    std::size_t ksplit_ws_bytes = 0;
-    const int np = static_cast<int>(plan.k0.size()) - 1;
-    std::int64_t kmax = 0;
-    for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
-    const std::int64_t kpitch = std::max<std::int64_t>(8, (kmax + 7) / 8 * 8);
-    const int nbuf = np > 1 ? 2 : 1;
-    // panel planes per range and buffer: fp32 hi, and either fp32 lo
-    // (tf32x3) or bf16 hi + bf16 lo packed in one buffer (mixed); 8 B/element
-    struct Planes {
-      float* hi;
-      float* lo;
-      void* hi16;
-      void* lo16;
-    };
-    auto alloc_planes = [&](const std::vector<Range>& rs, std::vector<std::array<Planes, 2>>& out) {
-      out.resize(rs.size());
-      for (std::size_t i = 0; i < rs.size(); ++i)
-        for (int b = 0; b < nbuf; ++b) {
-          const std::size_t elems = static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1) * kpitch);
-          lv.bufs.push_back(w.pool->acquire(elems * 4));
-          float* hi = lv.bufs.back().f32();
-          lv.bufs.push_back(w.pool->acquire(elems * 4));
-          char* second = static_cast<char*>(lv.bufs.back().data());
-          if (gemm_mode == kModeMixed)
-            out[i][b] = Planes{hi, nullptr, second, second + elems * 2};
-          else
-            out[i][b] = Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr};
-        }
-    };
-    std::vector<std::array<Planes, 2>> pa, pb;
-    alloc_planes(plan.ar, pa);
-    alloc_planes(plan.br, pb);
-    // operands of this worker's GEMMs were written by earlier commands on
-    // its own streams; order the split stream after the compute stream.
-    {
-      cudaEvent_t e;
-      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-      lv.events.push_back(e);
-      cuda_check(cudaEventRecord(e, w.stream), "event");
-      cuda_check(cudaStreamWaitEvent(w.side, e, 0), "wait");
-    }
-
-    // Panels with the fewest peer bytes first: the GEMM starts on local data
-    // while the first remote pulls are still in flight (K order does not
-    // matter mathematically; every panel accumulates into C).
-    std::vector<int> order(np);
-    for (int p = 0; p < np; ++p) order[p] = p;
-    if (np > 1) {
-      std::vector<std::uint64_t> remote_bytes(np, 0);
-      for (int p = 0; p < np; ++p)
-        for (const auto* ranges : {&plan.ar, &plan.br})
-          for (const Range& r : *ranges)
-            for (const Piece& pc : r.panels[p]) {
-              bool remote = false;
-              source_ptr(w, pc.matrix, pc.coord, pol, &remote);
-              if (remote) remote_bytes[p] += pc.bytes();
-            }
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int x, int y) { return remote_bytes[x] < remote_bytes[y]; });
-    }
-
-    // Pieces that live on another GPU cross NVLink on a copy engine into a
-    // local landing buffer (no SMs taken from the concurrently running GEMM);
-    // the split then reads local HBM.  Landing buffers are double-buffered so
-    // the copy of panel s+1 overlaps the split and GEMM of panel s.
-    // Copy engines for remote pieces only when panels pipeline: there the
-    // transfer must not take SMs from the concurrently running GEMM.  A
-    // single-panel command has nothing to overlap, and one split kernel that
-    // reads peer memory directly moves the bytes once instead of twice.
-    const bool use_ce = env_int("DM_PULL_CE", 1) != 0 && np > 1;
-    auto resolve = [&](const Piece& pc, bool* remote, bool* cross) {
-      const void* src = static_cast<const char*>(source_ptr(w, pc.matrix, pc.coord, pol, remote)) +
-                        pc.src_off * static_cast<std::int64_t>(esz);
-      *cross = false;
-      if (*remote && use_ce) {
-        const Worker* ow = local(table_.at(pc.matrix).layout.owner(pc.coord));
-        *cross = ow == nullptr || ow->device != w.device;
-      }
-      return src;
-    };
-    // landing rectangle of a piece: source rows (op-k rows when transposed)
-    auto land_width = [](const Piece& pc) { return pc.trans ? pc.rows : pc.kcols; };
-    auto land_height = [](const Piece& pc) { return pc.trans ? pc.kcols : pc.rows; };
-    auto land_pitch = [&](const Piece& pc) { return (land_width(pc) + 7) / 8 * 8; };
-    auto land_bytes = [&](const Piece& pc) {
-      return static_cast<std::size_t>((land_pitch(pc) * land_height(pc) * static_cast<std::int64_t>(esz) + 255) /
-                                      256 * 256);
-    };
-    std::size_t land_max = 0;
-    for (int p = 0; p < np; ++p) {
-      std::size_t tot = 0;
-      for (const auto* ranges : {&plan.ar, &plan.br})
-        for (const Range& r : *ranges)
-          for (const Piece& pc : r.panels[p]) {
-            bool remote, cross;
-            resolve(pc, &remote, &cross);
-            if (cross) tot += land_bytes(pc);
-          }
-      land_max = std::max(land_max, tot);
-    }
-    char* landing[2] = {nullptr, nullptr};
-    if (land_max > 0) {
-      for (int b = 0; b < nbuf; ++b) {
-        lv.bufs.push_back(w.pool->acquire(land_max));
-        landing[b] = static_cast<char*>(lv.bufs.back().data());
-      }
-      if (!w.pull_flag.data()) {
-        w.pull_flag = w.pool->acquire(256);
-        cuda_check(cudaMemset(w.pull_flag.data(), 0, 256), "cudaMemset(flag)");
-        w.pull_seq = 0;
-      }
-    }
-    unsigned* flag = static_cast<unsigned*>(w.pull_flag.data());
-    auto new_event = [&]() {
-      cudaEvent_t e;
-      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-      lv.events.push_back(e);
-      return e;
-    };
-    // Per panel step: landed (copies done), consumed (landing buffer read by
-    // the split), split (planes written), gemm (planes read).
-    std::vector<cudaEvent_t> landed_ev(np, nullptr), consumed_ev(np, nullptr), split_ev(np, nullptr),
-        gemm_ev(np, nullptr);
-    // The copy stream starts where the split stream is (after the operand
-    // waits / device barrier above).
-    if (land_max > 0) {
-      cudaEvent_t e = new_event();
-      cuda_check(cudaEventRecord(e, w.side), "event");
-      cuda_check(cudaStreamWaitEvent(w.pull, e, 0), "wait");
-    }
-    // DM_FUSE_SPLIT: 0 never, 1 when the carrying GEMM hides the split, 2 always
-    const std::int64_t fuse_mode = env_int("DM_FUSE_SPLIT", 1);
-    const bool fuse = fuse_mode != 0 && !half_in;
-
-    // One split item per piece: effective source (landing buffer for pieces
-    // that crossed a link), target planes, and whether it waits on the flag.
-    struct Item {
-      const void* src;
-      std::int64_t lds;
-      const Piece* pc;
-      const Planes* pl;
-      bool landed;
-    };
-    std::vector<std::vector<Item>> items(np);
-    std::vector<unsigned> seq(np, 0);
-    // Issue the copy-engine pulls of step s and build its split items.
-    auto prepare = [&](int s) {
-      const int p = order[s];
-      const int buf = s % nbuf;
-      std::size_t loff = 0;
-      std::uint64_t pulled = 0;
-      cudaEvent_t tp = nullptr;
-      bool any = false;
-      for (int side_ab = 0; side_ab < 2; ++side_ab) {
-        const std::vector<Range>& rs = side_ab == 0 ? plan.ar : plan.br;
-        const std::vector<std::array<Planes, 2>>& planes = side_ab == 0 ? pa : pb;
-        for (std::size_t i = 0; i < rs.size(); ++i)
-          for (const Piece& pc : rs[i].panels[p]) {
-            bool remote, cross;
-            const void* src = resolve(pc, &remote, &cross);
-            (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
-            if (!cross) {
-              items[s].push_back({src, pc.lds, &pc, &planes[i][buf], false});
-              continue;
-            }
-            if (!any) {
-              any = true;
-              // landing[buf] was last read by the split of step s - nbuf
-              if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.pull, consumed_ev[s - nbuf], 0), "wait");
-              if (trace) tp = trace_event(w.pull);
-            }
-            char* dst = landing[buf] + loff;
-            cuda_check(cudaMemcpy2DAsync(dst, land_pitch(pc) * esz, src, pc.lds * esz, land_width(pc) * esz,
-                                         land_height(pc), cudaMemcpyDefault, w.pull),
-                       "cudaMemcpy2DAsync(peer)");
-            items[s].push_back({dst, land_pitch(pc), &pc, &planes[i][buf], true});
-            loff += land_bytes(pc);
-            pulled += pc.bytes() / 4 * esz;
-          }
-      }
-      if (any) {
-        landed_ev[s] = new_event();
-        seq[s] = ++w.pull_seq;
-        cuda_check(stream_write_flag(w.pull, flag, seq[s]), "cuStreamWriteValue32");
-        cuda_check(cudaEventRecord(landed_ev[s], w.pull), "event");
-        if (trace) w.trace.push_back({"pull", p, pulled, 0.0, tp, trace_event(w.pull)});
-      }
-    };
-    auto plane_off = [&](const Item& it) { return it.pc->dst_row * kpitch + it.pc->dst_k; };
-    // Split step s with its own kernels on the split stream.
-    auto split_separate = [&](int s) {
-      const int p = order[s];
-      if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_ev[s - nbuf], 0), "wait");  // planes free
-      if (landed_ev[s]) cuda_check(cudaStreamWaitEvent(w.side, landed_ev[s], 0), "wait");
-      cudaEvent_t ta = trace ? trace_event(w.side) : nullptr;
-      std::uint64_t bytes = 0;
-      for (const Item& it : items[s]) {
-        const Piece& pc = *it.pc;
-        const Planes& pl = *it.pl;
-        const std::int64_t off = plane_off(it);
-        cuda_check(split_tf32(it.src, half_in ? 1 : 0, it.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
-                              pl.lo ? pl.lo + off : nullptr, kpitch,
-                              pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
-                              pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch, w.side),
-                   "split_tf32");
-        w.stats.split_launches += 1;
-        bytes += pc.bytes() / 4 * esz;
-      }
-      if (trace) w.trace.push_back({"split", p, bytes, 0.0, ta, trace_event(w.side)});
-      split_ev[s] = new_event();
-      cuda_check(cudaEventRecord(split_ev[s], w.side), "event");
-      consumed_ev[s] = split_ev[s];
-    };
-    // Split jobs of step s for the split warps of step s-1's GEMM launches.
-    // Fused only when the carrying GEMM is long enough to hide the split: two
-    // warps per SM split ~150 GB/s of input beside a ~300 TFLOP/s GEMM (a
-    // narrow lead panel cannot hide a full panel's split -- that one runs as
-    // its own full-machine kernels instead).
-    auto fused_jobs = [&](int s, SplitJobs* out) {
-      if (!fuse || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs)) return false;
-      double bytes_in = 0, flops = 0;
-      for (const Item& it : items[s]) bytes_in += static_cast<double>(it.pc->bytes());
-      for (const Task& t : plan.tasks) {
-        auto [mb, nb] = block_extent(table_.at(g.c).layout.grid, t.c);
-        flops += 2.0 * mb * nb * static_cast<double>(plan.k0[order[s - 1] + 1] - plan.k0[order[s - 1]]);
-      }
-      if (fuse_mode == 1 && bytes_in / 150e9 > flops / 300e12) return false;
-      out->n = 0;
-      std::int64_t t = 0;
-      for (const Item& it : items[s]) {
-        const Piece& pc = *it.pc;
-        const Planes& pl = *it.pl;
-        const std::int64_t off = plane_off(it);
-        SplitJob& j = out->job[out->n++];
-        j = SplitJob{};
-        j.src = static_cast<const float*>(it.src);
-        j.lds = it.lds;
-        j.trans = pc.trans;
-        j.rows = pc.rows;
-        j.kcols = pc.kcols;
-        j.hi = pl.hi + off;
-        j.lo = pl.lo ? pl.lo + off : nullptr;
-        j.hi16 = pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr;
-        j.lo16 = pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr;
-        j.ldo = j.ldo16 = kpitch;
-        j.flag = it.landed ? flag : nullptr;
-        j.flag_val = it.landed ? seq[s] : 0;
-        j.t0 = t;
-        if (!split_job_fusable(j)) return false;
-        t += split_job_tiles(j);
-      }
-      out->t_begin = 0;
-      out->t_end = t;
-      return true;
-    };
-
-    prepare(0);
-    split_separate(0);
-    for (int step = 0; step < np; ++step) {
-      const int p = order[step];
-      const int buf = step % nbuf;
-      SplitJobs jobs;
-      bool fused_next = false;
-      if (step + 1 < np) {
-        prepare(step + 1);
-        fused_next = fused_jobs(step + 1, &jobs);
-        if (!fused_next) split_separate(step + 1);
-      }
-      if (split_ev[step]) cuda_check(cudaStreamWaitEvent(w.stream, split_ev[step], 0), "wait");
-      const std::int64_t kw = plan.k0[p + 1] - plan.k0[p];
-      cudaEvent_t tg = trace ? trace_event(w.stream) : nullptr;
-      const double flops0 = w.stats.gemm_flops;
-      const std::int64_t ntask = static_cast<std::int64_t>(plan.tasks.size());
-      for (std::int64_t ti = 0; ti < ntask; ++ti) {
-        const Task& t = plan.tasks[ti];
-        StoredBlock& cb = w.owned.at({g.c, t.c});
-        Tf32x3Args a;
-        a.mode = gemm_mode;
-        const Planes& A = pa[t.ra][buf];
-        const Planes& B = pb[t.rb][buf];
-        a.a_hi = A.hi;
-        a.a_lo = A.lo;
-        a.a_hi16 = A.hi16;
-        a.a_lo16 = A.lo16;
-        a.lda = a.lda16 = kpitch;
-        a.b_hi = B.hi;
-        a.b_lo = B.lo;
-        a.b_hi16 = B.hi16;
-        a.b_lo16 = B.lo16;
-        a.ldb = a.ldb16 = kpitch;
-        a.c = cb.mem.f32();
-        a.c_half = half_in ? 1 : 0;
-        a.ldc = cb.cols;
-        a.m = cb.rows;
-        a.n = cb.cols;
-        a.k = kw;
-        a.alpha = alpha;
-        a.beta = step == 0 ? beta : 1.0f;
-        a.read_c = step == 0 ? (read_c0 ? 1 : 0) : 1;
-        a.cta_group = cta_group;
-        a.flush_k = flush_k;
-        a.group_m = group_m;
-        a.l2_policy = l2_policy;
-        a.lockstep = lockstep;
-        if (lockstep > 0) {
-          const std::size_t need = tf32x3_sync_bytes(a);
-          if (need > sync_bytes) {
-            lv.bufs.push_back(w.pool->acquire(need));
-            sync = static_cast<unsigned*>(lv.bufs.back().data());
-            sync_bytes = lv.bufs.back().capacity();
-          }
-          a.sync = sync;
-          a.sync_bytes = sync_bytes;
-        }
-        if (fused_next) {
-          // the next panel's split tiles, spread evenly over this step's launches
-          const std::int64_t total = jobs.job[jobs.n - 1].t0 + split_job_tiles(jobs.job[jobs.n - 1]);
-          jobs.t_begin = total * ti / ntask;
-          jobs.t_end = total * (ti + 1) / ntask;
-          a.split = &jobs;
-        }
-        if (const std::size_t need = tf32x3_splitk_bytes(a)) {
-          if (need > ksplit_ws_bytes) {
-            lv.bufs.push_back(w.pool->acquire(need));
-            ksplit_ws = lv.bufs.back().f32();
-            ksplit_ws_bytes = lv.bufs.back().capacity();
-          }
-          a.ws = ksplit_ws;
-          a.ws_bytes = ksplit_ws_bytes;
-        }
-        record_timing(w, true);
-        cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");
-        record_timing(w, false);
-        w.stats.gemm_launches += 1;
-        w.stats.gemm_flops += 2.0 * static_cast<double>(a.m) * a.n * a.k;
-      }
-      if (trace)
-        w.trace.push_back({fused_next ? "gemm+split" : "gemm", p, 0, w.stats.gemm_flops - flops0, tg,
-                           trace_event(w.stream)});
-      gemm_ev[step] = new_event();
-      cuda_check(cudaEventRecord(gemm_ev[step], w.stream), "event");
-      if (fused_next) {
-        split_ev[step + 1] = nullptr;  // written inside this step's GEMM launches
-        consumed_ev[step + 1] = gemm_ev[step];
-      }
-    }
-    if (async_) {
-      mark_write(w, w.stream, g.c);
-      // A and B are read by the split stream and by the GEMMs' fused split warps
-      for (cudaStream_t st : {w.side, w.stream}) {
-        mark_read(w, st, g.a);
-        mark_read(w, st, g.b);
-      }
-      // panel planes live until the last GEMM of this command has run
-      Worker::Inflight f;
-      cuda_check(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming), "event");
-      cuda_check(cudaEventRecord(f.done, w.stream), "event");
-      f.bufs = std::move(lv.bufs);
-      f.events = std::move(lv.events);
-      f.events.push_back(f.done);
-      w.inflight.push_back(std::move(f));
-    }
-  }
-  if (async_) return;
-  sync_local();
-  for (auto& wp : workers_) {
-    if (!wp) continue;
-    DeviceGuard guard(wp->device);
-    for (cudaEvent_t e : live[wp->id].events) cudaEventDestroy(e);
-    live[wp->id].bufs.clear();
-  }
 }
 
 void Session::cache_foreign_a(const GemmArgs& g) {

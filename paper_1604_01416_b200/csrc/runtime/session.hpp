@@ -223,6 +223,8 @@ class Session {
   const void* source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
                          bool* remote) const;
   void run_gemm(const GemmArgs& g, SourcePolicy pol);
+  struct GemmRun;  // one worker's K-panel pipeline of one GEMM command (session_gemm.cpp)
+  friend struct GemmRun;
   void cache_foreign_a(const GemmArgs& g);
   void record_timing(Worker& w, bool start);
   void collect_timing();

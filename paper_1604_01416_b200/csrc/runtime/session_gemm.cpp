@@ -1,0 +1,481 @@
+// One worker's K-panel pipeline of one distributed GEMM command -- the B200
+// form of GeneralGemmExec / CyclicGemmExec / CachedBackwardExec's
+// "assemble op(A) rows and op(B) columns, then local_gemm" (ops.hpp:214-330,
+// 336-383, 406-503): the same pieces, pulled panel by panel and overlapped
+// with the tcgen05 GEMM.
+//
+// Per panel step s (panels in `order`, the least-remote first):
+//   pull   (stream `pull`, copy engines): pieces on another GPU land in a
+//          double-buffered local buffer; a stream memory op then publishes
+//          the step's sequence number in the worker's flag word;
+//   split  (stream `side` for step 0 and whenever fusing does not pay; else
+//          the split warps of step s-1's GEMM launches): transpose/assemble
+//          into K-major planes, fp32 -> tf32 hi + bf16 hi/lo;
+//   GEMM   (stream `stream`): C += op(A)_s op(B)_s over double-buffered planes.
+// Buffer reuse is event-ordered: landing[s % 2] waits until step s-2's split
+// consumed it, planes[s % 2] until step s-2's GEMM read them.
+#include <algorithm>
+#include <array>
+
+#include "../kernels/tf32x3_gemm.h"
+#include "session.hpp"
+
+namespace dm {
+
+struct Session::GemmRun {
+  // panel planes of one range and buffer: fp32 hi, and either fp32 lo
+  // (tf32x3) or bf16 hi + bf16 lo packed in one buffer (mixed); 8 B/element
+  struct Planes {
+    float* hi;
+    float* lo;
+    void* hi16;
+    void* lo16;
+  };
+  // one split item per piece: effective source (the landing buffer for pieces
+  // that crossed a link), target planes, and whether it waits on the flag
+  struct Item {
+    const void* src;
+    std::int64_t lds;
+    const Piece* pc;
+    const Planes* pl;
+    bool landed;
+  };
+
+  Session& S;
+  Worker& w;
+  const GemmArgs& g;
+  const SourcePolicy pol;
+  const WorkerPlan plan;
+  std::vector<DeviceBuffer>& bufs;
+  std::vector<cudaEvent_t>& events;
+
+  // command-wide settings
+  const bool half_in;  // Half16 operands: fp32 compute, C rounded once (AccumOf<Half>, kernels.hpp:29-35)
+  const std::size_t esz;
+  const int gemm_mode;
+  const bool trace;
+  const int np;
+  const int nbuf;
+  std::int64_t kpitch = 8;
+  int lockstep = 0;
+  std::int64_t fuse_mode = 1;
+
+  std::vector<std::array<Planes, 2>> pa, pb;
+  std::vector<int> order;
+  bool use_ce = false;
+  char* landing[2] = {nullptr, nullptr};
+  unsigned* flag = nullptr;
+  std::vector<cudaEvent_t> landed_ev, consumed_ev, split_ev, gemm_ev;
+  std::vector<std::vector<Item>> items;
+  std::vector<unsigned> seq;
+  unsigned* sync = nullptr;  // lockstep counters
+  std::size_t sync_bytes = 0;
+  float* ksplit_ws = nullptr;  // split-K partials (stream-ordered reuse)
+  std::size_t ksplit_ws_bytes = 0;
+
+  GemmRun(Session& s, Worker& wk, const GemmArgs& ga, SourcePolicy p, WorkerPlan pl, std::vector<DeviceBuffer>& b,
+          std::vector<cudaEvent_t>& e)
+      : S(s), w(wk), g(ga), pol(p), plan(std::move(pl)), bufs(b), events(e),
+        half_in(s.table_.at(ga.a).precision == Precision::Half16),
+        esz(byte_width(s.table_.at(ga.a).precision)),
+        gemm_mode(env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed),
+        trace(s.tracing() && !s.async_),
+        np(static_cast<int>(plan.k0.size()) - 1),
+        nbuf(np > 1 ? 2 : 1) {}
+
+  cudaEvent_t new_event() {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    events.push_back(e);
+    return e;
+  }
+
+  // ------------------------------------------------------------ setup
+  void setup() {
+    std::int64_t kmax = 0;
+    for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
+    kpitch = std::max<std::int64_t>(8, (kmax + 7) / 8 * 8);
+    // Producer lockstep needs the GEMM's CTAs co-resident: off when another
+    // local worker shares this device (its GEMMs run concurrently).
+    int sharing = 0;
+    for (auto& o : S.workers_) sharing += (o && o->device == w.device) ? 1 : 0;
+    lockstep = sharing == 1 ? static_cast<int>(env_int("DM_LOCKSTEP", 32)) : 0;
+    // DM_FUSE_SPLIT: 0 never, 1 when the carrying GEMM hides the split, 2 always
+    fuse_mode = half_in ? 0 : env_int("DM_FUSE_SPLIT", 1);
+
+    alloc_planes(plan.ar, pa);
+    alloc_planes(plan.br, pb);
+    // operands of this worker's GEMMs were written by earlier commands on
+    // its own streams; order the split stream after the compute stream
+    cudaEvent_t e = new_event();
+    cuda_check(cudaEventRecord(e, w.stream), "event");
+    cuda_check(cudaStreamWaitEvent(w.side, e, 0), "wait");
+
+    order_panels();
+    setup_landing();
+    landed_ev.assign(np, nullptr);
+    consumed_ev.assign(np, nullptr);
+    split_ev.assign(np, nullptr);
+    gemm_ev.assign(np, nullptr);
+    items.assign(np, {});
+    seq.assign(np, 0);
+  }
+
+  void alloc_planes(const std::vector<Range>& rs, std::vector<std::array<Planes, 2>>& out) {
+    out.resize(rs.size());
+    for (std::size_t i = 0; i < rs.size(); ++i)
+      for (int b = 0; b < nbuf; ++b) {
+        const std::size_t elems = static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1) * kpitch);
+        bufs.push_back(w.pool->acquire(elems * 4));
+        float* hi = bufs.back().f32();
+        bufs.push_back(w.pool->acquire(elems * 4));
+        char* second = static_cast<char*>(bufs.back().data());
+        out[i][b] = gemm_mode == kModeMixed ? Planes{hi, nullptr, second, second + elems * 2}
+                                            : Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr};
+      }
+  }
+
+  template <class F>
+  void for_pieces(int p, F&& f) const {
+    for (const auto* ranges : {&plan.ar, &plan.br})
+      for (const Range& r : *ranges)
+        for (const Piece& pc : r.panels[p]) f(pc);
+  }
+
+  // Panels with the fewest peer bytes first: the GEMM starts on local data
+  // while the first remote pulls are in flight (K order does not matter
+  // mathematically; every panel accumulates into C).
+  void order_panels() {
+    order.resize(np);
+    for (int p = 0; p < np; ++p) order[p] = p;
+    if (np < 2) return;
+    std::vector<std::uint64_t> remote_bytes(np, 0);
+    for (int p = 0; p < np; ++p)
+      for_pieces(p, [&](const Piece& pc) {
+        bool remote = false;
+        S.source_ptr(w, pc.matrix, pc.coord, pol, &remote);
+        if (remote) remote_bytes[p] += pc.bytes();
+      });
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return remote_bytes[x] < remote_bytes[y]; });
+  }
+
+  // Copy engines carry remote pieces only when panels pipeline: there the
+  // transfer must not take SMs from the concurrently running GEMM.  A
+  // single-panel command has nothing to overlap, and one split kernel that
+  // reads peer memory directly moves the bytes once instead of twice.
+  const void* resolve(const Piece& pc, bool* remote, bool* cross) const {
+    const void* src = static_cast<const char*>(S.source_ptr(w, pc.matrix, pc.coord, pol, remote)) +
+                      pc.src_off * static_cast<std::int64_t>(esz);
+    *cross = false;
+    if (*remote && use_ce) {
+      const Worker* ow = S.local(S.table_.at(pc.matrix).layout.owner(pc.coord));
+      *cross = ow == nullptr || ow->device != w.device;
+    }
+    return src;
+  }
+  // landing rectangle of a piece: source rows (op-k rows when transposed)
+  static std::int64_t land_width(const Piece& pc) { return pc.trans ? pc.rows : pc.kcols; }
+  static std::int64_t land_height(const Piece& pc) { return pc.trans ? pc.kcols : pc.rows; }
+  static std::int64_t land_pitch(const Piece& pc) { return (land_width(pc) + 7) / 8 * 8; }
+  std::size_t land_bytes(const Piece& pc) const {
+    return static_cast<std::size_t>((land_pitch(pc) * land_height(pc) * static_cast<std::int64_t>(esz) + 255) /
+                                    256 * 256);
+  }
+
+  void setup_landing() {
+    use_ce = env_int("DM_PULL_CE", 1) != 0 && np > 1;
+    std::size_t land_max = 0;
+    for (int p = 0; p < np; ++p) {
+      std::size_t tot = 0;
+      for_pieces(p, [&](const Piece& pc) {
+        bool remote, cross;
+        resolve(pc, &remote, &cross);
+        if (cross) tot += land_bytes(pc);
+      });
+      land_max = std::max(land_max, tot);
+    }
+    if (land_max == 0) return;
+    for (int b = 0; b < nbuf; ++b) {
+      bufs.push_back(w.pool->acquire(land_max));
+      landing[b] = static_cast<char*>(bufs.back().data());
+    }
+    if (!w.pull_flag.data()) {
+      w.pull_flag = w.pool->acquire(256);
+      cuda_check(cudaMemset(w.pull_flag.data(), 0, 256), "cudaMemset(flag)");
+      w.pull_seq = 0;
+    }
+    flag = static_cast<unsigned*>(w.pull_flag.data());
+    // the copy stream starts where the split stream is (after the operand
+    // waits / device barrier of the command)
+    cudaEvent_t e = new_event();
+    cuda_check(cudaEventRecord(e, w.side), "event");
+    cuda_check(cudaStreamWaitEvent(w.pull, e, 0), "wait");
+  }
+
+  // ------------------------------------------------------------ per step
+  // Issue the copy-engine pulls of step s and build its split items.
+  void prepare(int s) {
+    const int p = order[s];
+    const int buf = s % nbuf;
+    std::size_t loff = 0;
+    std::uint64_t pulled = 0;
+    cudaEvent_t tp = nullptr;
+    bool any = false;
+    for (int ab = 0; ab < 2; ++ab) {
+      const std::vector<Range>& rs = ab == 0 ? plan.ar : plan.br;
+      const std::vector<std::array<Planes, 2>>& planes = ab == 0 ? pa : pb;
+      for (std::size_t i = 0; i < rs.size(); ++i)
+        for (const Piece& pc : rs[i].panels[p]) {
+          bool remote, cross;
+          const void* src = resolve(pc, &remote, &cross);
+          (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
+          if (!cross) {
+            items[s].push_back({src, pc.lds, &pc, &planes[i][buf], false});
+            continue;
+          }
+          if (!any) {
+            any = true;
+            // landing[buf] was last read by the split of step s - nbuf
+            if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.pull, consumed_ev[s - nbuf], 0), "wait");
+            if (trace) tp = S.trace_event(w.pull);
+          }
+          char* dst = landing[buf] + loff;
+          cuda_check(cudaMemcpy2DAsync(dst, land_pitch(pc) * esz, src, pc.lds * esz, land_width(pc) * esz,
+                                       land_height(pc), cudaMemcpyDefault, w.pull),
+                     "cudaMemcpy2DAsync(peer)");
+          items[s].push_back({dst, land_pitch(pc), &pc, &planes[i][buf], true});
+          loff += land_bytes(pc);
+          pulled += pc.bytes() / 4 * esz;
+        }
+    }
+    if (!any) return;
+    landed_ev[s] = new_event();
+    seq[s] = ++w.pull_seq;
+    cuda_check(stream_write_flag(w.pull, flag, seq[s]), "cuStreamWriteValue32");
+    cuda_check(cudaEventRecord(landed_ev[s], w.pull), "event");
+    if (trace) w.trace.push_back({"pull", p, pulled, 0.0, tp, S.trace_event(w.pull)});
+  }
+
+  std::int64_t plane_off(const Item& it) const { return it.pc->dst_row * kpitch + it.pc->dst_k; }
+
+  // Split step s with its own kernels on the split stream.
+  void split_separate(int s) {
+    if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_ev[s - nbuf], 0), "wait");  // planes free
+    if (landed_ev[s]) cuda_check(cudaStreamWaitEvent(w.side, landed_ev[s], 0), "wait");
+    cudaEvent_t ta = trace ? S.trace_event(w.side) : nullptr;
+    std::uint64_t bytes = 0;
+    for (const Item& it : items[s]) {
+      const Piece& pc = *it.pc;
+      const Planes& pl = *it.pl;
+      const std::int64_t off = plane_off(it);
+      cuda_check(split_tf32(it.src, half_in ? 1 : 0, it.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
+                            pl.lo ? pl.lo + off : nullptr, kpitch,
+                            pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
+                            pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch, w.side),
+                 "split_tf32");
+      w.stats.split_launches += 1;
+      bytes += pc.bytes() / 4 * esz;
+    }
+    if (trace) w.trace.push_back({"split", order[s], bytes, 0.0, ta, S.trace_event(w.side)});
+    split_ev[s] = new_event();
+    cuda_check(cudaEventRecord(split_ev[s], w.side), "event");
+    consumed_ev[s] = split_ev[s];
+  }
+
+  // Split jobs of step s for the split warps of step s-1's GEMM launches.
+  // Fused only when the carrying GEMM is long enough to hide the split: two
+  // warps per SM split ~150 GB/s of input beside a ~300 TFLOP/s GEMM (a
+  // narrow panel cannot hide a full panel's split -- that one runs as its own
+  // full-machine kernels instead).
+  bool fused_jobs(int s, SplitJobs* out) const {
+    if (fuse_mode == 0 || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs)) return false;
+    double bytes_in = 0, flops = 0;
+    for (const Item& it : items[s]) bytes_in += static_cast<double>(it.pc->bytes());
+    const std::int64_t kw = plan.k0[order[s - 1] + 1] - plan.k0[order[s - 1]];
+    for (const Task& t : plan.tasks) {
+      auto [mb, nb] = block_extent(S.table_.at(g.c).layout.grid, t.c);
+      flops += 2.0 * mb * nb * static_cast<double>(kw);
+    }
+    if (fuse_mode == 1 && bytes_in / 150e9 > flops / 300e12) return false;
+    out->n = 0;
+    std::int64_t t = 0;
+    for (const Item& it : items[s]) {
+      const Piece& pc = *it.pc;
+      const Planes& pl = *it.pl;
+      const std::int64_t off = plane_off(it);
+      SplitJob& j = out->job[out->n++];
+      j = SplitJob{};
+      j.src = static_cast<const float*>(it.src);
+      j.lds = it.lds;
+      j.trans = pc.trans;
+      j.rows = pc.rows;
+      j.kcols = pc.kcols;
+      j.hi = pl.hi + off;
+      j.lo = pl.lo ? pl.lo + off : nullptr;
+      j.hi16 = pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr;
+      j.lo16 = pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr;
+      j.ldo = j.ldo16 = kpitch;
+      j.flag = it.landed ? flag : nullptr;
+      j.flag_val = it.landed ? seq[s] : 0;
+      j.t0 = t;
+      if (!split_job_fusable(j)) return false;
+      t += split_job_tiles(j);
+    }
+    out->t_begin = 0;
+    out->t_end = t;
+    return true;
+  }
+
+  // The GEMM launches of step `step` (one per owned C block), carrying the
+  // next panel's split tiles when `jobs` is set.
+  void gemm_step(int step, SplitJobs* jobs) {
+    const int p = order[step];
+    const int buf = step % nbuf;
+    if (split_ev[step]) cuda_check(cudaStreamWaitEvent(w.stream, split_ev[step], 0), "wait");
+    const std::int64_t kw = plan.k0[p + 1] - plan.k0[p];
+    cudaEvent_t tg = trace ? S.trace_event(w.stream) : nullptr;
+    const double flops0 = w.stats.gemm_flops;
+    const std::int64_t ntask = static_cast<std::int64_t>(plan.tasks.size());
+    const std::int64_t split_tiles =
+        jobs ? jobs->job[jobs->n - 1].t0 + split_job_tiles(jobs->job[jobs->n - 1]) : 0;
+    for (std::int64_t ti = 0; ti < ntask; ++ti) {
+      const Task& t = plan.tasks[ti];
+      StoredBlock& cb = w.owned.at({g.c, t.c});
+      const Planes& A = pa[t.ra][buf];
+      const Planes& B = pb[t.rb][buf];
+      Tf32x3Args a;
+      a.mode = gemm_mode;
+      a.a_hi = A.hi;
+      a.a_lo = A.lo;
+      a.a_hi16 = A.hi16;
+      a.a_lo16 = A.lo16;
+      a.lda = a.lda16 = kpitch;
+      a.b_hi = B.hi;
+      a.b_lo = B.lo;
+      a.b_hi16 = B.hi16;
+      a.b_lo16 = B.lo16;
+      a.ldb = a.ldb16 = kpitch;
+      a.c = cb.mem.f32();
+      a.c_half = half_in ? 1 : 0;
+      a.ldc = cb.cols;
+      a.m = cb.rows;
+      a.n = cb.cols;
+      a.k = kw;
+      a.alpha = static_cast<float>(g.alpha);
+      // the first panel applies beta (beta == 0 never reads C, kernels.hpp:69-71);
+      // later panels accumulate into what it wrote
+      a.beta = step == 0 ? static_cast<float>(g.beta) : 1.0f;
+      a.read_c = step == 0 ? (g.beta != 0.0 ? 1 : 0) : 1;
+      a.cta_group = static_cast<int>(env_int("DM_CTA_GROUP", 0));
+      a.flush_k = env_int("DM_FLUSH_K", 0);
+      a.group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
+      a.l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
+      a.lockstep = lockstep;
+      if (lockstep > 0) {
+        const std::size_t need = tf32x3_sync_bytes(a);
+        if (need > sync_bytes) {
+          bufs.push_back(w.pool->acquire(need));
+          sync = static_cast<unsigned*>(bufs.back().data());
+          sync_bytes = bufs.back().capacity();
+        }
+        a.sync = sync;
+        a.sync_bytes = sync_bytes;
+      }
+      if (jobs) {
+        // the next panel's split tiles, spread evenly over this step's launches
+        jobs->t_begin = split_tiles * ti / ntask;
+        jobs->t_end = split_tiles * (ti + 1) / ntask;
+        a.split = jobs;
+      }
+      if (const std::size_t need = tf32x3_splitk_bytes(a)) {
+        if (need > ksplit_ws_bytes) {
+          bufs.push_back(w.pool->acquire(need));
+          ksplit_ws = bufs.back().f32();
+          ksplit_ws_bytes = bufs.back().capacity();
+        }
+        a.ws = ksplit_ws;
+        a.ws_bytes = ksplit_ws_bytes;
+      }
+      S.record_timing(w, true);
+      cuda_check(tf32x3_gemm(a, w.stream), "tf32x3_gemm");
+      S.record_timing(w, false);
+      w.stats.gemm_launches += 1;
+      w.stats.gemm_flops += 2.0 * static_cast<double>(a.m) * a.n * a.k;
+    }
+    if (trace)
+      w.trace.push_back({jobs ? "gemm+split" : "gemm", p, 0, w.stats.gemm_flops - flops0, tg,
+                         S.trace_event(w.stream)});
+    gemm_ev[step] = new_event();
+    cuda_check(cudaEventRecord(gemm_ev[step], w.stream), "event");
+  }
+
+  void run() {
+    setup();
+    prepare(0);
+    split_separate(0);
+    for (int step = 0; step < np; ++step) {
+      SplitJobs jobs;
+      bool fused_next = false;
+      if (step + 1 < np) {
+        prepare(step + 1);
+        fused_next = fused_jobs(step + 1, &jobs);
+        if (!fused_next) split_separate(step + 1);
+      }
+      gemm_step(step, fused_next ? &jobs : nullptr);
+      if (fused_next) consumed_ev[step + 1] = gemm_ev[step];  // split inside this step's launches
+    }
+  }
+};
+
+void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
+  struct Live {
+    std::vector<DeviceBuffer> bufs;
+    std::vector<cudaEvent_t> events;
+  };
+  std::vector<Live> live(P_);
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    Worker& w = *wp;
+    DeviceGuard guard(w.device);
+    WorkerPlan plan = plan_worker(g, w.id, pol);
+    if (async_) {
+      // pulls start once A and B are written everywhere; C is overwritten only
+      // after its previous writes and reads (e.g. an async gather) finished
+      bound_inflight(w);
+      wait_writes(w.side, g.a);
+      wait_writes(w.side, g.b);
+      device_barrier(w.side, 1);  // every rank, even one without C blocks
+      wait_all(w.stream, g.c);
+    }
+    if (plan.tasks.empty()) continue;
+    Live& lv = live[w.id];
+    if (tracing() && !async_) w.trace_t0 = trace_event(w.stream);
+    GemmRun(*this, w, g, pol, std::move(plan), lv.bufs, lv.events).run();
+    if (async_) {
+      mark_write(w, w.stream, g.c);
+      // A and B are read by the split stream and by the GEMMs' fused split warps
+      for (cudaStream_t st : {w.side, w.stream}) {
+        mark_read(w, st, g.a);
+        mark_read(w, st, g.b);
+      }
+      // panel planes live until the last GEMM of this command has run
+      Worker::Inflight f;
+      cuda_check(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming), "event");
+      cuda_check(cudaEventRecord(f.done, w.stream), "event");
+      f.bufs = std::move(lv.bufs);
+      f.events = std::move(lv.events);
+      f.events.push_back(f.done);
+      w.inflight.push_back(std::move(f));
+    }
+  }
+  if (async_) return;
+  sync_local();
+  for (auto& wp : workers_) {
+    if (!wp) continue;
+    DeviceGuard guard(wp->device);
+    for (cudaEvent_t e : live[wp->id].events) cudaEventDestroy(e);
+    live[wp->id].bufs.clear();
+  }
+}
+
+}  // namespace dm
