@@ -134,6 +134,31 @@ def test_half_gemm(cuda, i):
     assert ulp.max() <= 1 and (ulp == 0).mean() > 0.9
 
 
+@pytest.mark.parametrize("P", [1, 2])
+def test_half_gemm_long_k(cuda, P):
+    """Half16 GEMM with few C tiles and a long K: split-K work items whose fp32
+    partials are summed in fixed order and rounded to half once (AccumOf<Half>,
+    kernels.hpp:29-35) -- within one half ulp of the reference."""
+    from oracle import RefOracle, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not shipped")
+    m, n, k = 128, 96, 4096
+    with session(P, 77) as s:
+        a = s.create_matrix(make_layout(0, m, k, m // P, k, P), Precision.Half16, FillKind.SeededRandom)
+        b = s.create_matrix(make_layout(1, k, n, k, n // P, P), Precision.Half16, FillKind.SeededRandom)
+        cm = s.create_matrix(make_layout(0, m, n, m // P, n, P), Precision.Half16, FillKind.SeededRandom)
+        s.general_gemm(1.5, a, b, -0.5, cm, False, False)
+        got = s.gather(cm)
+    with RefOracle().session(P, 77) as rs:
+        ra = rs.create_p(0, m, k, m // P, k, P, 0)
+        rb = rs.create_p(1, k, n, k, n // P, P, 0)
+        rc = rs.create_p(0, m, n, m // P, n, P, 0)
+        rs.general_gemm(1.5, ra, rb, -0.5, rc, False, False)
+        want = rs.gather_p(rc)
+    ulp = np.abs(got.view(np.int16).astype(np.int32) - want.view(np.int16).astype(np.int32))
+    assert ulp.max() <= 1 and (ulp == 0).mean() > 0.8
+
+
 def test_double_gemm_unsupported(cuda):
     with session(1, 1) as s:
         lay = make_layout(0, 8, 8, 8, 8, 1)
