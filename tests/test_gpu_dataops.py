@@ -153,10 +153,17 @@ def test_half_gemm_long_k(cuda, P):
         ra = rs.create_p(0, m, k, m // P, k, P, 0)
         rb = rs.create_p(1, k, n, k, n // P, P, 0)
         rc = rs.create_p(0, m, n, m // P, n, P, 0)
+        A, B, C0 = rs.gather_p(ra), rs.gather_p(rb), rs.gather_p(rc)
         rs.general_gemm(1.5, ra, rb, -0.5, rc, False, False)
         want = rs.gather_p(rc)
-    ulp = np.abs(got.view(np.int16).astype(np.int32) - want.view(np.int16).astype(np.int32))
-    assert ulp.max() <= 1 and (ulp == 0).mean() > 0.8
+    exact = 1.5 * (A.astype(np.float64) @ B.astype(np.float64)) - 0.5 * C0.astype(np.float64)
+
+    def rel(x):
+        return np.linalg.norm(x.astype(np.float64) - exact) / np.linalg.norm(exact)
+    # near-zero outputs differ by many half ulps between any two fp32 summation
+    # orders over K=4096; the bar is "no less accurate than the reference"
+    assert rel(got) <= 1.5 * rel(want) + 1e-6
+    assert (got.view(np.int16) == want.view(np.int16)).mean() > 0.8
 
 
 def test_double_gemm_unsupported(cuda):
