@@ -36,7 +36,7 @@ enum dm_status {
   DM_ERR_CACHE_MISS = 8,  /* CacheMissError  common.hpp:72-78 */
   DM_ERR_CUDA = 9,        /* device runtime failure (no reference equivalent) */
   DM_ERR_NCCL = 10,       /* NCCL failure (no reference equivalent) */
-  DM_ERR_UNSUPPORTED = 11 /* outside the fp32 hot path (Half16/Double64 storage) */
+  DM_ERR_UNSUPPORTED = 11 /* reserved: an operation this build does not provide */
 };
 
 /* ---- enums mirroring the reference ---- */

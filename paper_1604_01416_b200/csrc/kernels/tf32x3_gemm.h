@@ -104,6 +104,16 @@ cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, in
                        int64_t kcols, float* hi, float* lo, int64_t ldo, void* hi16, void* lo16,
                        int64_t ldo16, cudaStream_t stream);
 
+// Double64 GEMM bit-exact with the reference's gemm_typed<double> (gemm_f64.cu):
+// C[i][j] <- alpha * sum_k A[i][k] B[j][k] (+ beta C[i][j] when read_c), A and B
+// K-major, k ascending, unfused multiply and add.
+cudaError_t gemm_f64_exact(const double* a, int64_t lda, const double* b, int64_t ldb, double* c, int64_t ldc,
+                           int64_t m, int64_t n, int64_t k, double alpha, double beta, int read_c,
+                           cudaStream_t stream);
+// fp64 panel assembly: dst[r][k] = trans ? src[k*lds + r] : src[r*lds + k].
+cudaError_t assemble_f64(const double* src, int64_t lds, int trans, int64_t rows, int64_t kcols, double* dst,
+                         int64_t ldo, cudaStream_t stream);
+
 // Stream-ordered 32-bit store without an SM (a stream memory operation):
 // *addr = value once the stream's earlier work (e.g. copy-engine transfers)
 // completed; pairs with SplitJob::flag.

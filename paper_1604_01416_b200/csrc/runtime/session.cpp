@@ -562,8 +562,6 @@ void Session::validate_general(const GemmArgs& g) const {
   if (da.precision != db.precision || da.precision != dc.precision)
     throw UsageError("gemm: operands must share a precision; reshape to convert first");
   if (dc.replicated) throw UsageError("gemm: destination matrix may not be replicated");
-  if (da.precision == Precision::Double64)
-    throw UnsupportedError("gemm: Double64 is outside the fp32 tensor-core path (reshape to Single32)");
   const std::int64_t kk = g.trans_a ? da.layout.grid.global_rows : da.layout.grid.global_cols;
   const std::int64_t m = g.trans_a ? da.layout.grid.global_cols : da.layout.grid.global_rows;
   const std::int64_t kb = g.trans_b ? db.layout.grid.global_cols : db.layout.grid.global_rows;
@@ -721,7 +719,7 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
   }
   const std::int64_t target = env_int("DM_PANEL_K", 8192);
   const std::int64_t local_lead = env_int("DM_PANEL_LOCAL", 0);
-  if (!plan.has_remote && local_lead > 0 && K >= 4 * local_lead) {
+  if (!plan.has_remote && local_lead > 0 && K >= 4 * local_lead && da.precision != Precision::Double64) {
     // All operands local: geometric panels.  Only the narrow lead panel's
     // split is exposed; every later panel is split by the previous panel's
     // GEMM (a GEMM of width w hides the split of ~3.7 w, tf32x3_gemm.cu).
@@ -747,7 +745,10 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     work += 2.0 * mb * nb * static_cast<double>(K);
   }
   const double min_work = static_cast<double>(env_int("DM_PIPELINE_MIN_GFLOP", 200)) * 1e9;
-  if (plan.has_remote && K > 2 * 256 && target > 0 && work >= min_work) {
+  // Double64 runs the bit-exact SIMT kernel over one panel: the reference's
+  // single k-ascending accumulation per output cannot be cut into panels.
+  const bool f64 = da.precision == Precision::Double64;
+  if (plan.has_remote && K > 2 * 256 && target > 0 && work >= min_work && !f64) {
     std::int64_t np = std::max<std::int64_t>(2, (K + target - 1) / target);
     np = std::min<std::int64_t>(np, K / 256);
     std::int64_t width = (K + np - 1) / np;

@@ -409,7 +409,54 @@ struct Session::GemmRun {
     cuda_check(cudaEventRecord(gemm_ev[step], w.stream), "event");
   }
 
+  // Double64: assemble op(A) rows / op(B) columns over the whole K, then the
+  // bit-exact fp64 kernel (no split, no panels; gemm_f64.cu).
+  void run_f64() {
+    const std::int64_t K = plan.k0.back();
+    const std::int64_t kp = std::max<std::int64_t>(1, K);
+    auto assemble = [&](const std::vector<Range>& rs, std::vector<double*>& out) {
+      for (const Range& r : rs) {
+        bufs.push_back(w.pool->acquire(static_cast<std::size_t>(std::max<std::int64_t>(r.len, 1) * kp) * 8));
+        double* panel = static_cast<double*>(bufs.back().data());
+        out.push_back(panel);
+        for (const Piece& pc : r.panels[0]) {
+          bool remote = false;
+          const double* src =
+              static_cast<const double*>(S.source_ptr(w, pc.matrix, pc.coord, pol, &remote)) + pc.src_off;
+          cuda_check(assemble_f64(src, pc.lds, pc.trans, pc.rows, pc.kcols, panel + pc.dst_row * kp + pc.dst_k, kp,
+                                  w.side),
+                     "assemble_f64");
+          w.stats.split_launches += 1;
+          (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() * 2;
+        }
+      }
+    };
+    cudaEvent_t e = new_event();
+    cuda_check(cudaEventRecord(e, w.stream), "event");
+    cuda_check(cudaStreamWaitEvent(w.side, e, 0), "wait");
+    std::vector<double*> pa64, pb64;
+    if (K > 0) {
+      assemble(plan.ar, pa64);
+      assemble(plan.br, pb64);
+    }
+    cudaEvent_t done = new_event();
+    cuda_check(cudaEventRecord(done, w.side), "event");
+    cuda_check(cudaStreamWaitEvent(w.stream, done, 0), "wait");
+    for (const Task& t : plan.tasks) {
+      StoredBlock& cb = w.owned.at({g.c, t.c});
+      S.record_timing(w, true);
+      cuda_check(gemm_f64_exact(K > 0 ? pa64[t.ra] : nullptr, kp, K > 0 ? pb64[t.rb] : nullptr, kp,
+                                static_cast<double*>(cb.mem.data()), cb.cols, cb.rows, cb.cols, K, g.alpha, g.beta,
+                                g.beta != 0.0 ? 1 : 0, w.stream),
+                 "gemm_f64_exact");
+      S.record_timing(w, false);
+      w.stats.gemm_launches += 1;
+      w.stats.gemm_flops += 2.0 * static_cast<double>(cb.rows) * cb.cols * K;
+    }
+  }
+
   void run() {
+    if (S.table_.at(g.a).precision == Precision::Double64) return run_f64();
     setup();
     prepare(0);
     split_separate(0);

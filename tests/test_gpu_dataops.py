@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 from paper_1604_01416_b200 import (Config, FillKind, IntegrityError, Precision, Session,
-                                   UnsupportedError, make_layout)
+                                   make_layout)
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -166,12 +166,52 @@ def test_half_gemm_long_k(cuda, P):
     assert (got.view(np.int16) == want.view(np.int16)).mean() > 0.8
 
 
-def test_double_gemm_unsupported(cuda):
-    with session(1, 1) as s:
-        lay = make_layout(0, 8, 8, 8, 8, 1)
-        a, b, c = (s.create_matrix(lay, Precision.Double64, FillKind.SeededRandom) for _ in range(3))
-        with pytest.raises(UnsupportedError):
-            s.general_gemm(1.0, a, b, 0.0, c)
+@pytest.mark.parametrize("P", [1, 3])
+@pytest.mark.parametrize("trans", [0, 1, 2, 3])
+def test_double_gemm_bitexact(cuda, P, trans):
+    """Double64 GEMMs reproduce the reference bit for bit: same k-ascending,
+    unfused accumulation per output (kernels.hpp:48-75; the reference's fp64
+    bar, tests/acceptance.cpp:61-65, tests/test_dist_ops.cpp:63-70)."""
+    from oracle import RefOracle, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not shipped")
+    ta, tb = bool(trans & 1), bool(trans & 2)
+    la, lb, lc = (3, 72, 72, 24, 20), (0, 72, 72, 17, 72), (2, 72, 72, 9, 72)
+    for alpha, beta in ((1.0, 0.0), (1.5, -0.5)):
+        with session(P, 31 + trans) as s:
+            a = s.create_matrix(make_layout(*la, P), Precision.Double64, FillKind.SeededRandom)
+            b = s.create_matrix(make_layout(*lb, P), Precision.Double64, FillKind.SeededRandom)
+            c = s.create_matrix(make_layout(*lc, P), Precision.Double64, FillKind.SeededRandom)
+            s.general_gemm(alpha, a, b, beta, c, ta, tb)
+            got = s.gather(c)
+        with RefOracle().session(P, 31 + trans) as rs:
+            ra, rb, rc = (rs.create_p(*l, P, 2) for l in (la, lb, lc))
+            rs.general_gemm(alpha, ra, rb, beta, rc, ta, tb)
+            want = rs.gather_p(rc)
+        assert got.tobytes() == want.tobytes(), (alpha, beta)
+
+
+def test_double_cyclic_and_cached_backward_bitexact(cuda):
+    from oracle import RefOracle, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not shipped")
+    P, fin, fout, batch = 3, 48, 40, 24
+    lw, lx, ly, ldy, ldx = ((0, fin, fout, fin // P, fout), (1, fin, batch, fin, batch // P),
+                            (1, fout, batch, fout, batch // P), (1, fout, batch, fout, batch // P),
+                            (1, fin, batch, fin, batch // P))
+    with session(P, 8) as s:
+        W, X, Y, dY, dX = (s.create_matrix(make_layout(*l, P), Precision.Double64, FillKind.SeededRandom)
+                           for l in (lw, lx, ly, ldy, ldx))
+        s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+        s.cached_backward_gemm(W, dY, dX)
+        got_y, got_dx = s.gather(Y), s.gather(dX)
+    with RefOracle().session(P, 8) as rs:
+        rW, rX, rY, rdY, rdX = (rs.create_p(*l, P, 2) for l in (lw, lx, ly, ldy, ldx))
+        rs.cyclic_gemm(1.0, rW, rX, 0.0, rY, True, False, True)
+        rs.cached_backward_gemm(rW, rdY, rdX)
+        want_y, want_dx = rs.gather_p(rY), rs.gather_p(rdX)
+    assert got_y.tobytes() == want_y.tobytes()
+    assert got_dx.tobytes() == want_dx.tobytes()
 
 
 def test_restore_reference_checkpoint(cuda, tmp_path):
