@@ -34,9 +34,9 @@ def _pipeline_on(monkeypatch):
     monkeypatch.setenv("DM_PIPELINE_MIN_GFLOP", "0")
 
 
-def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77):
+def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77, devices=None):
     ta, tb = bool(trans & 1), bool(trans & 2)
-    with Session(Config(worker_count=P, root_seed=seed + trans, devices=[0] * P)) as s:
+    with Session(Config(worker_count=P, root_seed=seed + trans, devices=devices or [0] * P)) as s:
         lay = make_layout(LayoutKind.Checkerboard2D, n, n, blk[0], blk[1], P)
         a, b, c = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(3))
         A, B, C0 = s.gather(a), s.gather(b), s.gather(c)
@@ -95,3 +95,19 @@ def test_beta_zero_ignores_garbage_c_across_panels(cuda, monkeypatch):
         got = s.gather(c)
         assert np.isfinite(got).all()
         assert relfro(got, A.astype(np.float64) @ B.astype(np.float64)) <= TOL
+
+
+@pytest.mark.parametrize("trans", [0, 3])
+def test_local_mode_across_gpus(cuda, monkeypatch, trans):
+    """One process driving workers on different GPUs: remote pieces cross NVLink
+    on copy engines into landing buffers, the split warps wait on the flag."""
+    import torch
+    ndev = torch.cuda.device_count()
+    if ndev < 2:
+        pytest.skip("needs >= 2 GPUs")
+    P = 4
+    monkeypatch.setenv("DM_PANEL_K", "512")
+    for fuse in ("2", "0"):
+        monkeypatch.setenv("DM_FUSE_SPLIT", fuse)
+        err, _ = run_case(P, 1536, (768, 768), trans, devices=[w % ndev for w in range(P)])
+        assert err <= TOL, fuse
