@@ -288,7 +288,8 @@ struct Session::GemmRun {
   // narrow panel cannot hide a full panel's split -- that one runs as its own
   // full-machine kernels instead).
   bool fused_jobs(int s, SplitJobs* out) const {
-    if (fuse_mode == 0 || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs)) return false;
+    if (fuse_mode == 0 || items[s].empty() || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs))
+      return false;
     double bytes_in = 0, flops = 0;
     for (const Item& it : items[s]) bytes_in += static_cast<double>(it.pc->bytes());
     const std::int64_t kw = plan.k0[order[s - 1] + 1] - plan.k0[order[s - 1]];
