@@ -100,12 +100,27 @@ def cfg4(args, ndev):
             bwd_ms, _ = timed(s, lambda: s.cached_backward_gemm(W, dY, dX), 20)
             bwd_peer = sum(s.worker_stats(w).peer_bytes_read for w in range(P))
             dw_ms, _ = timed(s, lambda: s.general_gemm(1.0, X, dY, 0.0, dW, False, True), 20)
+            # W-stationary forward: W split by output features,
+            # X replicated (one all-gather per batch), Y row-blocked: 0 W bytes move
+            Wc = s.create_matrix(dm.make_layout(1, fin, fout, fin, fout // P, P), fill=dm.FillKind.SeededRandom)
+            Xr = s.create_matrix(dm.make_layout(1, fin, batch, fin, strip, P), fill=dm.FillKind.SeededRandom)
+            Yr = s.create_matrix(dm.make_layout(0, fout, batch, fout // P, batch, P))
+            s.barrier()
+            s.marker_record(0, 4)
+            s.replicate(Xr, True)  # the per-batch all-gather of X
+            s.marker_record(0, 5)
+            rep_ms = s.marker_elapsed(0, 4, 5)
+            s.reset_worker_stats()
+            ws_ms, _ = timed(s, lambda: s.general_gemm(1.0, Wc, Xr, 0.0, Yr, True, False), 20)
+            ws_peer = sum(s.worker_stats(w).peer_bytes_read for w in range(P))
             fl = 2.0 * fin * fout * batch
             fl_pull = fl = 2.0 * fin * fout * batch
             out = {"config": 4, "workload": f"FC {fin}->{fout}, batch {batch}, P={P}", "devices": devs,
                    "fwd_TN_pull_ms": round(fwd_pull_ms, 4), "fwd_pull_peer_bytes_per_call": int(pulled),
                    "fwd_TN_cached_ms": round(fwd_ms, 4), "fwd_cached_peer_bytes": int(fwd_cached_peer), "bwd_NN_cached_ms": round(bwd_ms, 4),
                    "bwd_peer_bytes": int(bwd_peer), "dW_NT_ms": round(dw_ms, 4),
+                   "fwd_wstationary_ms": round(ws_ms, 4), "fwd_wstationary_peer_bytes": int(ws_peer),
+                   "replicate_X_ms": round(rep_ms, 4),
                    "fwd_pull_tflops": fl_pull / fwd_pull_ms / 1e9, "fwd_tflops": fl / fwd_ms / 1e9, "bwd_tflops": fl / bwd_ms / 1e9, "dW_tflops": fl / dw_ms / 1e9}
             if args.ref:
                 from oracle import RefOracle
