@@ -658,7 +658,9 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
 
   EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
                a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws};
-  if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1) {
+  // lockstep keeps the CTAs of a wave together; with a single wave there is
+  // nothing to align (and no counters to clear)
+  if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1 && tiles > units) {
     const size_t need = tf32x3_sync_bytes(a);
     if (a.sync_bytes < need) return cudaErrorInvalidValue;
     ep.lockstep = a.lockstep;

@@ -517,10 +517,14 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     }
   }
   if (async_) return;
-  sync_local();
+  // Every split / pull of a command feeds the worker's GEMM stream (stream
+  // waits, or the landing flag the GEMM's split warps spin on), so that
+  // stream draining means the command's buffers are free; end_command()
+  // synchronises the remaining streams.
   for (auto& wp : workers_) {
     if (!wp) continue;
     DeviceGuard guard(wp->device);
+    cuda_check(cudaStreamSynchronize(wp->stream), "gemm stream sync");
     for (cudaEvent_t e : live[wp->id].events) cudaEventDestroy(e);
     live[wp->id].bufs.clear();
   }
