@@ -749,29 +749,50 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
   // single k-ascending accumulation per output cannot be cut into panels.
   const bool f64 = da.precision == Precision::Double64;
   if (plan.has_remote && K > 2 * 256 && target > 0 && work >= min_work && !f64) {
-    std::int64_t np = std::max<std::int64_t>(2, (K + target - 1) / target);
-    np = std::min<std::int64_t>(np, K / 256);
-    std::int64_t width = (K + np - 1) / np;
-    width = (width + 31) / 32 * 32;
-    plan.k0.clear();
-    for (std::int64_t k = 0; k < K; k += width) plan.k0.push_back(k);
-    plan.k0.push_back(K);
-    for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
-    for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
-    // If even the least-remote panel must cross a link, cut a narrow lead
-    // panel off it: only that sliver's pull is exposed before the first GEMM,
-    // the rest streams behind compute.
+    // Uniform panels of about `tgt`; per panel: remote and total piece bytes.
+    std::vector<std::uint64_t> rb, tb;
+    auto build = [&](std::int64_t tgt) {
+      std::int64_t np = std::max<std::int64_t>(2, (K + tgt - 1) / tgt);
+      np = std::min<std::int64_t>(np, K / 256);
+      std::int64_t width = (K + np - 1) / np;
+      width = (width + 31) / 32 * 32;
+      plan.k0.clear();
+      for (std::int64_t k = 0; k < K; k += width) plan.k0.push_back(k);
+      plan.k0.push_back(K);
+      for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
+      for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
+      const int n = static_cast<int>(plan.k0.size()) - 1;
+      rb.assign(n, 0);
+      tb.assign(n, 0);
+      for (int p = 0; p < n; ++p)
+        for (const auto* ranges : {&plan.ar, &plan.br})
+          for (const Range& r : *ranges)
+            for (const Piece& pc : r.panels[p]) {
+              bool remote = false;
+              source_ptr(*local(w), pc.matrix, pc.coord, pol, &remote);
+              if (remote) rb[p] += pc.bytes();
+              tb[p] += pc.bytes();
+            }
+    };
+    if (std::getenv("DM_PANEL_K") != nullptr) {
+      build(target);
+    } else {
+      // Widest panels whose exposed start -- the least-remote panel's pull
+      // (~400 GB/s) and split (~1.5 TB/s of input) before the first GEMM --
+      // stays within 3% of this worker's GEMM time (~320 TFLOP/s): fewer
+      // panels mean fewer beta=1 passes over C (measured at 2 GPUs: 16384-wide
+      // 608 vs 8192-wide 595 TFLOP/s), but a wide all-remote first panel
+      // stalls the start (8 GPUs: 2x4 grid).
+      for (std::int64_t tgt : {std::int64_t{16384}, std::int64_t{8192}}) {
+        build(tgt);
+        const int b = static_cast<int>(std::min_element(rb.begin(), rb.end()) - rb.begin());
+        const double exposed = static_cast<double>(rb[b]) / 400e9 + static_cast<double>(tb[b]) / 1.5e12;
+        if (exposed <= 0.03 * work / 320e12) break;
+      }
+    }
+    // If even the least-remote panel must cross a link, optionally cut a
+    // ramp of narrow lead panels off it (DM_LEAD_PANEL_K; off by default).
     const std::int64_t lead = env_int("DM_LEAD_PANEL_K", 0);
-    const int np0 = static_cast<int>(plan.k0.size()) - 1;
-    std::vector<std::uint64_t> rb(np0, 0);
-    for (int p = 0; p < np0; ++p)
-      for (const auto* ranges : {&plan.ar, &plan.br})
-        for (const Range& r : *ranges)
-          for (const Piece& pc : r.panels[p]) {
-            bool remote = false;
-            source_ptr(*local(w), pc.matrix, pc.coord, pol, &remote);
-            if (remote) rb[p] += pc.bytes();
-          }
     const int best = static_cast<int>(std::min_element(rb.begin(), rb.end()) - rb.begin());
     if (lead > 0 && rb[best] > 0 && plan.k0[best + 1] - plan.k0[best] > 2 * lead) {
       // Ramp: lead, lead, 2 lead, 4 lead, ... so each sub-panel's GEMM is long
