@@ -111,3 +111,18 @@ def test_local_mode_across_gpus(cuda, monkeypatch, trans):
         monkeypatch.setenv("DM_FUSE_SPLIT", fuse)
         err, _ = run_case(P, 1536, (768, 768), trans, devices=[w % ndev for w in range(P)])
         assert err <= TOL, fuse
+
+
+def test_eight_workers_2x4_across_gpus(cuda, monkeypatch):
+    """The 8-GPU grid (2x4 checkerboard) driven in LOCAL mode over the visible
+    GPUs (two workers per GPU on a 4-GPU box): its pull plans, copy-engine
+    landing and fused splits against the oracle."""
+    import torch
+    ndev = torch.cuda.device_count()
+    if ndev < 2:
+        pytest.skip("needs >= 2 GPUs")
+    monkeypatch.setenv("DM_PANEL_K", "512")
+    P, n = 8, 2048
+    for trans in (0, 3):
+        err, _ = run_case(P, n, (n // 2, n // 4), trans, devices=[w % ndev for w in range(P)])
+        assert err <= TOL, trans
