@@ -748,7 +748,7 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
   // Double64 runs the bit-exact SIMT kernel over one panel: the reference's
   // single k-ascending accumulation per output cannot be cut into panels.
   const bool f64 = da.precision == Precision::Double64;
-  if (plan.has_remote && K > 2 * 256 && target > 0 && work >= min_work && !f64) {
+  if (plan.has_remote && K > 2 * 256 && target != 0 && work >= min_work && !f64) {
     // Uniform panels of about `tgt`; per panel: remote and total piece bytes.
     std::vector<std::uint64_t> rb, tb;
     auto build = [&](std::int64_t tgt) {
@@ -774,7 +774,7 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
               tb[p] += pc.bytes();
             }
     };
-    if (std::getenv("DM_PANEL_K") != nullptr) {
+    if (target > 0 && std::getenv("DM_PANEL_K") != nullptr) {  // forced width (-1: the model)
       build(target);
     } else {
       // Widest panels whose exposed start -- the least-remote panel's pull
