@@ -28,6 +28,7 @@
 
 #include <cstdint>
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 
 #include "ptx.cuh"
@@ -635,15 +636,17 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
     bad |= make_operand_map(&maps.m[5], a.b_lo16, a.n, a.k, a.ldb16, true);
   }
   if (bad) return cudaErrorInvalidValue;
-  static bool attr_set[2][2][64] = {};
+  // per-device opt-in to > 48 KB dynamic smem (idempotent; atomic so concurrent
+  // host threads launching on different devices are well defined)
+  static std::atomic<bool> attr_set[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!attr_set[CG - 1][MODE][dev & 63]) {
+  if (!attr_set[dev & 63].load(std::memory_order_acquire)) {
     cudaError_t e = cudaFuncSetAttribute(tf32x3_gemm_kernel<CG, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set[CG - 1][MODE][dev & 63] = true;
+    attr_set[dev & 63].store(true, std::memory_order_release);
   }
   int sms = a.num_sms;
   if (sms <= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
