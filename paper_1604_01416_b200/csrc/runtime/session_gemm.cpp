@@ -16,6 +16,7 @@
 // consumed it, planes[s % 2] until step s-2's GEMM read them.
 #include <algorithm>
 #include <array>
+#include <deque>
 
 #include "../kernels/tf32x3_gemm.h"
 #include "session.hpp"
@@ -39,6 +40,7 @@ struct Session::GemmRun {
     const Piece* pc;
     const Planes* pl;
     bool landed;
+    cudaEvent_t ready;  // landed chunk: its own copy-done event (separate splits wait on it)
   };
 
   Session& S;
@@ -67,6 +69,7 @@ struct Session::GemmRun {
   unsigned* flag = nullptr;
   std::vector<cudaEvent_t> landed_ev, consumed_ev, split_ev, gemm_ev;
   std::vector<std::vector<Item>> items;
+  std::deque<Piece> chunk_pieces;  // sub-pieces of chunked pulls (stable addresses)
   std::vector<unsigned> seq;
   unsigned* sync = nullptr;  // lockstep counters
   std::size_t sync_bytes = 0;
@@ -230,7 +233,7 @@ struct Session::GemmRun {
           const void* src = resolve(pc, &remote, &cross);
           (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
           if (!cross) {
-            items[s].push_back({src, pc.lds, &pc, &planes[i][buf], false});
+            items[s].push_back({src, pc.lds, &pc, &planes[i][buf], false, nullptr});
             continue;
           }
           if (!any) {
@@ -239,11 +242,44 @@ struct Session::GemmRun {
             if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.pull, consumed_ev[s - nbuf], 0), "wait");
             if (trace) tp = S.trace_event(w.pull);
           }
+          // The first panel's pull is exposed (its split runs before any
+          // GEMM): cut it into row chunks of about DM_PULL_CHUNK_MB, each with
+          // its own event, so splitting chunk i overlaps copying chunk i+1.
+          // Later panels stay whole (their splits are usually fused).
+          const std::int64_t h = land_height(pc);
+          const std::int64_t chunk_mb = s == 0 ? env_int("DM_PULL_CHUNK_MB", 128) : 0;
+          const std::int64_t row_bytes = land_width(pc) * static_cast<std::int64_t>(esz);
+          const std::int64_t rows_per =
+              chunk_mb > 0 ? std::max<std::int64_t>(8, (chunk_mb << 20) / std::max<std::int64_t>(1, row_bytes)) : h;
+          const std::int64_t lp = land_pitch(pc);
           char* dst = landing[buf] + loff;
-          cuda_check(cudaMemcpy2DAsync(dst, land_pitch(pc) * esz, src, pc.lds * esz, land_width(pc) * esz,
-                                       land_height(pc), cudaMemcpyDefault, w.pull),
-                     "cudaMemcpy2DAsync(peer)");
-          items[s].push_back({dst, land_pitch(pc), &pc, &planes[i][buf], true});
+          for (std::int64_t h0 = 0; h0 < h; h0 += rows_per) {
+            const std::int64_t hn = std::min(rows_per, h - h0);
+            const Piece* sub = &pc;
+            if (hn != h) {  // sub-piece: rows (direct) or k (transposed) [h0, h0 + hn)
+              Piece q = pc;
+              if (pc.trans) {
+                q.kcols = hn;
+                q.dst_k = pc.dst_k + h0;
+              } else {
+                q.rows = hn;
+                q.dst_row = pc.dst_row + h0;
+              }
+              chunk_pieces.push_back(q);
+              sub = &chunk_pieces.back();
+            }
+            char* cdst = dst + h0 * lp * static_cast<std::int64_t>(esz);
+            const char* csrc = static_cast<const char*>(src) + h0 * pc.lds * static_cast<std::int64_t>(esz);
+            cuda_check(cudaMemcpy2DAsync(cdst, lp * esz, csrc, pc.lds * esz, land_width(pc) * esz, hn,
+                                         cudaMemcpyDefault, w.pull),
+                       "cudaMemcpy2DAsync(peer)");
+            cudaEvent_t ready = nullptr;
+            if (hn != h) {
+              ready = new_event();
+              cuda_check(cudaEventRecord(ready, w.pull), "event");
+            }
+            items[s].push_back({cdst, lp, sub, &planes[i][buf], true, ready});
+          }
           loff += land_bytes(pc);
           pulled += pc.bytes() / 4 * esz;
         }
@@ -261,10 +297,18 @@ struct Session::GemmRun {
   // Split step s with its own kernels on the split stream.
   void split_separate(int s) {
     if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_ev[s - nbuf], 0), "wait");  // planes free
-    if (landed_ev[s]) cuda_check(cudaStreamWaitEvent(w.side, landed_ev[s], 0), "wait");
     cudaEvent_t ta = trace ? S.trace_event(w.side) : nullptr;
     std::uint64_t bytes = 0;
-    for (const Item& it : items[s]) {
+    // local pieces first (no wait), then landed ones as their copies complete
+    std::vector<const Item*> seq_items;
+    for (const Item& it : items[s])
+      if (!it.landed) seq_items.push_back(&it);
+    for (const Item& it : items[s])
+      if (it.landed) seq_items.push_back(&it);
+    for (const Item* itp : seq_items) {
+      const Item& it = *itp;
+      if (it.landed)
+        cuda_check(cudaStreamWaitEvent(w.side, it.ready ? it.ready : landed_ev[s], 0), "wait");
       const Piece& pc = *it.pc;
       const Planes& pl = *it.pl;
       const std::int64_t off = plane_off(it);

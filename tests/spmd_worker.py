@@ -43,7 +43,7 @@ def main():
     A, B, C0 = s.gather(a), s.gather(b), s.gather(c)   # root 0 assembles (others untouched)
     # default schedule, then the K-panel pipeline forced on at this small size:
     # copy-engine landing + stream flags + split warps fused into the GEMM
-    forced = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PANEL_K": "512", "DM_FUSE_SPLIT": "2"}
+    forced = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PANEL_K": "512", "DM_FUSE_SPLIT": "2", "DM_PULL_CHUNK_MB": "1"}
     for tag, env in (("", {}), ("ce_", forced)):
         os.environ.update(env)
         for trans in range(4):

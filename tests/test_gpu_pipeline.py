@@ -107,10 +107,11 @@ def test_local_mode_across_gpus(cuda, monkeypatch, trans):
         pytest.skip("needs >= 2 GPUs")
     P = 4
     monkeypatch.setenv("DM_PANEL_K", "512")
-    for fuse in ("2", "0"):
+    for fuse, chunk in (("2", "0"), ("0", "0"), ("2", "1")):  # chunk 1 MiB: chunked first-panel pull
         monkeypatch.setenv("DM_FUSE_SPLIT", fuse)
+        monkeypatch.setenv("DM_PULL_CHUNK_MB", chunk)
         err, _ = run_case(P, 1536, (768, 768), trans, devices=[w % ndev for w in range(P)])
-        assert err <= TOL, fuse
+        assert err <= TOL, (fuse, chunk)
 
 
 def test_eight_workers_2x4_across_gpus(cuda, monkeypatch):
