@@ -205,6 +205,9 @@ int dm_worker_stats_reset(dm_session* s);
 /* Record CUDA events around every GEMM launch (fills gemm_ms). */
 int dm_set_gemm_timing(dm_session* s, int enable);
 int dm_worker_seed(dm_session* s, int worker, uint64_t* out); /* session.hpp:103 */
+/* seed_workers (session.hpp:115-125): new root seed for worker seeds and for
+ * matrices created afterwards; seeds[w] = mix64(root, w) for w < cap. */
+int dm_seed_workers(dm_session* s, uint64_t root, uint64_t* seeds, int cap);
 int dm_descriptor_digest(dm_session* s, uint64_t* master, uint64_t* workers, int cap);
 /* device pointer of an owned block (for tests / zero-copy interop) */
 int dm_block_device_ptr(dm_session* s, dm_matrix_id id, int row, int col, void** ptr,

@@ -402,6 +402,11 @@ class Session {
     check(dm_worker_seed(s_, w, &v));
     return v;
   }
+  std::vector<std::uint64_t> seed_workers(std::uint64_t root) {  // session.hpp:115-125
+    std::vector<std::uint64_t> v(static_cast<std::size_t>(worker_count()));
+    check(dm_seed_workers(s_, root, v.data(), static_cast<int>(v.size())));
+    return v;
+  }
   dm_worker_stats worker_stats(WorkerId w) const {
     dm_worker_stats st{};
     check(dm_worker_stats_get(s_, w, &st));

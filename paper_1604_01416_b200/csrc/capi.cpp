@@ -449,6 +449,13 @@ int dm_worker_seed(dm_session* s, int worker, uint64_t* out) {
   return guarded([&] { *out = S(s).worker_seed(worker); });
 }
 
+int dm_seed_workers(dm_session* s, uint64_t root, uint64_t* seeds, int cap) {
+  return guarded([&] {
+    const std::vector<uint64_t> v = S(s).seed_workers(root);
+    for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) seeds[i] = v[i];
+  });
+}
+
 int dm_descriptor_digest(dm_session* s, uint64_t* master, uint64_t* workers, int cap) {
   std::vector<uint64_t> v;
   const int rc = guarded([&] {

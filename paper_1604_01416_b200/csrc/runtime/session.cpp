@@ -981,6 +981,19 @@ std::uint64_t Session::worker_seed(int w) const {
   return mix64(root_seed_, static_cast<std::uint64_t>(w));
 }
 
+std::vector<std::uint64_t> Session::seed_workers(std::uint64_t root) {
+  require_live();
+  SyncScope scope(this);
+  root_seed_ = root;
+  std::vector<std::uint64_t> seeds;
+  for (int w = 0; w < P_; ++w) {
+    seeds.push_back(mix64(root, static_cast<std::uint64_t>(w)));
+    if (workers_[w]) workers_[w]->seed = seeds.back();  // OpCode::Seed on each worker
+  }
+  end_command();
+  return seeds;
+}
+
 std::uint64_t Session::master_digest() const { return table_digest(table_); }
 
 std::vector<std::uint64_t> Session::worker_digests() const {

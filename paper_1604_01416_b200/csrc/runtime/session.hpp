@@ -148,6 +148,9 @@ class Session {
   void reset_worker_stats();
   void set_gemm_timing(bool on) { timing_ = on; }
   std::uint64_t worker_seed(int w) const;
+  // Session::seed_workers (session.hpp:115-125): new root seed for the worker
+  // seeds and for every matrix created afterwards; returns mix64(root, w).
+  std::vector<std::uint64_t> seed_workers(std::uint64_t root);
   std::uint64_t master_digest() const;
   std::vector<std::uint64_t> worker_digests() const;
   void* block_device_ptr(MatrixId id, BlockCoord c, int* device) const;

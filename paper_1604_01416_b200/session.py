@@ -321,6 +321,14 @@ class Session:
         _check(lib.dm_worker_seed(self._h, w, C.byref(v)))
         return v.value
 
+    def seed_workers(self, root: int):
+        """Session::seed_workers (session.hpp:115-125): the new root seeds the
+        workers and every matrix created afterwards; returns mix64(root, w)."""
+        n = self.worker_count()
+        buf = (C.c_uint64 * n)()
+        _check(lib.dm_seed_workers(self._h, C.c_uint64(root & 0xFFFFFFFFFFFFFFFF), buf, n))
+        return list(buf)
+
     def descriptor_digests(self):
         m = C.c_uint64()
         buf = (C.c_uint64 * 1024)()

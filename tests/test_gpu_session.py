@@ -218,3 +218,20 @@ def test_async_pipeline_double_buffered(cuda, P):
         for got, want in zip(outs, sync_out):
             assert got.tobytes() == want.tobytes()
         assert s.descriptor(mats[0][2]).version == 2 + 4  # 4 sync + 2 async GEMMs on set 0
+
+
+def test_seed_workers_reseeds_new_matrices(cuda):
+    """Session::seed_workers (session.hpp:115-125): worker seeds become
+    mix64(root, w) and matrices created afterwards derive from the new root;
+    existing matrices keep their contents."""
+    from oracle import COracle
+    orc = COracle()
+    with Session(Config(worker_count=4, root_seed=42, devices=[0] * 4)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, 64, 48, 32, 24, 4)
+        a = s.create_matrix(lay, fill=FillKind.SeededRandom)  # id 1 under root 42
+        seeds = s.seed_workers(7)
+        assert seeds == [orc.matrix_seed(7, w) for w in range(4)]
+        assert [s.worker_seed(w) for w in range(4)] == seeds
+        b = s.create_matrix(lay, fill=FillKind.SeededRandom)  # id 2 under root 7
+        assert s.gather(b).tobytes() == orc.seeded_matrix(7, 2, 3, 64, 48, 32, 24).tobytes()
+        assert s.gather(a).tobytes() == orc.seeded_matrix(42, 1, 3, 64, 48, 32, 24).tobytes()
