@@ -725,12 +725,12 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     // GEMM (a GEMM of width w hides the split of ~3.7 w, tf32x3_gemm.cu).
     const std::int64_t growth = std::max<std::int64_t>(2, env_int("DM_PANEL_GROWTH", 3));
     plan.k0.clear();
-    std::int64_t k = 0, w = (local_lead + 31) / 32 * 32;
+    std::int64_t k = 0, width = (local_lead + 31) / 32 * 32;
     while (k < K) {
       plan.k0.push_back(k);
-      if (K - k < w + w * growth / 2) break;  // last panel absorbs a short tail
-      k += w;
-      w *= growth;
+      if (K - k < width + width * growth / 2) break;  // last panel absorbs a short tail
+      k += width;
+      width *= growth;
     }
     plan.k0.push_back(K);
     for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
