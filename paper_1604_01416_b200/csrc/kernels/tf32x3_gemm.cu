@@ -54,7 +54,6 @@ struct Cfg {
   static constexpr int kColsPerThread = kAccCols / 2;        // master accumulator registers
   static constexpr int kSplitWarps = 2;                      // fused split of the next panel
   static constexpr int kThreads = 64 + 32 * kEpiWarps + 32 * kSplitWarps;
-  static constexpr int kGroupM = 8;                          // rasterisation group
   static constexpr int kSplitTileBytes = 32 * (128 + 4) * 4;  // transposed split tile
   static constexpr int kSmemBytes =
       kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kSplitTileBytes;
