@@ -122,3 +122,22 @@ def test_error_codes_match_reference():
         assert _CODES[code].__name__ == name
     e = GOLDEN["errors"]
     assert (e["alias"], e["shape"], e["plan"], e["unknown_id"]) == (1, 3, 7, 1)
+
+
+def test_ctypes_signatures_match_header():
+    """Every C-ABI declaration's parameter count and return type agree with the
+    ctypes binding (guards the Python mirror against ABI drift)."""
+    import ctypes
+    hdr = open(os.path.join(ROOT, "include", "dmath_b200.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    decls = re.findall(r"^((?:const )?\w+\**)\s+\**(dm_[a-z0-9_]+)\(([^;]*?)\);", hdr, re.M | re.S)
+    assert len(decls) == len(EXPORTED)
+    ret_map = {"int": ctypes.c_int, "uint64_t": ctypes.c_uint64, "const char*": ctypes.c_char_p,
+               "const": ctypes.c_char_p}
+    for ret, name, params in decls:
+        params = " ".join(params.split())
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        fn = getattr(lib, name)
+        assert fn.argtypes is not None and len(fn.argtypes) == n, (name, n, fn.argtypes)
+        want = ret_map.get(ret.strip(), None)
+        assert want is None or fn.restype is want, (name, ret, fn.restype)
