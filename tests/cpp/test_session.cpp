@@ -108,6 +108,10 @@ static void host_checks() {
   CHECK(t.block_extent({2, 0}) == std::make_pair(std::int64_t{20}, std::int64_t{30}));  // trimmed edge
   const LayoutSpec cu = make_custom_layout(4, 4, 2, 2, 2, {1, 0, 0, 1});
   CHECK(cu.owner({0, 0}) == 1 && cu.owner({1, 1}) == 1);
+  // invalid geometry raises the reference's UsageError (layout.hpp:43-59, 122-139)
+  CHECK(throws<UsageError>([] { make_layout(LayoutKind::Checkerboard2D, 10, 10, 0, 5, 4).owner({0, 0}); }));
+  CHECK(throws<UsageError>([] { make_layout(LayoutKind::Checkerboard2D, 10, 10, 5, 5, 0).owner({0, 0}); }));
+  CHECK(throws<UsageError>([] { make_layout(LayoutKind::Checkerboard2D, 10, 10, 5, 5, 4).owner({5, 0}); }));
   // binary16 narrowing rules of the host conversion (half.hpp)
   HostMatrix h(1, 4, Precision::Half16);
   h.set(0, 0, 1.0);
