@@ -95,6 +95,17 @@ typedef struct dm_descriptor {
   dm_layout layout; /* layout.custom points into session-owned storage */
 } dm_descriptor;
 
+/* One worker-to-worker block transfer (TransferRecord, transport.hpp:27-38):
+ * `bytes` = payload read from src's block (a GEMM may read part of a block). */
+typedef struct dm_transfer_record {
+  uint64_t seq;
+  int32_t src, dst;
+  uint64_t matrix_id;
+  int32_t row, col;
+  uint64_t bytes;
+  char op[32];
+} dm_transfer_record;
+
 typedef struct dm_session_config {
   int32_t worker_count;     /* P (Config::worker_count, session.hpp:56) */
   int32_t mode;             /* dm_mode */
@@ -205,6 +216,10 @@ int dm_worker_stats_reset(dm_session* s);
 /* Record CUDA events around every GEMM launch (fills gemm_ms). */
 int dm_set_gemm_timing(dm_session* s, int enable);
 int dm_worker_seed(dm_session* s, int worker, uint64_t* out); /* session.hpp:103 */
+/* trace() (session.hpp:94; TraceLog, transport.hpp:56-71): the block transfers
+ * this process's workers pulled, oldest first; fills up to cap records and
+ * returns the total count (negative status on error). */
+int dm_transfer_log(dm_session* s, dm_transfer_record* out, int cap);
 /* seed_workers (session.hpp:115-125): new root seed for worker seeds and for
  * matrices created afterwards; seeds[w] = mix64(root, w) for w < cap. */
 int dm_seed_workers(dm_session* s, uint64_t root, uint64_t* seeds, int cap);

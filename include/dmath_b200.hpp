@@ -12,6 +12,7 @@
 // the reference throws for the same condition (status codes map 1:1).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -401,6 +402,17 @@ class Session {
     std::uint64_t v = 0;
     check(dm_worker_seed(s_, w, &v));
     return v;
+  }
+  // Session::trace() (session.hpp:94): worker-to-worker block transfers pulled by
+  // this process's workers, oldest first (TransferRecord, transport.hpp:27-38).
+  std::vector<dm_transfer_record> trace() const {
+    const int n = dm_transfer_log(s_, nullptr, 0);
+    if (n < 0) check(-n);
+    std::vector<dm_transfer_record> out(static_cast<std::size_t>(n));
+    const int m = dm_transfer_log(s_, out.data(), n);
+    if (m < 0) check(-m);
+    out.resize(static_cast<std::size_t>(std::min(m, n)));
+    return out;
   }
   std::vector<std::uint64_t> seed_workers(std::uint64_t root) {  // session.hpp:115-125
     std::vector<std::uint64_t> v(static_cast<std::size_t>(worker_count()));

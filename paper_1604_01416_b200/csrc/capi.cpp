@@ -449,6 +449,28 @@ int dm_worker_seed(dm_session* s, int worker, uint64_t* out) {
   return guarded([&] { *out = S(s).worker_seed(worker); });
 }
 
+int dm_transfer_log(dm_session* s, dm_transfer_record* out, int cap) {
+  int n = 0;
+  const int rc = guarded([&] {
+    const auto& log = S(s).transfers();
+    n = static_cast<int>(log.size());
+    for (int i = 0; i < cap && i < n; ++i) {
+      const dm::TransferRecord& r = log[static_cast<std::size_t>(i)];
+      dm_transfer_record& o = out[i];
+      o.seq = r.seq;
+      o.src = r.src;
+      o.dst = r.dst;
+      o.matrix_id = r.matrix;
+      o.row = r.coord.row;
+      o.col = r.coord.col;
+      o.bytes = r.bytes;
+      std::memset(o.op, 0, sizeof o.op);
+      std::strncpy(o.op, r.op.c_str(), sizeof o.op - 1);
+    }
+  });
+  return rc != DM_OK ? -rc : n;
+}
+
 int dm_seed_workers(dm_session* s, uint64_t root, uint64_t* seeds, int cap) {
   return guarded([&] {
     const std::vector<uint64_t> v = S(s).seed_workers(root);

@@ -897,6 +897,7 @@ void Session::cache_foreign_a(const GemmArgs& g) {
                  "cache copy");
       (void)remote;
       w.stats.peer_bytes_read += blk.bytes();
+      log_transfer(da.layout.owner({r, 0}), w.id, g.a, {r, 0}, blk.bytes());
       w.cache[{g.a, {r, 0}}] = std::move(blk);
     }
   }
@@ -906,6 +907,7 @@ void Session::cache_foreign_a(const GemmArgs& g) {
 void Session::general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
                            bool tb) {
   require_live();
+  op_tag_ = "general_gemm";
   GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, false);
   validate_general(g);
   run_gemm(g, SourcePolicy::Peer);
@@ -918,13 +920,18 @@ void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, Mat
                           bool tb, bool cache_a) {
   require_live();
   SyncScope scope(this);
+  op_tag_ = "cyclic_gemm";
   GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, cache_a);
   validate_cyclic(g, nullptr);
-  run_gemm(g, SourcePolicy::Peer);
   if (cache_a) {
-    cache_foreign_a(g);  // CyclicGemmExec::finish, ops.hpp:278-289
+    // Keep what you've seen (CyclicGemmExec::finish, ops.hpp:278-289): fill the
+    // cache first, so the GEMM reads the fresh copies and every foreign block
+    // crosses the link once per version instead of twice.
+    cache_foreign_a(g);
     cache_meta_[a] = table_.at(a).version;
+    run_gemm(g, SourcePolicy::Peer);
   } else {
+    run_gemm(g, SourcePolicy::Peer);
     for (auto& w : workers_) {
       if (!w) continue;
       auto it = w->cache.lower_bound({a, {0, 0}});
@@ -939,6 +946,7 @@ void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, Mat
 void Session::cached_backward_gemm(MatrixId w_id, MatrixId dy, MatrixId dx) {
   require_live();
   SyncScope scope(this);
+  op_tag_ = "cached_backward_gemm";
   GemmArgs g = gemm_command(1.0, w_id, dy, 0.0, dx, false, false, false);
   std::vector<WorkerId> strip_owners;
   validate_cyclic(g, &strip_owners);

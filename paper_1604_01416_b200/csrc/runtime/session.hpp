@@ -50,6 +50,18 @@ struct BlockKey {
   }
 };
 
+// One worker-to-worker block transfer (the reference's TransferRecord,
+// transport.hpp:27-38): `bytes` is the payload this worker read from `src`'s
+// block (a GEMM may read part of a block), op the command that moved it.
+struct TransferRecord {
+  std::uint64_t seq = 0;
+  int src = 0, dst = 0;
+  MatrixId matrix = 0;
+  BlockCoord coord;
+  std::uint64_t bytes = 0;
+  std::string op;
+};
+
 struct GemmArgs {
   double alpha = 1.0, beta = 0.0;
   MatrixId a = 0, b = 0, c = 0;
@@ -251,6 +263,14 @@ class Session {
   std::map<MatrixId, MatrixDescriptor> table_;
   std::map<MatrixId, std::uint64_t> cache_meta_;
   std::uint64_t nondet_counter_ = 0;
+  std::vector<TransferRecord> transfers_;  // trace() (transport.hpp:56-71); this process's pulls
+  const char* op_tag_ = "";                // command being executed (TransferRecord::op)
+ public:
+  const std::vector<TransferRecord>& transfers() const { return transfers_; }
+  void log_transfer(int src, int dst, MatrixId m, BlockCoord c, std::uint64_t bytes) {
+    transfers_.push_back({transfers_.size() + 1, src, dst, m, c, bytes, op_tag_});
+  }
+ private:
   std::size_t arena_bytes_ = 0;               // replicated: every worker's arena size
   std::vector<void*> arena_ptrs_;             // per worker (peer-readable)
   std::unique_ptr<Comm> comm_;

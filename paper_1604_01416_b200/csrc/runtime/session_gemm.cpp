@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <array>
 #include <deque>
+#include <map>
 
 #include "../kernels/tf32x3_gemm.h"
 #include "session.hpp"
@@ -70,6 +71,7 @@ struct Session::GemmRun {
   std::vector<cudaEvent_t> landed_ev, consumed_ev, split_ev, gemm_ev;
   std::vector<std::vector<Item>> items;
   std::deque<Piece> chunk_pieces;  // sub-pieces of chunked pulls (stable addresses)
+  std::map<BlockKey, std::uint64_t> pulled_blocks;  // remote bytes read per block (trace())
   std::vector<unsigned> seq;
   unsigned* sync = nullptr;  // lockstep counters
   std::size_t sync_bytes = 0;
@@ -232,6 +234,7 @@ struct Session::GemmRun {
           bool remote, cross;
           const void* src = resolve(pc, &remote, &cross);
           (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() / 4 * esz;
+          if (remote) pulled_blocks[{pc.matrix, pc.coord}] += pc.bytes() / 4 * esz;
           if (!cross) {
             items[s].push_back({src, pc.lds, &pc, &planes[i][buf], false, nullptr});
             continue;
@@ -473,6 +476,7 @@ struct Session::GemmRun {
                      "assemble_f64");
           w.stats.split_launches += 1;
           (remote ? w.stats.peer_bytes_read : w.stats.local_bytes_read) += pc.bytes() * 2;
+          if (remote) pulled_blocks[{pc.matrix, pc.coord}] += pc.bytes() * 2;
         }
       }
     };
@@ -500,8 +504,17 @@ struct Session::GemmRun {
     }
   }
 
+  // one trace() record per foreign block this worker read in the command
+  void log_pulls() {
+    for (const auto& [key, bytes] : pulled_blocks)
+      S.log_transfer(S.table_.at(key.matrix).layout.owner(key.coord), w.id, key.matrix, key.coord, bytes);
+  }
+
   void run() {
-    if (S.table_.at(g.a).precision == Precision::Double64) return run_f64();
+    if (S.table_.at(g.a).precision == Precision::Double64) {
+      run_f64();
+      return log_pulls();
+    }
     setup();
     prepare(0);
     split_separate(0);
@@ -516,6 +529,7 @@ struct Session::GemmRun {
       gemm_step(step, fused_next ? &jobs : nullptr);
       if (fused_next) consumed_ev[step + 1] = gemm_ev[step];  // split inside this step's launches
     }
+    log_pulls();
   }
 };
 

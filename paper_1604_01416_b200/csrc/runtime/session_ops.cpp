@@ -142,6 +142,7 @@ void Session::sync_replicas(MatrixId id) {
                                    cudaMemcpyDefault, w.side),
                    "replica pull");
         w.stats.peer_bytes_read += blk.bytes();
+        log_transfer(d.layout.owner({r, c}), w.id, id, {r, c}, blk.bytes());
         w.replicas[{id, {r, c}}] = std::move(blk);
       }
   }
@@ -150,6 +151,7 @@ void Session::sync_replicas(MatrixId id) {
 
 // ReplicateExec (ops.hpp:660-702) + descriptor effects (runtime_types.hpp:302-307).
 void Session::replicate(MatrixId id, bool enable) {
+  op_tag_ = "replicate";
   require_live();
   SyncScope scope(this);
   descriptor(id);

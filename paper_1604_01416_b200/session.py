@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from ._lib import Descriptor, Layout, PoolStats, SessionConfig, WorkerStats, lib
+from ._lib import Descriptor, Layout, PoolStats, SessionConfig, TransferRecord, WorkerStats, lib
 
 
 # --------------------------------------------------------------- errors
@@ -320,6 +320,21 @@ class Session:
         v = C.c_uint64()
         _check(lib.dm_worker_seed(self._h, w, C.byref(v)))
         return v.value
+
+    def trace(self):
+        """Session::trace() (session.hpp:94; TraceLog, transport.hpp:56-71): the
+        worker-to-worker block transfers this process's workers pulled, oldest
+        first, as dicts {seq, src, dst, matrix_id, row, col, bytes, op}.  A GEMM
+        logs one record per foreign block it read (bytes = the part it read)."""
+        n = lib.dm_transfer_log(self._h, None, 0)
+        if n < 0:
+            _check(-n)
+        buf = (TransferRecord * max(n, 1))()
+        n = lib.dm_transfer_log(self._h, buf, n)
+        if n < 0:
+            _check(-n)
+        return [{"seq": r.seq, "src": r.src, "dst": r.dst, "matrix_id": r.matrix_id, "row": r.row,
+                 "col": r.col, "bytes": r.bytes, "op": r.op.decode()} for r in buf[:n]]
 
     def seed_workers(self, root: int):
         """Session::seed_workers (session.hpp:115-125): the new root seeds the

@@ -235,3 +235,40 @@ def test_seed_workers_reseeds_new_matrices(cuda):
         b = s.create_matrix(lay, fill=FillKind.SeededRandom)  # id 2 under root 7
         assert s.gather(b).tobytes() == orc.seeded_matrix(7, 2, 3, 64, 48, 32, 24).tobytes()
         assert s.gather(a).tobytes() == orc.seeded_matrix(42, 1, 3, 64, 48, 32, 24).tobytes()
+
+
+def test_trace_records_block_pulls(cuda):
+    """Session::trace() (TraceLog, transport.hpp:56-71), as the reference's
+    acceptance tests count transfers (tests/acceptance.cpp:165-171, 213-220):
+    a general_gemm pulls exactly the foreign blocks of its plan
+    (GeneralGemmExec::add_needed, ops.hpp:503-524); a cached forward pulls each
+    foreign W block once per version; the cached backward pulls nothing."""
+    from paper_1604_01416_b200 import plan_general_gemm
+    P, n = 4, 256
+    with Session(Config(worker_count=P, root_seed=5, devices=[0] * P)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
+        a, b, c = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(3))
+        assert s.trace() == []
+        s.general_gemm(1.0, a, b, 0.0, c)
+        recs = s.trace()
+        assert [r["seq"] for r in recs] == list(range(1, len(recs) + 1))
+        assert all(r["op"] == "general_gemm" and r["src"] != r["dst"] for r in recs)
+        for w in range(P):
+            nb, by = plan_general_gemm(lay, False, lay, False, lay, w)
+            mine = [r for r in recs if r["dst"] == w]
+            assert len(mine) == nb and sum(r["bytes"] for r in mine) == by
+            assert all(lay.owner(r["row"], r["col"]) == r["src"] for r in mine)
+    fin, fout, batch = 64 * P, 48, 8 * P
+    with Session(Config(worker_count=P, root_seed=6, devices=[0] * P)) as s:
+        W = s.create_matrix(make_layout(0, fin, fout, fin // P, fout, P), fill=FillKind.SeededRandom)
+        X = s.create_matrix(make_layout(1, fin, batch, fin, batch // P, P), fill=FillKind.SeededRandom)
+        Y = s.create_matrix(make_layout(1, fout, batch, fout, batch // P, P))
+        dY = s.create_matrix(make_layout(1, fout, batch, fout, batch // P, P), fill=FillKind.SeededRandom)
+        dX = s.create_matrix(make_layout(1, fin, batch, fin, batch // P, P))
+        s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+        first = s.trace()
+        assert len(first) == P * (P - 1)  # every worker caches every foreign W block once
+        assert all(r["matrix_id"] == W and r["bytes"] == (fin // P) * fout * 4 for r in first)
+        s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
+        s.cached_backward_gemm(W, dY, dX)
+        assert len(s.trace()) == len(first)  # fresh cache: nothing crosses again
