@@ -199,7 +199,9 @@ static void fc_zero_transfer_backward() {
   s.cyclic_gemm(1.0, W, X, 0.0, Y, true, false, true);  // Y = W^T X, keep W blocks
   CHECK(relfro(s.gather(Y), oracle(1.0, Wh, true, Xh, false, 0.0, Wh)) <= 1e-5);
   s.reset_worker_stats();
+  const std::size_t before = s.trace().size();  // as tests/acceptance.cpp:165-171
   s.cached_backward_gemm(W, dY, dX);  // dX = W dY from cached blocks only
+  CHECK(s.trace().size() == before);
   for (int w = 0; w < P; ++w) CHECK(s.worker_stats(w).peer_bytes_read == 0);
   CHECK(relfro(s.gather(dX), oracle(1.0, Wh, false, dYh, false, 0.0, Wh)) <= 1e-5);
 }
