@@ -20,6 +20,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <deque>
 #include <map>
 #include <memory>
@@ -263,12 +264,17 @@ class Session {
   std::map<MatrixId, MatrixDescriptor> table_;
   std::map<MatrixId, std::uint64_t> cache_meta_;
   std::uint64_t nondet_counter_ = 0;
-  std::vector<TransferRecord> transfers_;  // trace() (transport.hpp:56-71); this process's pulls
-  const char* op_tag_ = "";                // command being executed (TransferRecord::op)
+  // trace() (transport.hpp:56-71): this process's pulls, the newest
+  // DM_TRACE_CAP (default 2^20) records -- bounded so long runs do not grow it
+  std::deque<TransferRecord> transfers_;
+  std::uint64_t transfer_seq_ = 0;
+  const char* op_tag_ = "";  // command being executed (TransferRecord::op)
  public:
-  const std::vector<TransferRecord>& transfers() const { return transfers_; }
+  const std::deque<TransferRecord>& transfers() const { return transfers_; }
   void log_transfer(int src, int dst, MatrixId m, BlockCoord c, std::uint64_t bytes) {
-    transfers_.push_back({transfers_.size() + 1, src, dst, m, c, bytes, op_tag_});
+    static const std::size_t cap = static_cast<std::size_t>(std::max<std::int64_t>(1, env_int("DM_TRACE_CAP", 1 << 20)));
+    transfers_.push_back({++transfer_seq_, src, dst, m, c, bytes, op_tag_});
+    while (transfers_.size() > cap) transfers_.pop_front();
   }
  private:
   std::size_t arena_bytes_ = 0;               // replicated: every worker's arena size
