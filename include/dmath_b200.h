@@ -220,6 +220,8 @@ int dm_worker_seed(dm_session* s, int worker, uint64_t* out); /* session.hpp:103
  * this process's workers pulled, oldest first; fills up to cap records and
  * returns the total count (negative status on error). */
 int dm_transfer_log(dm_session* s, dm_transfer_record* out, int cap);
+/* root_seed (session.hpp:92): current root (after seed_workers / restore). */
+int dm_root_seed(dm_session* s, uint64_t* out);
 /* seed_workers (session.hpp:115-125): new root seed for worker seeds and for
  * matrices created afterwards; seeds[w] = mix64(root, w) for w < cap. */
 int dm_seed_workers(dm_session* s, uint64_t root, uint64_t* seeds, int cap);

@@ -305,6 +305,11 @@ class Session {
   }
 
   int worker_count() const { return cfg_.worker_count; }
+  std::uint64_t root_seed() const {  // session.hpp:92
+    std::uint64_t v = 0;
+    check(dm_root_seed(s_, &v));
+    return v;
+  }
 
   MatrixId create_matrix(const LayoutSpec& layout, Precision precision, FillKind fill,
                          const HostMatrix* host = nullptr) {

@@ -93,6 +93,7 @@ def _load() -> C.CDLL:
         "dm_set_gemm_timing": (C.c_int, [vp, C.c_int]),
         "dm_worker_seed": (C.c_int, [vp, C.c_int, P(u64)]),
         "dm_seed_workers": (C.c_int, [vp, u64, P(u64), C.c_int]),
+        "dm_root_seed": (C.c_int, [vp, P(u64)]),
         "dm_transfer_log": (C.c_int, [vp, P(TransferRecord), C.c_int]),
         "dm_descriptor_digest": (C.c_int, [vp, P(u64), P(u64), C.c_int]),
         "dm_block_device_ptr": (C.c_int, [vp, u64, C.c_int, C.c_int, P(vp), P(C.c_int)]),
@@ -125,6 +126,6 @@ EXPORTED = [
     "dm_add_row_col_sum", "dm_checkpoint", "dm_restore", "dm_general_gemm", "dm_cyclic_gemm", "dm_broadcast_gemm_reference",
     "dm_cached_backward_gemm", "dm_worker_count", "dm_local_workers", "dm_descriptor_get",
     "dm_pool_stats_get", "dm_pool_trim", "dm_worker_stats_get", "dm_worker_stats_reset",
-    "dm_set_gemm_timing", "dm_worker_seed", "dm_seed_workers", "dm_transfer_log", "dm_descriptor_digest", "dm_block_device_ptr",
+    "dm_set_gemm_timing", "dm_worker_seed", "dm_seed_workers", "dm_root_seed", "dm_transfer_log", "dm_descriptor_digest", "dm_block_device_ptr",
     "dm_barrier", "dm_set_async", "dm_marker_record", "dm_marker_elapsed", "dm_local_gemm_f32", "dm_local_gemm_f32_ex", "dm_fill_seeded_f32",
 ]

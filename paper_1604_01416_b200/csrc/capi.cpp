@@ -471,6 +471,10 @@ int dm_transfer_log(dm_session* s, dm_transfer_record* out, int cap) {
   return rc != DM_OK ? -rc : n;
 }
 
+int dm_root_seed(dm_session* s, uint64_t* out) {
+  return guarded([&] { *out = S(s).root_seed(); });
+}
+
 int dm_seed_workers(dm_session* s, uint64_t root, uint64_t* seeds, int cap) {
   return guarded([&] {
     const std::vector<uint64_t> v = S(s).seed_workers(root);

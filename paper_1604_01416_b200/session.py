@@ -180,6 +180,11 @@ class Config:
     rank: int = 0                    # spmd only
     devices: Optional[Sequence[int]] = None  # local: device per worker; spmd: [device]
     nccl_id: Optional[bytes] = None  # spmd only: 128-byte id from nccl_unique_id() on rank 0
+    # Config::deterministic (session.hpp:60): the reference picks single-threaded
+    # interleaving for reproducibility; here every command already runs in one
+    # global order with fixed-order reductions (non-deterministic row/col sums
+    # are chosen per call), so the flag is accepted and reported, never needed.
+    deterministic: bool = True
 
 
 def nccl_unique_id() -> bytes:
@@ -273,6 +278,16 @@ class Session:
         _check(lib.dm_session_shutdown(self._h))
 
     # -- introspection
+    def deterministic(self) -> bool:
+        """Session::deterministic (session.hpp:91)."""
+        return bool(self._cfg.deterministic)
+
+    def root_seed(self) -> int:
+        """Session::root_seed (session.hpp:92); follows seed_workers and restore."""
+        v = C.c_uint64()
+        _check(lib.dm_root_seed(self._h, C.byref(v)))
+        return v.value
+
     def worker_count(self) -> int:
         n = C.c_int()
         _check(lib.dm_worker_count(self._h, C.byref(n)))

@@ -229,7 +229,9 @@ def test_seed_workers_reseeds_new_matrices(cuda):
     with Session(Config(worker_count=4, root_seed=42, devices=[0] * 4)) as s:
         lay = make_layout(LayoutKind.Checkerboard2D, 64, 48, 32, 24, 4)
         a = s.create_matrix(lay, fill=FillKind.SeededRandom)  # id 1 under root 42
+        assert s.root_seed() == 42 and s.deterministic()
         seeds = s.seed_workers(7)
+        assert s.root_seed() == 7
         assert seeds == [orc.matrix_seed(7, w) for w in range(4)]
         assert [s.worker_seed(w) for w in range(4)] == seeds
         b = s.create_matrix(lay, fill=FillKind.SeededRandom)  # id 2 under root 7
