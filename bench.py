@@ -263,8 +263,21 @@ def run_ours(args):
                 band[:] = np.random.default_rng(fill_seed).random(band.shape, dtype=np.float32)
             return h, band
 
-        (hA, bA), (hB, bB) = host_matrix(rank), host_matrix(rank + 1000)
-        (hC0, bC0), (hC1, bC1) = host_matrix(None), host_matrix(None)
+        # Pin all four host matrices, then agree across ranks before any
+        # collective: a rank that cannot pin must not leave the others waiting.
+        pinned, why = [], ""
+        try:
+            for seed in (rank, rank + 1000, None, None):
+                pinned.append(host_matrix(seed))
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line
+            why = f"host pinning failed on rank {rank}: {e}"
+        if sum_over_ranks(1.0 if len(pinned) == 4 else 0.0) < world:
+            for _, band in pinned:
+                cudart.cudaHostUnregister(band.ctypes.data)
+            e2e = {"value": None, "unit": "TFLOP/s", "unavailable": why or "a peer rank could not pin host memory"}
+            pinned = None
+    if not args.no_e2e and pinned is not None:
+        (hA, bA), (hB, bB), (hC0, bC0), (hC1, bC1) = pinned
         root = -1 if world > 1 else 0
         # Double-buffered device operands + asynchronous commands: step i's
         # H2D (copy engine), GEMM (tensor cores) and D2H (copy engine) overlap
