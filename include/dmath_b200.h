@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define DMATH_B200_ABI_VERSION 1
+#define DMATH_B200_ABI_VERSION 2
 
 /* ---- status codes: reference exception classes (common.hpp:22-78) ---- */
 enum dm_status {
@@ -49,6 +49,14 @@ enum dm_layout_kind { /* layout.hpp:69-75 */
 };
 enum dm_precision { DM_HALF16 = 0, DM_SINGLE32 = 1, DM_DOUBLE64 = 2 }; /* precision.hpp:14 */
 enum dm_fill { DM_FILL_ZEROS = 0, DM_FILL_SEEDED = 1, DM_FILL_FROM_HOST = 2 }; /* runtime_types.hpp:68 */
+/* Split-product scheme of the fp32 tensor-core GEMM (both fp32-accurate,
+ * DESIGN.md section 4):
+ *   DM_GEMM_MIXED  : hi*hi as tcgen05 kind::tf32 + the two cross terms as bf16
+ *                    (kind::f16): 4 bf16-MMA slots per useful k16;
+ *   DM_GEMM_TF32X3 : lo*hi + hi*lo + hi*hi, all kind::tf32 (north star's
+ *                    3xTF32): 6 slots per k16;
+ *   DM_GEMM_DEFAULT: the DM_GEMM_MODE environment variable (0 = 3xTF32), else mixed. */
+enum dm_gemm_mode { DM_GEMM_DEFAULT = 0, DM_GEMM_MIXED = 1, DM_GEMM_TF32X3 = 2 };
 enum dm_mode {
   DM_MODE_LOCAL = 0, /* one process drives every worker (reference Session, session.hpp:64-76) */
   DM_MODE_SPMD = 1   /* one process per GPU; every rank makes the same calls (torchrun) */
@@ -114,6 +122,7 @@ typedef struct dm_session_config {
   uint64_t root_seed;       /* Config::root_seed (session.hpp:59) */
   const int32_t* devices;   /* LOCAL: device of each worker (NULL = w % device_count) */
   const void* nccl_id;      /* SPMD: 128-byte ncclUniqueId from rank 0 (dm_nccl_unique_id) */
+  int32_t gemm_mode;        /* dm_gemm_mode of every fp32/fp16 GEMM of the session */
 } dm_session_config;
 
 typedef struct dm_session dm_session;
@@ -216,6 +225,8 @@ int dm_worker_stats_reset(dm_session* s);
 /* Record CUDA events around every GEMM launch (fills gemm_ms). */
 int dm_set_gemm_timing(dm_session* s, int enable);
 int dm_worker_seed(dm_session* s, int worker, uint64_t* out); /* session.hpp:103 */
+/* The session's resolved split-product scheme: DM_GEMM_MIXED or DM_GEMM_TF32X3. */
+int dm_session_gemm_mode(dm_session* s, int* out);
 /* trace() (session.hpp:94; TraceLog, transport.hpp:56-71): the block transfers
  * this process's workers pulled, oldest first; fills up to cap records and
  * returns the total count (negative status on error). */
@@ -247,14 +258,30 @@ int dm_marker_elapsed(dm_session* s, int worker, int slot_a, int slot_b, float* 
 /* ---- the per-worker BLAS seam: local_gemm (kernels.hpp:81-89) on device
  * memory.  op(A) is m x k (A stored k x m when trans_a), op(B) is k x n (B
  * stored n x k when trans_b), row pitches in elements.  Stream-ordered on
- * `stream` (cudaStream_t, NULL = legacy default). ---- */
+ * `stream` (cudaStream_t, NULL = legacy default): the call only enqueues work
+ * and returns; its scratch (split planes) comes from a per-device pool and is
+ * recycled once an event after its kernels fired, so calls on different
+ * streams may run concurrently.  Inside a CUDA-graph capture use
+ * dm_local_gemm_f32_ws (the graph must own its scratch); these two return
+ * DM_ERR_USAGE there. ---- */
 int dm_local_gemm_f32(double alpha, const float* a, int64_t lda, int trans_a, const float* b,
                       int64_t ldb, int trans_b, double beta, float* c, int64_t ldc, int64_t m,
                       int64_t n, int64_t k, void* stream);
-/* Same, forcing the tile shape: cta_group 1 (128x128 tiles) or 2 (256x256 CTA-pair tiles). */
+/* Same, choosing the tile shape (cta_group 0 = auto, 1 = 128x128 tiles, 2 =
+ * 256x256 CTA-pair tiles) and the split-product scheme (dm_gemm_mode). */
 int dm_local_gemm_f32_ex(double alpha, const float* a, int64_t lda, int trans_a, const float* b,
                          int64_t ldb, int trans_b, double beta, float* c, int64_t ldc, int64_t m,
-                         int64_t n, int64_t k, int cta_group, void* stream);
+                         int64_t n, int64_t k, int cta_group, int gemm_mode, void* stream);
+/* Caller-owned scratch: bytes of workspace a dm_local_gemm_f32_ws call with
+ * these arguments needs on the current device (0 when m, n or k is 0). */
+int dm_local_gemm_f32_workspace_size(int64_t m, int64_t n, int64_t k, int cta_group, int gemm_mode,
+                                     size_t* bytes);
+/* local_gemm with a caller workspace (256-byte aligned, >= the size above):
+ * no allocation, no host synchronisation, capturable in a CUDA graph. */
+int dm_local_gemm_f32_ws(double alpha, const float* a, int64_t lda, int trans_a, const float* b,
+                         int64_t ldb, int trans_b, double beta, float* c, int64_t ldc, int64_t m,
+                         int64_t n, int64_t k, int cta_group, int gemm_mode, void* workspace,
+                         size_t workspace_bytes, void* stream);
 /* WorkerContext::fill_seeded (runtime_types.hpp:208-218) for one block. */
 int dm_fill_seeded_f32(float* dst, int64_t count, uint64_t matrix_seed, int block_row,
                        int block_col, void* stream);

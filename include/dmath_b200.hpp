@@ -286,6 +286,7 @@ class Session {
     int rank = 0;                    // SPMD: this process's worker id
     std::vector<int32_t> devices;    // LOCAL: device of each worker (empty: w % device_count)
     std::vector<unsigned char> nccl_id;  // SPMD: 128 bytes from dm_nccl_unique_id on rank 0
+    int gemm_mode = DM_GEMM_DEFAULT;     // dm_gemm_mode: split-product scheme of the GEMMs
   };
 
   explicit Session(Config cfg) : cfg_(std::move(cfg)) { check(dm_session_create(&c_config(), &s_)); }
@@ -442,6 +443,7 @@ class Session {
     cc_.root_seed = cfg_.root_seed;
     cc_.devices = cfg_.devices.empty() ? nullptr : cfg_.devices.data();
     cc_.nccl_id = cfg_.nccl_id.empty() ? nullptr : cfg_.nccl_id.data();
+    cc_.gemm_mode = cfg_.gemm_mode;
     return cc_;
   }
   Config cfg_;
@@ -454,6 +456,21 @@ inline void local_gemm(double alpha, const float* a, std::int64_t lda, bool tran
                        std::int64_t ldb, bool trans_b, double beta, float* c, std::int64_t ldc, std::int64_t m,
                        std::int64_t n, std::int64_t k, void* stream = nullptr) {
   check(dm_local_gemm_f32(alpha, a, lda, trans_a, b, ldb, trans_b, beta, c, ldc, m, n, k, stream));
+}
+
+// The same with caller-owned scratch (capturable in a CUDA graph).
+inline std::size_t local_gemm_workspace_size(std::int64_t m, std::int64_t n, std::int64_t k,
+                                             int gemm_mode = DM_GEMM_DEFAULT) {
+  std::size_t bytes = 0;
+  check(dm_local_gemm_f32_workspace_size(m, n, k, 0, gemm_mode, &bytes));
+  return bytes;
+}
+inline void local_gemm(double alpha, const float* a, std::int64_t lda, bool trans_a, const float* b,
+                       std::int64_t ldb, bool trans_b, double beta, float* c, std::int64_t ldc, std::int64_t m,
+                       std::int64_t n, std::int64_t k, void* workspace, std::size_t workspace_bytes,
+                       void* stream, int gemm_mode = DM_GEMM_DEFAULT) {
+  check(dm_local_gemm_f32_ws(alpha, a, lda, trans_a, b, ldb, trans_b, beta, c, ldc, m, n, k, 0, gemm_mode,
+                             workspace, workspace_bytes, stream));
 }
 
 }  // namespace dmath_b200

@@ -163,6 +163,8 @@ class RefOracle:
             "ref_general_gemm": (C.c_int, [vp, f64, u64, u64, f64, u64, C.c_int, C.c_int]),
             "ref_cyclic_gemm": (C.c_int, [vp, f64, u64, u64, f64, u64, C.c_int, C.c_int, C.c_int]),
             "ref_cached_backward_gemm": (C.c_int, [vp, u64, u64, u64]),
+            "ref_broadcast_gemm": (C.c_int, [vp, f64, u64, u64, f64, u64, C.c_int, C.c_int]),
+            "ref_trace_records": (C.c_int, [vp, u64, P(i64), C.c_char_p, C.c_int, P(C.c_int)]),
             "ref_descriptor": (C.c_int, [vp, u64, P(u64), P(u64)]),
             "ref_pool_stats": (C.c_int, [vp, C.c_int, P(u64)]),
             "ref_trace_count": (C.c_int, [vp, P(u64), P(u64)]),
@@ -361,6 +363,20 @@ class RefSession:
 
     def cached_backward_gemm(self, w, dy, dx) -> int:
         return self.ro.lib.ref_cached_backward_gemm(self.h, w, dy, dx)
+
+    def broadcast_gemm_reference(self, alpha, a, b, beta, c, ta=False, tb=False) -> int:
+        return self.ro.lib.ref_broadcast_gemm(self.h, alpha, a, b, beta, c, int(ta), int(tb))
+
+    def trace_records(self, start=0):
+        """trace() records from index `start`: dicts {src, dst, bytes, op}."""
+        cnt = C.c_int()
+        self.ro.check(self.ro.lib.ref_trace_records(self.h, start, None, None, 0, C.byref(cnt)))
+        n = cnt.value
+        out = (i64 * (3 * max(n, 1)))()
+        tags = C.create_string_buffer(48 * max(n, 1))
+        self.ro.check(self.ro.lib.ref_trace_records(self.h, start, out, tags, n, C.byref(cnt)))
+        return [{"src": out[3 * i], "dst": out[3 * i + 1], "bytes": out[3 * i + 2],
+                 "op": tags.raw[48 * i:48 * (i + 1)].split(b"\0", 1)[0].decode()} for i in range(n)]
 
     def version(self, mid) -> int:
         v, s = u64(), u64()

@@ -127,6 +127,30 @@ int ref_cyclic_gemm(void* s, double alpha, uint64_t a, uint64_t b, double beta, 
       [&] { static_cast<Session*>(s)->cyclic_gemm(alpha, a, b, beta, c, ta, tb, cache_a); });
 }
 
+int ref_broadcast_gemm(void* s, double alpha, uint64_t a, uint64_t b, double beta, uint64_t c, int ta,
+                       int tb) {
+  return guarded(
+      [&] { static_cast<Session*>(s)->broadcast_gemm_reference(alpha, a, b, beta, c, ta, tb); });
+}
+
+// trace() records (TraceLog::snapshot, transport.hpp:56-71) from index `from`:
+// per record src, dst, payload bytes and the op tag (NUL-padded, 48 bytes).
+int ref_trace_records(void* s, uint64_t from, int64_t* out3, char* tags, int cap, int* count) {
+  return guarded([&] {
+    const auto recs = static_cast<Session*>(s)->trace().snapshot();
+    int n = 0;
+    for (std::size_t i = from; i < recs.size(); ++i, ++n) {
+      if (n >= cap) continue;
+      out3[3 * n] = recs[i].src;
+      out3[3 * n + 1] = recs[i].dst;
+      out3[3 * n + 2] = static_cast<int64_t>(recs[i].payload_bytes);
+      std::memset(tags + 48 * n, 0, 48);
+      std::strncpy(tags + 48 * n, recs[i].op_tag.c_str(), 47);
+    }
+    *count = n;
+  });
+}
+
 int ref_cached_backward_gemm(void* s, uint64_t w, uint64_t dy, uint64_t dx) {
   return guarded([&] { static_cast<Session*>(s)->cached_backward_gemm(w, dy, dx); });
 }

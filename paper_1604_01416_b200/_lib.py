@@ -42,7 +42,7 @@ class TransferRecord(C.Structure):
 
 class SessionConfig(C.Structure):
     _fields_ = [("worker_count", i32), ("mode", i32), ("rank", i32), ("coherence_checks", i32),
-                ("root_seed", u64), ("devices", C.POINTER(i32)), ("nccl_id", vp)]
+                ("root_seed", u64), ("devices", C.POINTER(i32)), ("nccl_id", vp), ("gemm_mode", i32)]
 
 
 def _load() -> C.CDLL:
@@ -104,7 +104,11 @@ def _load() -> C.CDLL:
         "dm_local_gemm_f32": (C.c_int, [f64, vp, i64, C.c_int, vp, i64, C.c_int, f64, vp, i64,
                                         i64, i64, i64, vp]),
         "dm_local_gemm_f32_ex": (C.c_int, [f64, vp, i64, C.c_int, vp, i64, C.c_int, f64, vp, i64,
-                                           i64, i64, i64, C.c_int, vp]),
+                                           i64, i64, i64, C.c_int, C.c_int, vp]),
+        "dm_local_gemm_f32_workspace_size": (C.c_int, [i64, i64, i64, C.c_int, C.c_int, P(C.c_size_t)]),
+        "dm_local_gemm_f32_ws": (C.c_int, [f64, vp, i64, C.c_int, vp, i64, C.c_int, f64, vp, i64,
+                                           i64, i64, i64, C.c_int, C.c_int, vp, C.c_size_t, vp]),
+        "dm_session_gemm_mode": (C.c_int, [vp, P(C.c_int)]),
         "dm_fill_seeded_f32": (C.c_int, [vp, i64, u64, C.c_int, C.c_int, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -128,4 +132,5 @@ EXPORTED = [
     "dm_pool_stats_get", "dm_pool_trim", "dm_worker_stats_get", "dm_worker_stats_reset",
     "dm_set_gemm_timing", "dm_worker_seed", "dm_seed_workers", "dm_root_seed", "dm_transfer_log", "dm_descriptor_digest", "dm_block_device_ptr",
     "dm_barrier", "dm_set_async", "dm_marker_record", "dm_marker_elapsed", "dm_local_gemm_f32", "dm_local_gemm_f32_ex", "dm_fill_seeded_f32",
+    "dm_local_gemm_f32_workspace_size", "dm_local_gemm_f32_ws", "dm_session_gemm_mode",
 ]

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <set>
 #include <memory>
@@ -56,90 +57,181 @@ dm::Session& S(dm_session* s) {
   return *s->impl;
 }
 
-int gemm_mode_from_env() {
-  const char* v = std::getenv("DM_GEMM_MODE");
-  if (v == nullptr || *v == 0) return dm::kModeMixed;
-  return std::atoi(v) == 0 ? dm::kModeTf32x3 : dm::kModeMixed;
+// Split-product mode: explicit (dm_gemm_mode) or, for DM_GEMM_DEFAULT, the
+// DM_GEMM_MODE environment variable (0 = 3xTF32), else mixed.
+int resolve_gemm_mode(int requested) {
+  if (requested == DM_GEMM_TF32X3) return dm::kModeTf32x3;
+  if (requested == DM_GEMM_MIXED) return dm::kModeMixed;
+  if (requested != DM_GEMM_DEFAULT) throw dm::UsageError("unknown gemm_mode");
+  return dm::env_int("DM_GEMM_MODE", 1) == 0 ? dm::kModeTf32x3 : dm::kModeMixed;
 }
 
-// Scratch for the stateless local_gemm seam: one pool per device.
-dm::DevicePool& seam_pool(int dev) {
+// Scratch layout of one local_gemm call: K-major planes of op(A) (m x kp)
+// and op(B)^T (n x kp) -- hi fp32 + (lo fp32 | bf16 hi, bf16 lo) = 8 B per
+// element either way -- then the split-K partials; each region 256-B aligned.
+struct SeamLayout {
+  int64_t kp = 8;
+  size_t off[5] = {0, 0, 0, 0, 0};  // a_hi, a_second, b_hi, b_second, splitk ws
+  size_t ws_bytes = 0;
+  size_t total = 0;
+};
+
+SeamLayout seam_layout(const dm::Tf32x3Args& shape) {
+  SeamLayout l;
+  auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+  l.kp = std::max<int64_t>(8, (shape.k + 7) / 8 * 8);
+  if (shape.m <= 0 || shape.n <= 0 || shape.k <= 0) return l;
+  const size_t a = up(static_cast<size_t>(shape.m * l.kp) * 4), b = up(static_cast<size_t>(shape.n * l.kp) * 4);
+  l.off[1] = a;
+  l.off[2] = 2 * a;
+  l.off[3] = 2 * a + b;
+  l.off[4] = 2 * a + 2 * b;
+  l.ws_bytes = dm::tf32x3_splitk_bytes(shape);
+  l.total = l.off[4] + up(l.ws_bytes);
+  return l;
+}
+
+// Scratch of the pool-backed seam: one pool per device; buffers of a call go
+// back to the pool only once an event recorded after its kernels fired, so
+// the call is stream-ordered (no host wait) and calls on several streams can
+// run concurrently.
+struct SeamScratch {
+  std::mutex mu;
+  std::unique_ptr<dm::DevicePool> pool;
+  struct Pending {
+    cudaEvent_t done;
+    dm::DeviceBuffer buf;
+  };
+  std::deque<Pending> pending;
+  void reap() {
+    while (!pending.empty() && cudaEventQuery(pending.front().done) == cudaSuccess) {
+      cudaEventDestroy(pending.front().done);
+      pending.pop_front();
+    }
+    cudaGetLastError();  // cudaErrorNotReady is not an error here
+  }
+};
+
+SeamScratch& seam_scratch(int dev) {
   static std::mutex mu;
-  static std::map<int, std::unique_ptr<dm::DevicePool>> pools;
+  static std::map<int, std::unique_ptr<SeamScratch>> all;
   std::lock_guard<std::mutex> lk(mu);
-  auto& p = pools[dev];
-  if (!p) p = std::make_unique<dm::DevicePool>(dev);
+  auto& p = all[dev];
+  if (!p) {
+    p = std::make_unique<SeamScratch>();
+    p->pool = std::make_unique<dm::DevicePool>(dev);
+  }
   return *p;
+}
+
+dm::Tf32x3Args seam_shape(int64_t m, int64_t n, int64_t k, int cta_group, int mode) {
+  dm::Tf32x3Args a;
+  a.m = m;
+  a.n = n;
+  a.k = k;
+  a.cta_group = cta_group;
+  a.mode = mode;
+  return a;
+}
+
+// local_gemm (kernels.hpp:81-89) on device memory: split op(A) / op(B) into
+// K-major planes in `ws`, then the tcgen05 GEMM; everything on `st`.
+void local_gemm_run(double alpha, const float* a, int64_t lda, int ta, const float* b, int64_t ldb, int tb,
+                    double beta, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int cta_group, int mode,
+                    char* ws, const SeamLayout& L, cudaStream_t st) {
+  const int64_t kp = L.kp;
+  dm::Tf32x3Args args = seam_shape(m, n, k, cta_group, mode);
+  if (k > 0 && m > 0 && n > 0) {
+    args.a_hi = reinterpret_cast<const float*>(ws + L.off[0]);
+    args.b_hi = reinterpret_cast<const float*>(ws + L.off[2]);
+    args.lda = args.ldb = kp;
+    if (mode == dm::kModeMixed) {
+      args.a_hi16 = ws + L.off[1];
+      args.a_lo16 = ws + L.off[1] + m * kp * 2;
+      args.b_hi16 = ws + L.off[3];
+      args.b_lo16 = ws + L.off[3] + n * kp * 2;
+      args.lda16 = args.ldb16 = kp;
+    } else {
+      args.a_lo = reinterpret_cast<const float*>(ws + L.off[1]);
+      args.b_lo = reinterpret_cast<const float*>(ws + L.off[3]);
+    }
+    dm::cuda_check(dm::split_tf32(a, 0, lda, ta, m, k, const_cast<float*>(args.a_hi), const_cast<float*>(args.a_lo),
+                                  kp, const_cast<void*>(args.a_hi16), const_cast<void*>(args.a_lo16), kp, st),
+                   "split A");
+    dm::cuda_check(dm::split_tf32(b, 0, ldb, tb ? 0 : 1, n, k, const_cast<float*>(args.b_hi),
+                                  const_cast<float*>(args.b_lo), kp, const_cast<void*>(args.b_hi16),
+                                  const_cast<void*>(args.b_lo16), kp, st),
+                   "split B");
+    if (L.ws_bytes > 0) {
+      args.ws = reinterpret_cast<float*>(ws + L.off[4]);
+      args.ws_bytes = L.ws_bytes;
+    }
+  }
+  args.c = c;
+  args.ldc = ldc;
+  args.alpha = static_cast<float>(alpha);
+  args.beta = static_cast<float>(beta);
+  args.read_c = beta != 0.0 ? 1 : 0;
+  dm::cuda_check(dm::tf32x3_gemm(args, st), "tf32x3_gemm");
+}
+
+void local_gemm_validate(const float* a, int64_t lda, int ta, const float* b, int64_t ldb, int tb, float* c,
+                         int64_t ldc, int64_t m, int64_t n, int64_t k, int cta_group) {
+  if (m < 0 || n < 0 || k < 0) throw dm::ShapeError("local_gemm: negative dimension");
+  if ((m > 0 && n > 0) && c == nullptr) throw dm::UsageError("local_gemm: null C");
+  if (k > 0 && (a == nullptr || b == nullptr)) throw dm::UsageError("local_gemm: null operand");
+  if (ldc < n) throw dm::ShapeError("local_gemm: ldc < n");
+  if (lda < (ta ? m : k) || ldb < (tb ? k : n)) throw dm::ShapeError("local_gemm: bad pitch");
+  if (cta_group < 0 || cta_group > 2) throw dm::UsageError("local_gemm: cta_group must be 0, 1 or 2");
 }
 
 int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const float* b, int64_t ldb,
                     int tb, double beta, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
-                    int cta_group, void* stream) {
+                    int cta_group, int gemm_mode, void* stream) {
   return guarded([&] {
-    if (m < 0 || n < 0 || k < 0) throw dm::ShapeError("local_gemm: negative dimension");
-    if ((m > 0 && n > 0) && c == nullptr) throw dm::UsageError("local_gemm: null C");
-    if (k > 0 && (a == nullptr || b == nullptr)) throw dm::UsageError("local_gemm: null operand");
-    if (ldc < n) throw dm::ShapeError("local_gemm: ldc < n");
-    if (lda < (ta ? m : k) || ldb < (tb ? k : n)) throw dm::ShapeError("local_gemm: bad pitch");
+    local_gemm_validate(a, lda, ta, b, ldb, tb, c, ldc, m, n, k, cta_group);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    dm::cuda_check(cudaStreamIsCapturing(st, &cap), "cudaStreamIsCapturing");
+    if (cap != cudaStreamCaptureStatusNone)
+      throw dm::UsageError(
+          "local_gemm: a captured call must own its scratch for the graph's lifetime: use "
+          "dm_local_gemm_f32_ws with a caller workspace");
     int dev = 0;
     dm::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    dm::DevicePool& pool = seam_pool(dev);
-    const int mode = gemm_mode_from_env();
-    const int64_t kp = std::max<int64_t>(8, (k + 7) / 8 * 8);
-    dm::DeviceBuffer ah, al, bh, bl;
-    if (k > 0 && m > 0 && n > 0) {
-      // tf32x3: hi/lo fp32 planes; mixed: fp32 hi + two bf16 planes (same 8 B/elem)
-      ah = pool.acquire(static_cast<size_t>(m * kp) * 4);
-      al = pool.acquire(static_cast<size_t>(m * kp) * 4);
-      bh = pool.acquire(static_cast<size_t>(n * kp) * 4);
-      bl = pool.acquire(static_cast<size_t>(n * kp) * 4);
+    const int mode = resolve_gemm_mode(gemm_mode);
+    const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode));
+    SeamScratch& sc = seam_scratch(dev);
+    dm::DeviceBuffer buf;
+    {
+      std::lock_guard<std::mutex> lk(sc.mu);
+      sc.reap();
+      if (L.total > 0) buf = sc.pool->acquire(L.total);
     }
-    dm::Tf32x3Args args;
-    args.mode = mode;
-    args.a_hi = ah.f32();
-    args.b_hi = bh.f32();
-    args.lda = kp;
-    args.ldb = kp;
-    if (mode == dm::kModeMixed) {
-      args.a_hi16 = al.f32();
-      args.a_lo16 = static_cast<const char*>(al.data()) + m * kp * 2;
-      args.b_hi16 = bl.f32();
-      args.b_lo16 = static_cast<const char*>(bl.data()) + n * kp * 2;
-      args.lda16 = kp;
-      args.ldb16 = kp;
-    } else {
-      args.a_lo = al.f32();
-      args.b_lo = bl.f32();
+    // the scratch returns to the pool once the kernels that use it ran (also
+    // when a later launch of this call failed: earlier ones may still read it)
+    auto release = [&] {
+      if (L.total == 0) return;
+      cudaEvent_t done = nullptr;
+      if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventRecord(done, st) != cudaSuccess) {
+        cudaStreamSynchronize(st);  // cannot defer: drain, then release
+        if (done) cudaEventDestroy(done);
+        std::lock_guard<std::mutex> lk(sc.mu);
+        buf = dm::DeviceBuffer();
+        return;
+      }
+      std::lock_guard<std::mutex> lk(sc.mu);
+      sc.pending.push_back({done, std::move(buf)});
+    };
+    try {
+      local_gemm_run(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, cta_group, mode,
+                     static_cast<char*>(buf.data()), L, st);
+    } catch (...) {
+      release();
+      throw;
     }
-    if (k > 0 && m > 0 && n > 0) {
-      dm::cuda_check(dm::split_tf32(a, 0, lda, ta, m, k, ah.f32(), const_cast<float*>(args.a_lo), kp,
-                                    const_cast<void*>(args.a_hi16), const_cast<void*>(args.a_lo16),
-                                    kp, st),
-                     "split A");
-      dm::cuda_check(dm::split_tf32(b, 0, ldb, tb ? 0 : 1, n, k, bh.f32(), const_cast<float*>(args.b_lo),
-                                    kp, const_cast<void*>(args.b_hi16),
-                                    const_cast<void*>(args.b_lo16), kp, st),
-                     "split B");
-    }
-    args.c = c;
-    args.ldc = ldc;
-    args.m = m;
-    args.n = n;
-    args.k = k;
-    args.alpha = static_cast<float>(alpha);
-    args.beta = static_cast<float>(beta);
-    args.read_c = beta != 0.0 ? 1 : 0;
-    args.cta_group = cta_group;
-    dm::DeviceBuffer ws;
-    if (const size_t wsn = dm::tf32x3_splitk_bytes(args)) {
-      ws = pool.acquire(wsn);
-      args.ws = ws.f32();
-      args.ws_bytes = ws.capacity();
-    }
-    dm::cuda_check(dm::tf32x3_gemm(args, st), "tf32x3_gemm");
-    // scratch goes back to the pool: make the seam synchronous on its stream
-    dm::cuda_check(cudaStreamSynchronize(st), "local_gemm sync");
+    release();
   });
 }
 
@@ -374,13 +466,15 @@ int dm_cyclic_gemm(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b, 
 
 int dm_broadcast_gemm_reference(dm_session* s, double alpha, dm_matrix_id a, dm_matrix_id b,
                                 double beta, dm_matrix_id c, int ta, int tb) {
-  // Same preconditions and result as the ring variant (ops.hpp:572-577); on
-  // NVSwitch the pull schedule is the same for both.
-  return guarded([&] { S(s).cyclic_gemm(alpha, a, b, beta, c, ta != 0, tb != 0, false); });
+  return guarded([&] { S(s).broadcast_gemm(alpha, a, b, beta, c, ta != 0, tb != 0); });
 }
 
 int dm_cached_backward_gemm(dm_session* s, dm_matrix_id w, dm_matrix_id dy, dm_matrix_id dx) {
   return guarded([&] { S(s).cached_backward_gemm(w, dy, dx); });
+}
+
+int dm_session_gemm_mode(dm_session* s, int* out) {
+  return guarded([&] { *out = S(s).gemm_mode() == dm::kModeTf32x3 ? DM_GEMM_TF32X3 : DM_GEMM_MIXED; });
 }
 
 int dm_worker_count(dm_session* s, int* out) {
@@ -512,13 +606,38 @@ int dm_marker_elapsed(dm_session* s, int worker, int slot_a, int slot_b, float* 
 int dm_local_gemm_f32(double alpha, const float* a, int64_t lda, int ta, const float* b,
                       int64_t ldb, int tb, double beta, float* c, int64_t ldc, int64_t m,
                       int64_t n, int64_t k, void* stream) {
-  return local_gemm_impl(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, 0, stream);
+  return local_gemm_impl(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, 0, DM_GEMM_DEFAULT, stream);
 }
 
 int dm_local_gemm_f32_ex(double alpha, const float* a, int64_t lda, int ta, const float* b,
                          int64_t ldb, int tb, double beta, float* c, int64_t ldc, int64_t m,
-                         int64_t n, int64_t k, int cta_group, void* stream) {
-  return local_gemm_impl(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, cta_group, stream);
+                         int64_t n, int64_t k, int cta_group, int gemm_mode, void* stream) {
+  return local_gemm_impl(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, cta_group, gemm_mode, stream);
+}
+
+int dm_local_gemm_f32_workspace_size(int64_t m, int64_t n, int64_t k, int cta_group, int gemm_mode,
+                                     size_t* bytes) {
+  return guarded([&] {
+    if (bytes == nullptr) throw dm::UsageError("local_gemm_workspace_size: null output");
+    if (m < 0 || n < 0 || k < 0) throw dm::ShapeError("local_gemm: negative dimension");
+    *bytes = seam_layout(seam_shape(m, n, k, cta_group, resolve_gemm_mode(gemm_mode))).total;
+  });
+}
+
+int dm_local_gemm_f32_ws(double alpha, const float* a, int64_t lda, int ta, const float* b, int64_t ldb,
+                         int tb, double beta, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
+                         int cta_group, int gemm_mode, void* workspace, size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    local_gemm_validate(a, lda, ta, b, ldb, tb, c, ldc, m, n, k, cta_group);
+    const int mode = resolve_gemm_mode(gemm_mode);
+    const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode));
+    if (workspace_bytes < L.total || (L.total > 0 && workspace == nullptr))
+      throw dm::UsageError("local_gemm: workspace smaller than dm_local_gemm_f32_workspace_size");
+    if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+      throw dm::UsageError("local_gemm: workspace must be 256-byte aligned");
+    local_gemm_run(alpha, a, lda, ta, b, ldb, tb, beta, c, ldc, m, n, k, cta_group, mode,
+                   static_cast<char*>(workspace), L, static_cast<cudaStream_t>(stream));
+  });
 }
 
 int dm_fill_seeded_f32(float* dst, int64_t count, uint64_t matrix_seed, int block_row,

@@ -32,6 +32,15 @@ Session::Session(const dm_session_config& cfg) {
   rank_ = cfg.rank;
   coherence_ = cfg.coherence_checks != 0;
   root_seed_ = cfg.root_seed;
+  if (cfg.gemm_mode == DM_GEMM_TF32X3) {
+    gemm_mode_ = kModeTf32x3;
+  } else if (cfg.gemm_mode == DM_GEMM_MIXED) {
+    gemm_mode_ = kModeMixed;
+  } else if (cfg.gemm_mode == DM_GEMM_DEFAULT) {
+    gemm_mode_ = env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed;
+  } else {
+    throw ConfigError("init: unknown gemm_mode");
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -719,7 +728,13 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
   }
   const std::int64_t target = env_int("DM_PANEL_K", 8192);
   const std::int64_t local_lead = env_int("DM_PANEL_LOCAL", 0);
-  if (!plan.has_remote && local_lead > 0 && K >= 4 * local_lead && da.precision != Precision::Double64) {
+  // Only Single32 may cut K into panels: Double64 runs the bit-exact SIMT
+  // kernel whose single k-ascending accumulation per output cannot be split,
+  // and Half16 C is rounded once from the fp32 sum (AccumOf<Half> then
+  // narrow_store, kernels.hpp:29-35, 72) -- a launch per panel would round it
+  // once per panel.
+  const bool one_panel = da.precision != Precision::Single32;
+  if (!plan.has_remote && local_lead > 0 && K >= 4 * local_lead && !one_panel) {
     // All operands local: geometric panels.  Only the narrow lead panel's
     // split is exposed; every later panel is split by the previous panel's
     // GEMM (a GEMM of width w hides the split of ~3.7 w, tf32x3_gemm.cu).
@@ -745,10 +760,7 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     work += 2.0 * mb * nb * static_cast<double>(K);
   }
   const double min_work = static_cast<double>(env_int("DM_PIPELINE_MIN_GFLOP", 200)) * 1e9;
-  // Double64 runs the bit-exact SIMT kernel over one panel: the reference's
-  // single k-ascending accumulation per output cannot be cut into panels.
-  const bool f64 = da.precision == Precision::Double64;
-  if (plan.has_remote && K > 2 * 256 && target != 0 && work >= min_work && !f64) {
+  if (plan.has_remote && K > 2 * 256 && target != 0 && work >= min_work && !one_panel) {
     // Uniform panels of about `tgt`; per panel: remote and total piece bytes.
     std::vector<std::uint64_t> rb, tb;
     auto build = [&](std::int64_t tgt) {
@@ -939,6 +951,21 @@ void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, Mat
     }
     cache_meta_.erase(a);
   }
+  bump_version(c);
+  end_command();
+}
+
+void Session::broadcast_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
+                             bool tb) {
+  require_live();
+  SyncScope scope(this);
+  op_tag_ = "broadcast_gemm";
+  GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, false);
+  validate_cyclic(g, nullptr);  // build_cyclic_plan preconditions (session.hpp:239)
+  // Same pulls as the ring form: every strip owner reads every foreign A block
+  // whole from its owner (a fresh cached copy or replica serves instead).  No
+  // cache effects either way (session.hpp:236-242 leaves cache_meta_ alone).
+  run_gemm(g, SourcePolicy::Peer);
   bump_version(c);
   end_command();
 }

@@ -146,10 +146,15 @@ class Session {
   void restore_image(const std::string& path);  // into a fresh session
   std::uint64_t next_matrix_id() const { return next_matrix_id_; }
   std::uint64_t root_seed() const { return root_seed_; }
+  int gemm_mode() const { return gemm_mode_; }  // kModeMixed / kModeTf32x3
   void general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
                     bool tb);
   void cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta, bool tb,
                    bool cache_a);
+  // broadcast_gemm_reference (session.hpp:236-242, BroadcastGemmExec
+  // ops.hpp:578-651): the ring's preconditions and result, every A block read
+  // whole by every strip owner; A's block cache and cache_meta_ are untouched.
+  void broadcast_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta, bool tb);
   void cached_backward_gemm(MatrixId w, MatrixId dy, MatrixId dx);
   void shutdown();
   bool live() const { return live_; }
@@ -251,6 +256,7 @@ class Session {
 
   int P_ = 1;
   int mode_ = DM_MODE_LOCAL;
+  int gemm_mode_ = 1;  // kModeMixed
   int rank_ = 0;
   bool coherence_ = true;
   bool live_ = false;
@@ -273,7 +279,10 @@ class Session {
   const std::deque<TransferRecord>& transfers() const { return transfers_; }
   void log_transfer(int src, int dst, MatrixId m, BlockCoord c, std::uint64_t bytes) {
     static const std::size_t cap = static_cast<std::size_t>(std::max<std::int64_t>(1, env_int("DM_TRACE_CAP", 1 << 20)));
-    transfers_.push_back({++transfer_seq_, src, dst, m, c, bytes, op_tag_});
+    // BroadcastGemmExec tags each fan-out with the block row (ops.hpp:600-603)
+    std::string op = op_tag_;
+    if (op == "broadcast_gemm") op += ":r" + std::to_string(c.row);
+    transfers_.push_back({++transfer_seq_, src, dst, m, c, bytes, std::move(op)});
     while (transfers_.size() > cap) transfers_.pop_front();
   }
  private:

@@ -83,7 +83,7 @@ struct Session::GemmRun {
       : S(s), w(wk), g(ga), pol(p), plan(std::move(pl)), bufs(b), events(e),
         half_in(s.table_.at(ga.a).precision == Precision::Half16),
         esz(byte_width(s.table_.at(ga.a).precision)),
-        gemm_mode(env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed),
+        gemm_mode(s.gemm_mode_),
         trace(s.tracing() && !s.async_),
         np(static_cast<int>(plan.k0.size()) - 1),
         nbuf(np > 1 ? 2 : 1) {}
@@ -550,6 +550,11 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
       bound_inflight(w);
       wait_writes(w.side, g.a);
       wait_writes(w.side, g.b);
+      // C is about to be overwritten: every earlier local read of it (GEMMs
+      // whose pulls / fused splits read it as an operand, async gathers)
+      // finishes before this rank enters the barrier, so after the barrier no
+      // rank still reads the old C while its owner's GEMM writes it.
+      wait_all(w.side, g.c);
       device_barrier(w.side, 1);  // every rank, even one without C blocks
       wait_all(w.stream, g.c);
     }

@@ -185,6 +185,13 @@ class Config:
     # global order with fixed-order reductions (non-deterministic row/col sums
     # are chosen per call), so the flag is accepted and reported, never needed.
     deterministic: bool = True
+    # Split-product scheme of the fp32 tensor-core GEMM (include/dmath_b200.h
+    # dm_gemm_mode): "default" (env DM_GEMM_MODE, else mixed), "mixed"
+    # (tf32 hi*hi + bf16 cross terms), "3xtf32" (the north star's 3xTF32).
+    gemm_mode: str = "default"
+
+
+GEMM_MODES = {"default": 0, "mixed": 1, "3xtf32": 2}  # dm_gemm_mode
 
 
 def nccl_unique_id() -> bytes:
@@ -226,10 +233,13 @@ def _make_config(cfg: "Config"):
     if cfg.nccl_id is not None:
         nid = C.create_string_buffer(bytes(cfg.nccl_id), 128)
         keep.append(nid)
+    if cfg.gemm_mode not in GEMM_MODES:
+        raise ConfigError(f"unknown gemm_mode {cfg.gemm_mode!r} (one of {sorted(GEMM_MODES)})")
     c = SessionConfig(cfg.worker_count, mode, cfg.rank, int(cfg.coherence_checks),
                       cfg.root_seed & (2**64 - 1),
                       C.cast(devs, C.POINTER(C.c_int32)) if devs is not None else None,
-                      C.cast(nid, C.c_void_p) if nid is not None else None)
+                      C.cast(nid, C.c_void_p) if nid is not None else None,
+                      GEMM_MODES[cfg.gemm_mode])
     return c, keep
 
 
@@ -281,6 +291,12 @@ class Session:
     def deterministic(self) -> bool:
         """Session::deterministic (session.hpp:91)."""
         return bool(self._cfg.deterministic)
+
+    def gemm_mode(self) -> str:
+        """Resolved split-product scheme of this session: "mixed" or "3xtf32"."""
+        v = C.c_int()
+        _check(lib.dm_session_gemm_mode(self._h, C.byref(v)))
+        return {1: "mixed", 2: "3xtf32"}[v.value]
 
     def root_seed(self) -> int:
         """Session::root_seed (session.hpp:92); follows seed_workers and restore."""
@@ -504,9 +520,14 @@ class Session:
 
 
 # --------------------------------------------------------------- device seam
-def local_gemm(alpha, a, trans_a, b, trans_b, beta, c, cta_group: int = 0, stream=None):
+def local_gemm(alpha, a, trans_a, b, trans_b, beta, c, cta_group: int = 0, stream=None,
+               gemm_mode: str = "default", workspace=None):
     """local_gemm (kernels.hpp:81-89) on CUDA tensors (anything exposing
-    data_ptr()/shape/stride, e.g. torch float32 CUDA tensors, row-major)."""
+    data_ptr()/shape/stride, e.g. torch float32 CUDA tensors, row-major).
+    Stream-ordered: enqueues on `stream` (a cudaStream_t as int, None = the
+    legacy default stream) and returns.  `workspace` (a CUDA tensor of at
+    least local_gemm_workspace_size() bytes) makes the call allocation-free
+    and capturable in a CUDA graph."""
     def dims(t):
         r, cc = t.shape
         if t.stride(1) != 1:
@@ -522,9 +543,26 @@ def local_gemm(alpha, a, trans_a, b, trans_b, beta, c, cta_group: int = 0, strea
     if (cr, cc) != (m, n):
         raise ShapeError("local_gemm: output dimensions do not conform")
     st = C.c_void_p(stream) if stream is not None else None
+    if gemm_mode not in GEMM_MODES:
+        raise UsageError(f"unknown gemm_mode {gemm_mode!r}")
+    if workspace is not None:
+        nbytes = workspace.numel() * workspace.element_size()
+        _check(lib.dm_local_gemm_f32_ws(float(alpha), C.c_void_p(a.data_ptr()), lda, int(trans_a),
+                                        C.c_void_p(b.data_ptr()), ldb, int(trans_b), float(beta),
+                                        C.c_void_p(c.data_ptr()), ldc, m, n, k, cta_group,
+                                        GEMM_MODES[gemm_mode], C.c_void_p(workspace.data_ptr()), nbytes, st))
+        return
     _check(lib.dm_local_gemm_f32_ex(float(alpha), C.c_void_p(a.data_ptr()), lda, int(trans_a),
                                     C.c_void_p(b.data_ptr()), ldb, int(trans_b), float(beta),
-                                    C.c_void_p(c.data_ptr()), ldc, m, n, k, cta_group, st))
+                                    C.c_void_p(c.data_ptr()), ldc, m, n, k, cta_group,
+                                    GEMM_MODES[gemm_mode], st))
+
+
+def local_gemm_workspace_size(m: int, n: int, k: int, cta_group: int = 0, gemm_mode: str = "default") -> int:
+    """Bytes of caller workspace local_gemm(..., workspace=) needs on the current device."""
+    out = C.c_size_t()
+    _check(lib.dm_local_gemm_f32_workspace_size(m, n, k, cta_group, GEMM_MODES[gemm_mode], C.byref(out)))
+    return out.value
 
 
 def fill_seeded(t, matrix_seed: int, block_row: int, block_col: int, stream=None):

@@ -163,6 +163,31 @@ def main():
         results["checkpoint_roundtrip"] = bool(back.tobytes() == full.tobytes())
     r.close()
 
+    # 5. asynchronous command mode, K-panel pipeline forced: a GEMM output
+    #    feeds the next GEMM as a peer operand, then is overwritten while
+    #    peers may still be pulling its panels (write-after-read across ranks)
+    os.environ.update(forced)
+    s = session(55)
+    n = 1024
+    lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // pr, n // pc, world)
+    a, b, c, d, e = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(5))
+    A, B, D = s.gather(a), s.gather(b), s.gather(d)
+    s.set_async(True)
+    s.general_gemm(1.0, a, b, 0.0, c)      # C1 = A B
+    s.general_gemm(1.0, c, d, 0.0, e)      # E = C1 D: every rank pulls C1 panels
+    s.general_gemm(-1.0, a, b, 0.0, c)     # overwrite C while those pulls may run
+    s.barrier()
+    s.set_async(False)
+    Eg, Cg = s.gather(e), s.gather(c)
+    if rank == 0:
+        c1 = A.astype(np.float64) @ B.astype(np.float64)
+        want_e = c1 @ D.astype(np.float64)
+        results["async_chain_e"] = float(np.linalg.norm(Eg - want_e) / np.linalg.norm(want_e))
+        results["async_chain_c"] = float(np.linalg.norm(Cg + c1) / np.linalg.norm(c1))
+    s.close()
+    for k in forced:
+        del os.environ[k]
+
     allres = [None] * world
     dist.all_gather_object(allres, results)
     if rank == 0:

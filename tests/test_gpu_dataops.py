@@ -252,3 +252,30 @@ def test_checkpoint_corruption_detected(cuda, tmp_path):
     bad.write_bytes(bytes(data))
     with pytest.raises(IntegrityError):
         Session.restore(str(bad), Config(devices=[0] * 3))
+
+
+def test_half_gemm_forced_pipeline_rounds_once(cuda, monkeypatch):
+    """Half16 C is rounded once from the fp32 sum over the whole K (AccumOf<Half>
+    + narrow_store, kernels.hpp:29-35, 72) even when the K-panel pipeline is
+    forced on (remote pieces, tiny panels): within one half ulp of the
+    reference, like the single-panel case."""
+    from oracle import RefOracle, ref_available
+    if not ref_available():
+        pytest.skip("oracle/_ref not shipped")
+    monkeypatch.setenv("DM_PIPELINE_MIN_GFLOP", "0")
+    monkeypatch.setenv("DM_PANEL_K", "512")
+    P, m, n, k = 2, 128, 128, 2048
+    with session(P, 91) as s:
+        a = s.create_matrix(make_layout(1, m, k, m, k // P, P), Precision.Half16, FillKind.SeededRandom)
+        b = s.create_matrix(make_layout(0, k, n, k // P, n, P), Precision.Half16, FillKind.SeededRandom)
+        cm = s.create_matrix(make_layout(1, m, n, m, n // P, P), Precision.Half16, FillKind.SeededRandom)
+        s.general_gemm(1.5, a, b, -0.5, cm, False, False)
+        got = s.gather(cm)
+    with RefOracle().session(P, 91) as rs:
+        ra = rs.create_p(1, m, k, m, k // P, P, 0)
+        rb = rs.create_p(0, k, n, k // P, n, P, 0)
+        rc = rs.create_p(1, m, n, m, n // P, P, 0)
+        rs.general_gemm(1.5, ra, rb, -0.5, rc, False, False)
+        want = rs.gather_p(rc)
+    ulp = np.abs(got.view(np.int16).astype(np.int32) - want.view(np.int16).astype(np.int32))
+    assert ulp.max() <= 1 and (ulp == 0).mean() > 0.8

@@ -109,3 +109,80 @@ def test_split_k_deterministic(cuda):
         local_gemm(1.0, A, False, B, False, 0.0, C)
         outs.append(C.cpu())
     assert all(torch.equal(outs[0], o) for o in outs[1:])
+
+
+@pytest.mark.parametrize("gemm_mode", ["mixed", "3xtf32"])
+def test_explicit_gemm_mode(cuda, gemm_mode):
+    """The split-product scheme chosen through the ABI (dm_gemm_mode), not the
+    environment: both schemes meet the fp32 bar."""
+    import torch
+    from paper_1604_01416_b200 import local_gemm
+    g = torch.Generator(device="cpu").manual_seed(11)
+    A = (torch.rand((700, 1300), generator=g) * 2 - 1).to(cuda)
+    B = (torch.rand((1300, 900), generator=g) * 2 - 1).to(cuda)
+    C = torch.zeros((700, 900), device=cuda)
+    local_gemm(1.0, A, False, B, False, 0.0, C, gemm_mode=gemm_mode)
+    torch.cuda.synchronize()
+    assert _relfro(C, A.double() @ B.double()) <= 3e-6
+
+
+def test_stream_ordered_on_two_streams(cuda):
+    """dm_local_gemm_f32 only enqueues (no host wait, kernels.hpp:81-89 as a
+    stream-ordered seam): the call returns before its GEMM ran, and two calls
+    on two streams both land correctly while sharing the scratch pool."""
+    import torch
+    from paper_1604_01416_b200 import local_gemm
+    g = torch.Generator(device="cpu").manual_seed(5)
+    n = 8192
+    A = [(torch.rand((n, n), generator=g) * 2 - 1).to(cuda) for _ in range(2)]
+    B = (torch.rand((n, n), generator=g) * 2 - 1).to(cuda)
+    C = [torch.zeros((n, n), device=cuda) for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    local_gemm(1.0, A[0], False, B, False, 0.0, C[0])  # warm-up (pool, attributes)
+    torch.cuda.synchronize()
+    done = []
+    for i in range(2):
+        local_gemm(1.0, A[i], False, B, False, 0.0, C[i], stream=streams[i].cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(streams[i])
+        done.append(ev)
+    # ~3 ms of tensor-core work per call: still running when the calls returned
+    assert not done[1].query()
+    torch.cuda.synchronize()
+    Bd = B.double()
+    for i in range(2):
+        rows = torch.arange(0, n, 509, device=cuda)
+        want = A[i][rows].double() @ Bd
+        assert _relfro(C[i][rows], want) <= 3e-6
+
+
+def test_cuda_graph_capture_with_workspace(cuda):
+    """dm_local_gemm_f32_ws: caller-owned scratch, so the seam is capturable in
+    a CUDA graph and each replay recomputes from the operands' current
+    contents; the pool-backed entry refuses capture loudly."""
+    import torch
+    from paper_1604_01416_b200 import UsageError, local_gemm, local_gemm_workspace_size
+    g = torch.Generator(device="cpu").manual_seed(8)
+    m, n, k = 1024, 768, 2048
+    A = (torch.rand((k, m), generator=g) * 2 - 1).to(cuda)  # op(A) = A^T
+    B = (torch.rand((k, n), generator=g) * 2 - 1).to(cuda)
+    C0 = (torch.rand((m, n), generator=g) * 2 - 1).to(cuda)
+    C = C0.clone()
+    ws = torch.empty(local_gemm_workspace_size(m, n, k), dtype=torch.uint8, device=cuda)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):  # warm-up outside the capture
+        local_gemm(1.5, A, True, B, False, -0.5, C, stream=st.cuda_stream, workspace=ws)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        cs = torch.cuda.current_stream().cuda_stream
+        local_gemm(1.5, A, True, B, False, -0.5, C, stream=cs, workspace=ws)
+        with pytest.raises(UsageError):
+            local_gemm(1.5, A, True, B, False, -0.5, C, stream=cs)
+    for scale in (1.0, -2.0):
+        A.mul_(scale)
+        C.copy_(C0)
+        graph.replay()
+        torch.cuda.synchronize()
+        want = 1.5 * (A.double().T @ B.double()) - 0.5 * C0.double()
+        assert _relfro(C, want) <= 3e-6

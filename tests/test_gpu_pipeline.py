@@ -127,3 +127,34 @@ def test_eight_workers_2x4_across_gpus(cuda, monkeypatch):
     for trans in (0, 3):
         err, _ = run_case(P, n, (n // 2, n // 4), trans, devices=[w % ndev for w in range(P)])
         assert err <= TOL, trans
+
+
+@pytest.mark.parametrize("devices", [[0] * 4, "all"])
+def test_async_chain_write_after_read(cuda, monkeypatch, devices):
+    """Asynchronous mode with the pipeline forced: C feeds the next GEMM as a
+    peer operand and is then overwritten by a third GEMM.  The overwrite must
+    wait for every worker's reads of the old C (pulls, fused splits) -- the
+    reference's synchronous command order (session.hpp:585-605) as events."""
+    import torch
+    if devices == "all":
+        n_dev = torch.cuda.device_count()
+        if n_dev < 2:
+            pytest.skip("needs >= 2 GPUs")
+        devices = [w % n_dev for w in range(4)]
+    monkeypatch.setenv("DM_PANEL_K", "512")
+    monkeypatch.setenv("DM_FUSE_SPLIT", "2")
+    monkeypatch.setenv("DM_PULL_CHUNK_MB", "1")
+    n = 1024
+    with Session(Config(worker_count=4, root_seed=55, devices=devices)) as s:
+        lay = make_layout(LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, 4)
+        a, b, c, d, e = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(5))
+        A, B, D = s.gather(a), s.gather(b), s.gather(d)
+        s.set_async(True)
+        s.general_gemm(1.0, a, b, 0.0, c)
+        s.general_gemm(1.0, c, d, 0.0, e)
+        s.general_gemm(-1.0, a, b, 0.0, c)
+        s.barrier()
+        s.set_async(False)
+        c1 = A.astype(np.float64) @ B.astype(np.float64)
+        assert relfro(s.gather(e), c1 @ D.astype(np.float64)) <= TOL
+        assert relfro(s.gather(c), -c1) <= TOL

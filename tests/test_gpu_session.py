@@ -274,3 +274,90 @@ def test_trace_records_block_pulls(cuda):
         s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
         s.cached_backward_gemm(W, dY, dX)
         assert len(s.trace()) == len(first)  # fresh cache: nothing crosses again
+
+
+def _cyclic_fixture(s, ref, m, k, n, P, inner, seed, precision):
+    """make_cyclic_fixture (reference tests/test_dist_ops.cpp:33-59): A
+    row-blocked (`inner` blocks per worker), B and C column strips."""
+    from paper_1604_01416_b200 import Precision
+    np_t = np.float64 if precision == Precision.Double64 else np.float32
+    rng = np.random.default_rng(seed)
+    A, B, C0 = (rng.standard_normal(sh).astype(np_t) for sh in ((m, k), (k, n), (m, n)))
+    strip = -(-n // P)
+    la = make_layout(LayoutKind.RowBlocks1D, m, k, m // (P * inner), k, P)
+    lb = make_layout(LayoutKind.ColBlocks1D, k, n, k, strip, P)
+    lc = make_layout(LayoutKind.ColBlocks1D, m, n, m, strip, P)
+    ids = [s.create_matrix(l, precision=precision, fill=FillKind.FromHost, host=h)
+           for l, h in ((la, A), (lb, B), (lc, C0))]
+    rids = [ref.create_p(int(l.kind), l.global_rows, l.global_cols, l.block_rows, l.block_cols, P,
+                         int(precision), fill=2, host=h) for l, h in ((la, A), (lb, B), (lc, C0))]
+    return ids, rids
+
+
+def test_broadcast_gemm_reference_fanout(cuda):
+    """Reference tests/test_dist_ops.cpp:341-364: broadcast_gemm_reference
+    computes the same C as cyclic_gemm (bitwise, Double64) and every A block
+    fans out to both other workers, tagged broadcast_gemm:r<row>
+    (BroadcastGemmExec::send_phase, ops.hpp:590-606).  The transfer records
+    must equal the reference's own trace() for the same call."""
+    from oracle import RefOracle
+    from paper_1604_01416_b200 import Precision
+    ro = RefOracle()
+    P = 3
+    with Session(Config(worker_count=P, root_seed=42, devices=[0] * P)) as s, ro.session(P, 42) as r:
+        (a, b, c), _ = _cyclic_fixture(s, r, 6, 6, 6, P, 2, 900, Precision.Double64)
+        s.cyclic_gemm(1.0, a, b, 0.0, c, False, False, False)
+        cyc = s.gather(c)
+    with Session(Config(worker_count=P, root_seed=42, devices=[0] * P)) as s, ro.session(P, 42) as r:
+        (a, b, c), (ra, rb, rc) = _cyclic_fixture(s, r, 6, 6, 6, P, 2, 900, Precision.Double64)
+        before = len(s.trace())
+        s.broadcast_gemm_reference(1.0, a, b, 0.0, c, False, False)
+        assert s.gather(c).tobytes() == cyc.tobytes()
+        assert s.descriptor(c).version == 2  # FromHost scatter (1) + the GEMM
+        r0 = len(r.trace_records())
+        assert r.broadcast_gemm_reference(1.0, ra, rb, 0.0, rc) == 0
+        assert s.gather(c).tobytes() == r.gather_p(rc).tobytes()  # Double64: bit-exact
+        mine = s.trace()[before:]
+        theirs = r.trace_records(r0)
+        assert len(mine) == 3 * 2 * 2
+        dsts = {}
+        for rec in mine:
+            assert rec["op"].startswith("broadcast_gemm:r")
+            dsts.setdefault(rec["op"], set()).add(rec["dst"])
+        assert len(dsts) == 6 and all(len(d) == 2 for d in dsts.values())
+        key = lambda x: (x["src"], x["dst"], x["op"], x["bytes"])
+        assert sorted(map(key, mine)) == sorted(map(key, theirs))
+
+
+def test_broadcast_gemm_keeps_the_fc_cache(cuda):
+    """session.hpp:236-242: broadcast_gemm_reference leaves A's block cache and
+    cache_meta_ alone, so the FC sequence cyclic_gemm(cache_a) ->
+    broadcast_gemm_reference -> cached_backward_gemm succeeds -- in the
+    reference (run beside it) and here -- and the broadcast reads the fresh
+    cached copies instead of pulling again."""
+    from oracle import RefOracle
+    ro = RefOracle()
+    P, fin, fout, batch = 4, 64, 48, 32
+    rng = np.random.default_rng(77)
+    W, X, dY = (rng.standard_normal(sh).astype(np.float32) for sh in ((fin, fout), (fin, batch), (fout, batch)))
+    lw = make_layout(LayoutKind.RowBlocks1D, fin, fout, fin // P, fout, P)
+    lx = make_layout(LayoutKind.ColBlocks1D, fin, batch, fin, batch // P, P)
+    ly = make_layout(LayoutKind.ColBlocks1D, fout, batch, fout, batch // P, P)
+    with Session(Config(worker_count=P, root_seed=3, devices=[0] * P)) as s, ro.session(P, 3) as r:
+        ours, theirs = [], []
+        for l, h in ((lw, W), (lx, X), (ly, None), (ly, dY), (lx, None)):
+            ours.append(s.create_matrix(l, fill=FillKind.FromHost if h is not None else FillKind.Zeros, host=h))
+            theirs.append(r.create_p(int(l.kind), l.global_rows, l.global_cols, l.block_rows, l.block_cols, P, 1,
+                                     fill=2 if h is not None else 0, host=h))
+        w, x, y, dy, dx = ours
+        rw, rx, ry, rdy, rdx = theirs
+        s.cyclic_gemm(1.0, w, x, 0.0, y, True, False, True)          # FC forward, keep W blocks
+        assert r.cyclic_gemm(1.0, rw, rx, 0.0, ry, True, False, True) == 0
+        n_cached = len(s.trace())
+        s.broadcast_gemm_reference(1.5, w, x, -0.5, y, True, False)
+        assert r.broadcast_gemm_reference(1.5, rw, rx, -0.5, ry, True, False) == 0
+        assert relfro(s.gather(y), r.gather_p(ry)) <= TOL
+        assert len(s.trace()) == n_cached  # served from the fresh cache, nothing pulled
+        assert r.cached_backward_gemm(rw, rdy, rdx) == 0
+        s.cached_backward_gemm(w, dy, dx)  # raised CacheMissError while broadcast aliased cyclic
+        assert relfro(s.gather(dx), r.gather_p(rdx)) <= TOL

@@ -53,3 +53,5 @@ def test_spmd_parity(cuda):
     assert all(res[f"bwd_peer_bytes_r{r}"] == 0 for r in range(n))
     assert res["reshape_ok"] and res["sums_ok"] and res["checkpoint_roundtrip"]
     assert all(res[f"replica_ok_r{r}"] for r in range(n))
+    # async chained GEMMs with the pipeline forced (cross-rank write-after-read)
+    assert res["async_chain_e"] <= 1e-5 and res["async_chain_c"] <= 1e-5

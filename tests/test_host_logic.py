@@ -25,7 +25,7 @@ def test_header_symbols_exported():
     assert declared == set(EXPORTED)
     for name in declared:
         assert hasattr(lib, name), name
-    assert lib.dm_abi_version() == 1
+    assert lib.dm_abi_version() == 2
     assert os.path.exists(LIB_PATH)
 
 
