@@ -172,6 +172,7 @@ class RefOracle:
             "ref_layout_string": (C.c_int, [C.c_int, i64, i64, i64, i64, C.c_int, C.c_char_p, C.c_int]),
             "ref_local_gemm_f32": (C.c_int, [f64, FP, i64, i64, C.c_int, FP, i64, i64, C.c_int, f64, FP, i64, i64]),
             "ref_sampled_rows": (C.c_int, [f64, FP, i64, i64, FP, i64, i64, C.c_int, f64, FP, FP, i64, C.c_int]),
+            "ref_sampled_cols": (C.c_int, [f64, FP, i64, i64, C.c_int, FP, i64, i64, f64, FP, FP, i64, C.c_int]),
             "ref_fill_block": (C.c_int, [FP, i64, i64, u64, C.c_int, C.c_int]),
             "ref_fnv1a": (u64, [vp, i64]),
             "ref_create_matrix_p": (C.c_int, [vp, C.c_int, i64, i64, i64, i64, C.c_int, C.c_int, C.c_int, vp, P(u64)]),
@@ -220,6 +221,20 @@ class RefOracle:
         self.check(self.lib.ref_sampled_rows(float(alpha), _fp(a_rows), a_rows.shape[0], a_rows.shape[1],
                                              _fp(b), b.shape[0], b.shape[1], int(tb), float(beta),
                                              _fp(c0), _fp(out), n, threads))
+        return out
+
+    def sampled_cols(self, alpha, a, ta, b_cols, beta, c0_cols, threads=1) -> np.ndarray:
+        """Columns of alpha*opA*opB + beta*C0 for the given op(B) columns
+        (`b_cols`: ncols x K, row j = op(B)[:, j]); returns ncols x m (row j =
+        C[:, j]), bit-exact with the reference's distributed result."""
+        a = np.ascontiguousarray(a, np.float32)
+        b_cols = np.ascontiguousarray(b_cols, np.float32)
+        m = a.shape[1] if ta else a.shape[0]
+        out = np.zeros((b_cols.shape[0], m), np.float32)
+        c0 = np.ascontiguousarray(c0_cols if c0_cols is not None else out, np.float32)
+        self.check(self.lib.ref_sampled_cols(float(alpha), _fp(a), a.shape[0], a.shape[1], int(ta), _fp(b_cols),
+                                             b_cols.shape[0], b_cols.shape[1], float(beta), _fp(c0), _fp(out), m,
+                                             threads))
         return out
 
     def fill_block(self, rows, cols, matrix_seed, brow, bcol) -> np.ndarray:

@@ -244,6 +244,40 @@ int ref_sampled_rows(double alpha, const float* a_rows, int64_t nrows, int64_t k
   });
 }
 
+// Sampled columns of C = alpha op(A) op(B) + beta C0: column j of C depends
+// only on op(A) and column j of op(B) (k ascending in every executor,
+// ops.hpp:274, 485), so local_gemm on a K x 1 column view reproduces the
+// reference's distributed result for that column bit for bit.  `a` is the
+// full A storage (ar x ac, op via ta), `b_cols` holds op(B)[:, j] for each
+// sampled column (ncols x K), c0_cols / out_cols are ncols x m.
+int ref_sampled_cols(double alpha, const float* a, int64_t ar, int64_t ac, int ta, const float* b_cols,
+                     int64_t ncols, int64_t k, double beta, const float* c0_cols, float* out_cols, int64_t m,
+                     int threads) {
+  return guarded([&] {
+    std::atomic<int64_t> next{0};
+    std::vector<std::thread> pool;
+    std::vector<std::string> errs(static_cast<size_t>(threads));
+    for (int t = 0; t < threads; ++t)
+      pool.emplace_back([&, t] {
+        try {
+          for (int64_t j = next++; j < ncols; j = next++) {
+            DynConstView va{reinterpret_cast<const std::byte*>(a), ar, ac, Precision::Single32};
+            DynConstView vb{reinterpret_cast<const std::byte*>(b_cols + j * k), k, 1, Precision::Single32};
+            float* col = out_cols + j * m;
+            if (beta != 0.0) std::memcpy(col, c0_cols + j * m, static_cast<size_t>(m) * 4);
+            DynView vc{reinterpret_cast<std::byte*>(col), m, 1, Precision::Single32};
+            local_gemm(alpha, va, ta != 0, vb, false, beta, vc);
+          }
+        } catch (const std::exception& e) {
+          errs[static_cast<size_t>(t)] = e.what();
+        }
+      });
+    for (auto& th : pool) th.join();
+    for (auto& e : errs)
+      if (!e.empty()) throw UsageError(e);
+  });
+}
+
 // ---- precision-generic entry points (SURVEY 8(f) operations) ----
 int ref_create_matrix_p(void* s, int kind, int64_t gr, int64_t gc, int64_t br, int64_t bc,
                         int workers, int precision, int fill, const void* host, uint64_t* out) {
