@@ -172,6 +172,7 @@ void local_gemm_run(double alpha, const float* a, int64_t lda, int ta, const flo
   args.alpha = static_cast<float>(alpha);
   args.beta = static_cast<float>(beta);
   args.read_c = beta != 0.0 ? 1 : 0;
+  args.flush_k = dm::env_int("DM_FLUSH_K", 0);
   dm::cuda_check(dm::tf32x3_gemm(args, st), "tf32x3_gemm");
 }
 
