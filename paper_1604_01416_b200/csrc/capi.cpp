@@ -66,22 +66,33 @@ int resolve_gemm_mode(int requested) {
   return dm::env_int("DM_GEMM_MODE", 1) == 0 ? dm::kModeTf32x3 : dm::kModeMixed;
 }
 
-// Scratch layout of one local_gemm call: K-major planes of op(A) (m x kp)
-// and op(B)^T (n x kp) -- hi fp32 + (lo fp32 | bf16 hi, bf16 lo) = 8 B per
-// element either way -- then the split-K partials; each region 256-B aligned.
+// Scratch layout of one local_gemm call: the split planes of op(A) and op(B)
+// -- hi fp32 + (lo fp32 | bf16 hi, bf16 lo) = 8 B per element either way --
+// then the split-K partials; each region 256-B aligned.  An operand whose
+// storage is M/N-contiguous (transposed A, non-transposed B) gets MN-major
+// planes, so both splits read their source row by row (no transpose).
 struct SeamLayout {
-  int64_t kp = 8;
+  bool a_mn = false, b_mn = false;
+  int64_t lda = 8, ldb = 8;  // plane pitches (elements): K-major kp, MN-major m / n rounded to 32
+  int64_t a_elems = 0, b_elems = 0;
   size_t off[5] = {0, 0, 0, 0, 0};  // a_hi, a_second, b_hi, b_second, splitk ws
   size_t ws_bytes = 0;
   size_t total = 0;
 };
 
-SeamLayout seam_layout(const dm::Tf32x3Args& shape) {
+SeamLayout seam_layout(const dm::Tf32x3Args& shape, int ta, int tb) {
   SeamLayout l;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  l.kp = std::max<int64_t>(8, (shape.k + 7) / 8 * 8);
+  const bool mn_ok = dm::env_int("DM_MN_MAJOR", 1) != 0;
+  l.a_mn = mn_ok && ta != 0;
+  l.b_mn = mn_ok && tb == 0;
+  const int64_t kp = std::max<int64_t>(8, (shape.k + 7) / 8 * 8);
+  l.lda = l.a_mn ? (shape.m + 31) / 32 * 32 : kp;
+  l.ldb = l.b_mn ? (shape.n + 31) / 32 * 32 : kp;
   if (shape.m <= 0 || shape.n <= 0 || shape.k <= 0) return l;
-  const size_t a = up(static_cast<size_t>(shape.m * l.kp) * 4), b = up(static_cast<size_t>(shape.n * l.kp) * 4);
+  l.a_elems = l.a_mn ? shape.k * l.lda : shape.m * kp;
+  l.b_elems = l.b_mn ? shape.k * l.ldb : shape.n * kp;
+  const size_t a = up(static_cast<size_t>(l.a_elems) * 4), b = up(static_cast<size_t>(l.b_elems) * 4);
   l.off[1] = a;
   l.off[2] = 2 * a;
   l.off[3] = 2 * a + b;
@@ -135,33 +146,39 @@ dm::Tf32x3Args seam_shape(int64_t m, int64_t n, int64_t k, int cta_group, int mo
 }
 
 // local_gemm (kernels.hpp:81-89) on device memory: split op(A) / op(B) into
-// K-major planes in `ws`, then the tcgen05 GEMM; everything on `st`.
+// planes in `ws`, then the tcgen05 GEMM; everything on `st`.
 void local_gemm_run(double alpha, const float* a, int64_t lda, int ta, const float* b, int64_t ldb, int tb,
                     double beta, float* c, int64_t ldc, int64_t m, int64_t n, int64_t k, int cta_group, int mode,
                     char* ws, const SeamLayout& L, cudaStream_t st) {
-  const int64_t kp = L.kp;
   dm::Tf32x3Args args = seam_shape(m, n, k, cta_group, mode);
   if (k > 0 && m > 0 && n > 0) {
+    args.a_mn = L.a_mn ? 1 : 0;
+    args.b_mn = L.b_mn ? 1 : 0;
     args.a_hi = reinterpret_cast<const float*>(ws + L.off[0]);
     args.b_hi = reinterpret_cast<const float*>(ws + L.off[2]);
-    args.lda = args.ldb = kp;
+    args.lda = args.lda16 = L.lda;
+    args.ldb = args.ldb16 = L.ldb;
     if (mode == dm::kModeMixed) {
       args.a_hi16 = ws + L.off[1];
-      args.a_lo16 = ws + L.off[1] + m * kp * 2;
+      args.a_lo16 = ws + L.off[1] + L.a_elems * 2;
       args.b_hi16 = ws + L.off[3];
-      args.b_lo16 = ws + L.off[3] + n * kp * 2;
-      args.lda16 = args.ldb16 = kp;
+      args.b_lo16 = ws + L.off[3] + L.b_elems * 2;
     } else {
       args.a_lo = reinterpret_cast<const float*>(ws + L.off[1]);
       args.b_lo = reinterpret_cast<const float*>(ws + L.off[3]);
     }
-    dm::cuda_check(dm::split_tf32(a, 0, lda, ta, m, k, const_cast<float*>(args.a_hi), const_cast<float*>(args.a_lo),
-                                  kp, const_cast<void*>(args.a_hi16), const_cast<void*>(args.a_lo16), kp, st),
-                   "split A");
-    dm::cuda_check(dm::split_tf32(b, 0, ldb, tb ? 0 : 1, n, k, const_cast<float*>(args.b_hi),
-                                  const_cast<float*>(args.b_lo), kp, const_cast<void*>(args.b_hi16),
-                                  const_cast<void*>(args.b_lo16), kp, st),
-                   "split B");
+    // split_tf32 writes x[r][q] at plane + r * pitch + q with x[r][q] = trans ?
+    // src[q * lds + r] : src[r * lds + q]; a K-major plane is op(X) [mn x k], an
+    // MN-major plane its transpose [k x mn] (rows and columns swapped, trans flipped)
+    auto split = [&](const float* src, int64_t lds, int trans, int64_t mn_len, bool mn, const float* hi,
+                     const float* lo, const void* hi16, const void* lo16, int64_t pitch, const char* what) {
+      dm::cuda_check(dm::split_tf32(src, 0, lds, mn ? !trans : trans, mn ? k : mn_len, mn ? mn_len : k,
+                                    const_cast<float*>(hi), const_cast<float*>(lo), pitch, const_cast<void*>(hi16),
+                                    const_cast<void*>(lo16), pitch, st),
+                     what);
+    };
+    split(a, lda, ta, m, L.a_mn, args.a_hi, args.a_lo, args.a_hi16, args.a_lo16, L.lda, "split A");
+    split(b, ldb, tb ? 0 : 1, n, L.b_mn, args.b_hi, args.b_lo, args.b_hi16, args.b_lo16, L.ldb, "split B");
     if (L.ws_bytes > 0) {
       args.ws = reinterpret_cast<float*>(ws + L.off[4]);
       args.ws_bytes = L.ws_bytes;
@@ -201,7 +218,7 @@ int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const flo
     int dev = 0;
     dm::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
     const int mode = resolve_gemm_mode(gemm_mode);
-    const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode));
+    const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb);
     SeamScratch& sc = seam_scratch(dev);
     dm::DeviceBuffer buf;
     {
@@ -621,7 +638,8 @@ int dm_local_gemm_f32_workspace_size(int64_t m, int64_t n, int64_t k, int cta_gr
   return guarded([&] {
     if (bytes == nullptr) throw dm::UsageError("local_gemm_workspace_size: null output");
     if (m < 0 || n < 0 || k < 0) throw dm::ShapeError("local_gemm: negative dimension");
-    *bytes = seam_layout(seam_shape(m, n, k, cta_group, resolve_gemm_mode(gemm_mode))).total;
+    *bytes = std::max(seam_layout(seam_shape(m, n, k, cta_group, resolve_gemm_mode(gemm_mode)), 0, 0).total,
+                      seam_layout(seam_shape(m, n, k, cta_group, resolve_gemm_mode(gemm_mode)), 1, 1).total);
   });
 }
 
@@ -631,7 +649,7 @@ int dm_local_gemm_f32_ws(double alpha, const float* a, int64_t lda, int ta, cons
   return guarded([&] {
     local_gemm_validate(a, lda, ta, b, ldb, tb, c, ldc, m, n, k, cta_group);
     const int mode = resolve_gemm_mode(gemm_mode);
-    const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode));
+    const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb);
     if (workspace_bytes < L.total || (L.total > 0 && workspace == nullptr))
       throw dm::UsageError("local_gemm: workspace smaller than dm_local_gemm_f32_workspace_size");
     if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)

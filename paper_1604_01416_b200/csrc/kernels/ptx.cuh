@@ -286,6 +286,26 @@ __device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t smem_addr) {
   return d;
 }
 
+// MN-major operand staged by TMA with the 128-byte swizzle: 128-B rows run
+// along M (or N) -- 32 fp32 / 64 bf16 elements -- one row per k; 8-row
+// (8-k) core groups 1024 B apart (SBO); the next 128-B slice along M/N sits
+// LBO = 4096 B further (one [32 k x 128 B] TMA box per slice).
+__device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);  // start address [0,14)
+  d |= static_cast<uint64_t>(4096u >> 4) << 16;              // LBO [16,30): next MN slice
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;              // SBO [32,46): next 8-k group
+  d |= static_cast<uint64_t>(1u) << 46;                      // version = 1
+  d |= static_cast<uint64_t>(2u) << 61;                      // SWIZZLE_128B
+  return d;
+}
+
+// Operand-major bits of the instruction descriptor: bit 15 = A MN-major,
+// bit 16 = B MN-major (valid for tf32 and bf16 sources).
+__host__ __device__ constexpr uint32_t idesc_major(int a_mn, int b_mn) {
+  return (static_cast<uint32_t>(a_mn != 0) << 15) | (static_cast<uint32_t>(b_mn != 0) << 16);
+}
+
 // Instruction descriptor for kind::f16 with bf16 A/B, f32 D, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |

@@ -72,6 +72,7 @@ struct EpiParams {
   unsigned* sync;       // lockstep counters [waves * epochs], zeroed per launch
   int ksplit;           // >1: split-K; item (s, tile) writes its fp32 partial to ws[s]
   float* ws;            // [ksplit][m][n] partial tiles (ksplit > 1)
+  int a_mn, b_mn;       // operand planes MN-major (M / N contiguous) instead of K-major
 };
 
 // Work item t of a launch: tile t % tiles of K-split t / tiles, whose k-blocks
@@ -304,23 +305,36 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           if constexpr (CG == 2)
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb_tx) : "r"(fb));
           if (leader) mbar_arrive_expect_tx(fb, CG * C::kStageBytes);
-          auto load = [&](int i, uint32_t off, int row) {
-            if constexpr (CG == 1) tma_load_2d(&maps.m[i], smem_u32(st + off), fb_tx, kx, row, pol);
-            else tma_load_2d_cg2(&maps.m[i], smem_u32(st + off), fb_tx, kx, row, pol);
+          auto load2 = [&](int i, uint32_t off, int x, int y) {
+            if constexpr (CG == 1) tma_load_2d(&maps.m[i], smem_u32(st + off), fb_tx, x, y, pol);
+            else tma_load_2d_cg2(&maps.m[i], smem_u32(st + off), fb_tx, x, y, pol);
           };
+          // one operand tile (128 rows of M or N x 32 k): K-major = one box of
+          // 128 rows; MN-major = 128-B slices along M/N (32 fp32 / 64 bf16
+          // elements) of 32 k rows each, 4 KB apart
+          auto load = [&](int i, uint32_t off, int row, bool mn, bool bf16) {
+            if (!mn) {
+              load2(i, off, kx, row);
+            } else {
+              const int w = bf16 ? 64 : 32;
+#pragma unroll 1
+              for (int c = 0; c < 128 / w; ++c) load2(i, off + c * 4096u, row + c * w, kx);
+            }
+          };
+          const bool amn = ep.a_mn != 0, bmn = ep.b_mn != 0;
           if constexpr (MODE == kModeTf32x3) {
-            load(0, 0, arow);
-            load(1, C::kTileBytes, arow);
-            load(2, 2 * C::kTileBytes, brow);
-            load(3, 3 * C::kTileBytes, brow);
+            load(0, 0, arow, amn, false);
+            load(1, C::kTileBytes, arow, amn, false);
+            load(2, 2 * C::kTileBytes, brow, bmn, false);
+            load(3, 3 * C::kTileBytes, brow, bmn, false);
           } else {
             constexpr uint32_t h = C::kTileBytes / 2;  // bf16 tile: 128 rows x 64 B
-            load(0, 0, arow);
-            load(1, C::kTileBytes, brow);
-            load(2, 2 * C::kTileBytes, arow);
-            load(3, 2 * C::kTileBytes + h, arow);
-            load(4, 3 * C::kTileBytes, brow);
-            load(5, 3 * C::kTileBytes + h, brow);
+            load(0, 0, arow, amn, false);
+            load(1, C::kTileBytes, brow, bmn, false);
+            load(2, 2 * C::kTileBytes, arow, amn, true);
+            load(3, 2 * C::kTileBytes + h, arow, amn, true);
+            load(4, 3 * C::kTileBytes, brow, bmn, true);
+            load(5, 3 * C::kTileBytes + h, brow, bmn, true);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
@@ -329,7 +343,14 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     if (leader && lane == 0) {
-      constexpr uint32_t idesc = idesc_tf32(C::kUmmaM, C::kUmmaN);
+      const uint32_t idesc = idesc_tf32(C::kUmmaM, C::kUmmaN) | idesc_major(ep.a_mn, ep.b_mn);
+      // descriptor of an operand tile and its advance (16-B units) per k8
+      // (fp32) / k16 (bf16) step: K-major moves 32 B along the swizzled row,
+      // MN-major moves 8 (16) k rows = 1024 (2048) B
+      auto d32 = [](uint32_t a, int mn) { return mn ? sdesc_mn_sw128(a) : sdesc_k_sw128(a); };
+      auto d16 = [](uint32_t a, int mn) { return mn ? sdesc_mn_sw128(a) : sdesc_k_sw64(a); };
+      const uint64_t ia32 = ep.a_mn ? 64 : 2, ib32 = ep.b_mn ? 64 : 2;
+      const uint64_t ia16 = ep.a_mn ? 128 : 2, ib16 = ep.b_mn ? 128 : 2;
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0;
@@ -350,37 +371,36 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             const uint32_t s0 = smem_u32(smem + stage * C::kStageBytes);
             const uint32_t acc0 = (kb != kb0) ? 1u : 0u;
             if constexpr (MODE == kModeTf32x3) {
-              const uint64_t ahi = sdesc_k_sw128(s0);
-              const uint64_t alo = sdesc_k_sw128(s0 + C::kTileBytes);
-              const uint64_t bhi = sdesc_k_sw128(s0 + 2 * C::kTileBytes);
-              const uint64_t blo = sdesc_k_sw128(s0 + 3 * C::kTileBytes);
+              const uint64_t ahi = d32(s0, ep.a_mn);
+              const uint64_t alo = d32(s0 + C::kTileBytes, ep.a_mn);
+              const uint64_t bhi = d32(s0 + 2 * C::kTileBytes, ep.b_mn);
+              const uint64_t blo = d32(s0 + 3 * C::kTileBytes, ep.b_mn);
 #pragma unroll
               for (int j = 0; j < C::kBK / 8; ++j) {
-                // advance 8 tf32 = 32 B along K inside the swizzle row (16-B units);
-                // small terms first, then hi*hi
-                const uint64_t off = static_cast<uint64_t>(j * 2);
-                mma_tf32<CG>(d_tmem, alo + off, bhi + off, idesc, (acc0 | j) != 0);
-                mma_tf32<CG>(d_tmem, ahi + off, blo + off, idesc, 1u);
-                mma_tf32<CG>(d_tmem, ahi + off, bhi + off, idesc, 1u);
+                // k8 step j; small terms first, then hi*hi
+                const uint64_t oa = j * ia32, ob = j * ib32;
+                mma_tf32<CG>(d_tmem, alo + oa, bhi + ob, idesc, (acc0 | j) != 0);
+                mma_tf32<CG>(d_tmem, ahi + oa, blo + ob, idesc, 1u);
+                mma_tf32<CG>(d_tmem, ahi + oa, bhi + ob, idesc, 1u);
               }
             } else {
               constexpr uint32_t h = C::kTileBytes / 2;
-              constexpr uint32_t idesc16 = idesc_bf16(C::kUmmaM, C::kUmmaN);
-              const uint64_t ahi = sdesc_k_sw128(s0);
-              const uint64_t bhi = sdesc_k_sw128(s0 + C::kTileBytes);
-              const uint64_t ah16 = sdesc_k_sw64(s0 + 2 * C::kTileBytes);
-              const uint64_t al16 = sdesc_k_sw64(s0 + 2 * C::kTileBytes + h);
-              const uint64_t bh16 = sdesc_k_sw64(s0 + 3 * C::kTileBytes);
-              const uint64_t bl16 = sdesc_k_sw64(s0 + 3 * C::kTileBytes + h);
+              const uint32_t idesc16 = idesc_bf16(C::kUmmaM, C::kUmmaN) | idesc_major(ep.a_mn, ep.b_mn);
+              const uint64_t ahi = d32(s0, ep.a_mn);
+              const uint64_t bhi = d32(s0 + C::kTileBytes, ep.b_mn);
+              const uint64_t ah16 = d16(s0 + 2 * C::kTileBytes, ep.a_mn);
+              const uint64_t al16 = d16(s0 + 2 * C::kTileBytes + h, ep.a_mn);
+              const uint64_t bh16 = d16(s0 + 3 * C::kTileBytes, ep.b_mn);
+              const uint64_t bl16 = d16(s0 + 3 * C::kTileBytes + h, ep.b_mn);
 #pragma unroll
               for (int j = 0; j < C::kBK / 16; ++j) {
-                // bf16 cross terms for k16 step j (32 B along the 64-B row) ...
-                const uint64_t o16 = static_cast<uint64_t>(j * 2);
-                mma_bf16<CG>(d_tmem, ah16 + o16, bl16 + o16, idesc16, (acc0 | j) != 0);
-                mma_bf16<CG>(d_tmem, al16 + o16, bh16 + o16, idesc16, 1u);
+                // bf16 cross terms for k16 step j ...
+                const uint64_t oa = j * ia16, ob = j * ib16;
+                mma_bf16<CG>(d_tmem, ah16 + oa, bl16 + ob, idesc16, (acc0 | j) != 0);
+                mma_bf16<CG>(d_tmem, al16 + oa, bh16 + ob, idesc16, 1u);
                 // ... then hi*hi in tf32 for the same 16 k (two k8 MMAs)
-                mma_tf32<CG>(d_tmem, ahi + 4 * j, bhi + 4 * j, idesc, 1u);
-                mma_tf32<CG>(d_tmem, ahi + 4 * j + 2, bhi + 4 * j + 2, idesc, 1u);
+                mma_tf32<CG>(d_tmem, ahi + 2 * j * ia32, bhi + 2 * j * ib32, idesc, 1u);
+                mma_tf32<CG>(d_tmem, ahi + (2 * j + 1) * ia32, bhi + (2 * j + 1) * ib32, idesc, 1u);
               }
             }
             if constexpr (CG == 1) mma_commit(smem_u32(&empty_bar[stage]));
@@ -548,21 +568,25 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// K-major operand plane [rows x K] with row pitch `ld` elements; box 32 x 128
-// elements: fp32 with the 128-B swizzle, bf16 with the 64-B swizzle.
+// Operand plane of `rows` (M or N) x K elements.
+//   K-major  (mn == false): [rows x K], row pitch `ld`; box 32 k x 128 rows --
+//            fp32 with the 128-B swizzle, bf16 with the 64-B swizzle;
+//   MN-major (mn == true) : [K x rows], row pitch `ld` (along M/N); box
+//            128 B along M/N (32 fp32 / 64 bf16) x 32 k, 128-B swizzle.
+// Out-of-range elements (edges of M, N, K) are zero-filled by the TMA.
 int make_operand_map(CUtensorMap* map, const void* base, int64_t rows, int64_t k, int64_t ld,
-                     bool bf16) {
+                     bool bf16, bool mn) {
   EncodeTiledFn enc = encode_fn();
   if (enc == nullptr) return -1;
   const int esz = bf16 ? 2 : 4;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(mn ? rows : k), static_cast<cuuint64_t>(mn ? k : rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esz};
-  cuuint32_t box[2] = {32, 128};
+  cuuint32_t box[2] = {mn ? static_cast<cuuint32_t>(128 / esz) : 32u, mn ? 32u : 128u};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   (bf16 && !mn) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
@@ -621,18 +645,19 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   using C = Cfg<CG>;
   Maps maps;
   int bad = 0;
+  const bool amn = a.a_mn != 0, bmn = a.b_mn != 0;
   if constexpr (MODE == kModeTf32x3) {
-    bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false);
-    bad |= make_operand_map(&maps.m[1], a.a_lo, a.m, a.k, a.lda, false);
-    bad |= make_operand_map(&maps.m[2], a.b_hi, a.n, a.k, a.ldb, false);
-    bad |= make_operand_map(&maps.m[3], a.b_lo, a.n, a.k, a.ldb, false);
+    bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false, amn);
+    bad |= make_operand_map(&maps.m[1], a.a_lo, a.m, a.k, a.lda, false, amn);
+    bad |= make_operand_map(&maps.m[2], a.b_hi, a.n, a.k, a.ldb, false, bmn);
+    bad |= make_operand_map(&maps.m[3], a.b_lo, a.n, a.k, a.ldb, false, bmn);
   } else {
-    bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false);
-    bad |= make_operand_map(&maps.m[1], a.b_hi, a.n, a.k, a.ldb, false);
-    bad |= make_operand_map(&maps.m[2], a.a_hi16, a.m, a.k, a.lda16, true);
-    bad |= make_operand_map(&maps.m[3], a.a_lo16, a.m, a.k, a.lda16, true);
-    bad |= make_operand_map(&maps.m[4], a.b_hi16, a.n, a.k, a.ldb16, true);
-    bad |= make_operand_map(&maps.m[5], a.b_lo16, a.n, a.k, a.ldb16, true);
+    bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false, amn);
+    bad |= make_operand_map(&maps.m[1], a.b_hi, a.n, a.k, a.ldb, false, bmn);
+    bad |= make_operand_map(&maps.m[2], a.a_hi16, a.m, a.k, a.lda16, true, amn);
+    bad |= make_operand_map(&maps.m[3], a.a_lo16, a.m, a.k, a.lda16, true, amn);
+    bad |= make_operand_map(&maps.m[4], a.b_hi16, a.n, a.k, a.ldb16, true, bmn);
+    bad |= make_operand_map(&maps.m[5], a.b_lo16, a.n, a.k, a.ldb16, true, bmn);
   }
   if (bad) return cudaErrorInvalidValue;
   // per-device opt-in to > 48 KB dynamic smem (idempotent; atomic so concurrent
@@ -659,7 +684,8 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   if (units < 1) units = 1;
 
   EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
-               a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws};
+               a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws,
+               a.a_mn, a.b_mn};
   // lockstep keeps the CTAs of a wave together; with a single wave there is
   // nothing to align (and no counters to clear)
   if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1 && tiles > units) {
@@ -684,7 +710,8 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const int kc_blocks = a.flush_k > 0 ? static_cast<int>((a.flush_k + C::kBK - 1) / C::kBK) : 8;
+  const int64_t flush = a.flush_k > 0 ? a.flush_k : tf32x3_default_flush_k(a.mode, a.k_total > 0 ? a.k_total : a.k);
+  const int kc_blocks = static_cast<int>(std::max<int64_t>(1, (flush + C::kBK - 1) / C::kBK));
   SplitJobs sj;
   if (a.split != nullptr) sj = *a.split;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG, MODE>, maps, static_cast<int>(a.k),
@@ -712,6 +739,13 @@ cudaError_t stream_write_flag(cudaStream_t stream, unsigned* addr, unsigned valu
   if (fn == nullptr) return cudaErrorNotSupported;
   return fn(stream, reinterpret_cast<CUdeviceptr>(addr), value, 0) == CUDA_SUCCESS ? cudaSuccess
                                                                                     : cudaErrorUnknown;
+}
+
+int64_t tf32x3_default_flush_k(int mode, int64_t k_total) {
+  if (k_total <= 512) return 32;
+  if (k_total <= 2048) return 64;
+  if (mode == kModeTf32x3) return 128;  // 3xTF32: 128 runs as fast as 256
+  return k_total <= 8192 ? 128 : 256;
 }
 
 int64_t split_job_tiles(const SplitJob& j) {

@@ -47,8 +47,11 @@ int64_t split_job_tiles(const SplitJob& j);
 bool split_job_fusable(const SplitJob& j);
 
 // C[m x n] (row pitch ldc) <- alpha * A B^T + beta * C, where A and B are
-// given as K-major splits: A planes [m x k] (fp32 containers pitch lda, bf16
-// planes pitch lda16), B planes [n x k] (i.e. op(B) transposed).
+// given as split planes, each either K-major -- A [m x k], B [n x k] (i.e.
+// op(B) transposed), fp32 containers pitch lda/ldb, bf16 planes lda16/ldb16 --
+// or MN-major (a_mn / b_mn): A [k x m], B [k x n] with the pitches along m / n
+// (a multiple of 4 fp32 / 8 bf16 elements).  MN-major lets a transposed
+// operand be split without a transpose.
 // read_c == 0 means C is never read (reference rule: beta == 0 ignores C).
 struct Tf32x3Args {
   const float* a_hi = nullptr;   // tf32-rounded hi (fp32 container)
@@ -62,6 +65,7 @@ struct Tf32x3Args {
   const void* b_lo16 = nullptr;
   int64_t ldb = 0, ldb16 = 0;
   int mode = kModeTf32x3;
+  int a_mn = 0, b_mn = 0;  // planes MN-major instead of K-major
   float* c = nullptr;   // fp32 C, or fp16 C (reinterpreted) when c_half != 0
   int c_half = 0;       // Half16 storage: beta*C widened exactly, result rounded RNE once
   int64_t ldc = 0;
@@ -70,7 +74,8 @@ struct Tf32x3Args {
   int read_c = 0;
   int cta_group = 0;  // 0 = auto, 1 = single-CTA 128x128 tiles, 2 = CTA-pair 256x256 tiles
   int num_sms = 0;    // 0 = all SMs of the current device
-  int64_t flush_k = 0;  // K per TMEM accumulation chunk (0 = default 256)
+  int64_t flush_k = 0;  // K per TMEM accumulation chunk (0 = tf32x3_default_flush_k)
+  int64_t k_total = 0;  // K of the whole product when this launch is one K panel of it (0 = k)
   int group_m = 0;      // rasterisation group of m-tiles (0 = default)
   int l2_policy = 1;    // TMA L2 hint: 0 evict_normal, 1 evict_last, 2 evict_first
   int lockstep = 0;     // >0: producers stay within this many k-blocks of each other
@@ -83,6 +88,16 @@ struct Tf32x3Args {
 };
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);
+
+// Default TMEM accumulation chunk for a product over k_total.  The tensor
+// core adds each MMA into its fp32 accumulator with truncation, so a chunk's
+// error grows with the MMAs issued into it; chunks are folded into an fp32
+// register master with round-to-nearest adds.  Shorter chunks cost epilogue
+// time (measured at 16384^3, mixed: 256 -> 280, 128 -> 269, 64 -> 260
+// TFLOP/s), so they are used where the reference's own k-ascending fp32 loop
+// is most accurate (small K): the chunk keeps the split GEMM's error at or
+// below the reference's at every K (profiles/r02/flush_probe.log).
+int64_t tf32x3_default_flush_k(int mode, int64_t k_total);
 
 // Bytes of lockstep counters a launch with these arguments needs (0 if off).
 // Lockstep requires every CTA of the launch to be co-resident: do not enable it

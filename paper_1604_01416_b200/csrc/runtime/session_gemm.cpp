@@ -26,12 +26,18 @@ namespace dm {
 
 struct Session::GemmRun {
   // panel planes of one range and buffer: fp32 hi, and either fp32 lo
-  // (tf32x3) or bf16 hi + bf16 lo packed in one buffer (mixed); 8 B/element
+  // (tf32x3) or bf16 hi + bf16 lo packed in one buffer (mixed); 8 B/element.
+  // K-major [len x kpitch] when the range's pieces are stored row-wise along
+  // K; MN-major [kpitch x ld] (ld = len rounded to 32) when they are stored
+  // K-row-wise (a transposed A, a non-transposed B), so every split reads its
+  // source row by row and none transposes.
   struct Planes {
     float* hi;
     float* lo;
     void* hi16;
     void* lo16;
+    bool mn;
+    std::int64_t ld;  // pitch of every plane (elements)
   };
   // one split item per piece: effective source (the landing buffer for pieces
   // that crossed a link), target planes, and whether it waits on the flag
@@ -126,18 +132,31 @@ struct Session::GemmRun {
     seq.assign(np, 0);
   }
 
+  // MN-major planes for a range whose pieces are transposed (all pieces of a
+  // range come from one operand, so they share the flag)
+  static bool range_mn(const Range& r) {
+    if (env_int("DM_MN_MAJOR", 1) == 0) return false;
+    for (const auto& panel : r.panels)
+      for (const Piece& pc : panel) return pc.trans != 0;
+    return false;
+  }
+
   void alloc_planes(const std::vector<Range>& rs, std::vector<std::array<Planes, 2>>& out) {
     out.resize(rs.size());
-    for (std::size_t i = 0; i < rs.size(); ++i)
+    for (std::size_t i = 0; i < rs.size(); ++i) {
+      const bool mn = range_mn(rs[i]);
+      const std::int64_t len = std::max<std::int64_t>(rs[i].len, 1);
+      const std::int64_t ld = mn ? (len + 31) / 32 * 32 : kpitch;
+      const std::size_t elems = static_cast<std::size_t>(mn ? kpitch * ld : len * kpitch);
       for (int b = 0; b < nbuf; ++b) {
-        const std::size_t elems = static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1) * kpitch);
         bufs.push_back(w.pool->acquire(elems * 4));
         float* hi = bufs.back().f32();
         bufs.push_back(w.pool->acquire(elems * 4));
         char* second = static_cast<char*>(bufs.back().data());
-        out[i][b] = gemm_mode == kModeMixed ? Planes{hi, nullptr, second, second + elems * 2}
-                                            : Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr};
+        out[i][b] = gemm_mode == kModeMixed ? Planes{hi, nullptr, second, second + elems * 2, mn, ld}
+                                            : Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr, mn, ld};
       }
+    }
   }
 
   template <class F>
@@ -295,7 +314,20 @@ struct Session::GemmRun {
     if (trace) w.trace.push_back({"pull", p, pulled, 0.0, tp, S.trace_event(w.pull)});
   }
 
-  std::int64_t plane_off(const Item& it) const { return it.pc->dst_row * kpitch + it.pc->dst_k; }
+  std::int64_t plane_off(const Item& it) const {
+    return it.pl->mn ? it.pc->dst_k * it.pl->ld + it.pc->dst_row : it.pc->dst_row * it.pl->ld + it.pc->dst_k;
+  }
+  // split_tf32 shape of an item: x[r][q] = trans ? src[q * lds + r] : src[r * lds + q]
+  // lands at plane + r * ld + q; an MN-major plane stores op(X)^T, i.e. the
+  // piece with rows and columns swapped and the transpose flag flipped
+  struct SplitShape {
+    int trans;
+    std::int64_t rows, cols;
+  };
+  static SplitShape split_shape(const Item& it) {
+    const Piece& pc = *it.pc;
+    return it.pl->mn ? SplitShape{pc.trans ? 0 : 1, pc.kcols, pc.rows} : SplitShape{pc.trans, pc.rows, pc.kcols};
+  }
 
   // Split step s with its own kernels on the split stream.
   void split_separate(int s) {
@@ -315,10 +347,11 @@ struct Session::GemmRun {
       const Piece& pc = *it.pc;
       const Planes& pl = *it.pl;
       const std::int64_t off = plane_off(it);
-      cuda_check(split_tf32(it.src, half_in ? 1 : 0, it.lds, pc.trans, pc.rows, pc.kcols, pl.hi + off,
-                            pl.lo ? pl.lo + off : nullptr, kpitch,
+      const SplitShape sh = split_shape(it);
+      cuda_check(split_tf32(it.src, half_in ? 1 : 0, it.lds, sh.trans, sh.rows, sh.cols, pl.hi + off,
+                            pl.lo ? pl.lo + off : nullptr, pl.ld,
                             pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr,
-                            pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, kpitch, w.side),
+                            pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr, pl.ld, w.side),
                  "split_tf32");
       w.stats.split_launches += 1;
       bytes += pc.bytes() / 4 * esz;
@@ -348,21 +381,21 @@ struct Session::GemmRun {
     out->n = 0;
     std::int64_t t = 0;
     for (const Item& it : items[s]) {
-      const Piece& pc = *it.pc;
       const Planes& pl = *it.pl;
       const std::int64_t off = plane_off(it);
+      const SplitShape sh = split_shape(it);
       SplitJob& j = out->job[out->n++];
       j = SplitJob{};
       j.src = static_cast<const float*>(it.src);
       j.lds = it.lds;
-      j.trans = pc.trans;
-      j.rows = pc.rows;
-      j.kcols = pc.kcols;
+      j.trans = sh.trans;
+      j.rows = sh.rows;
+      j.kcols = sh.cols;
       j.hi = pl.hi + off;
       j.lo = pl.lo ? pl.lo + off : nullptr;
       j.hi16 = pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr;
       j.lo16 = pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr;
-      j.ldo = j.ldo16 = kpitch;
+      j.ldo = j.ldo16 = pl.ld;
       j.flag = it.landed ? flag : nullptr;
       j.flag_val = it.landed ? seq[s] : 0;
       j.t0 = t;
@@ -393,16 +426,18 @@ struct Session::GemmRun {
       const Planes& B = pb[t.rb][buf];
       Tf32x3Args a;
       a.mode = gemm_mode;
+      a.a_mn = A.mn ? 1 : 0;
+      a.b_mn = B.mn ? 1 : 0;
       a.a_hi = A.hi;
       a.a_lo = A.lo;
       a.a_hi16 = A.hi16;
       a.a_lo16 = A.lo16;
-      a.lda = a.lda16 = kpitch;
+      a.lda = a.lda16 = A.ld;
       a.b_hi = B.hi;
       a.b_lo = B.lo;
       a.b_hi16 = B.hi16;
       a.b_lo16 = B.lo16;
-      a.ldb = a.ldb16 = kpitch;
+      a.ldb = a.ldb16 = B.ld;
       a.c = cb.mem.f32();
       a.c_half = half_in ? 1 : 0;
       a.ldc = cb.cols;
@@ -416,6 +451,7 @@ struct Session::GemmRun {
       a.read_c = step == 0 ? (g.beta != 0.0 ? 1 : 0) : 1;
       a.cta_group = static_cast<int>(env_int("DM_CTA_GROUP", 0));
       a.flush_k = env_int("DM_FLUSH_K", 0);
+      a.k_total = plan.k0.back();  // the chunk length follows the whole product's K
       a.group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
       a.l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
       a.lockstep = lockstep;

@@ -133,12 +133,12 @@ def test_config2_16384_sampled_rows_and_columns(cuda, ref):
     assert res["gpu_vs_exact"] <= res["ref_vs_exact"], res  # no less accurate than the reference
 
 
-# GPU distance from exact <= RATIO x the reference's own + FLOOR (relFro):
-# the reference's fp32 k-ascending loop is ~2e-7 from exact at K=256 and
-# ~3e-6 at K=32768; the split GEMM's error is
-# K-independent (chunked TMEM accumulation): ~1e-6 for the
-# mixed split (bf16 cross terms), less for 3xTF32.
-RATIO = {"mixed": (1.0, 2.0e-6), "3xtf32": (1.0, 1.0e-6)}
+# GPU distance from exact <= RATIO x the reference's own + FLOOR (relFro).
+# The reference's fp32 k-ascending loop is ~2e-7 from exact at K=256 and
+# ~3e-6 at K=32768; the split GEMM's error is set by its
+# TMEM accumulation chunk, which the default shortens at small K
+# (tf32x3_default_flush_k) so that it stays near or below the reference's.
+RATIO = {"mixed": (1.5, 3e-7), "3xtf32": (1.5, 3e-7)}
 _REF_CACHE = {}
 
 
