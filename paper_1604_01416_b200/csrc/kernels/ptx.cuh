@@ -300,6 +300,20 @@ __device__ __forceinline__ uint64_t sdesc_mn_sw128(uint32_t smem_addr) {
   return d;
 }
 
+// MN-major 32-bit (tf32) operand: the only MN-major layout tcgen05 takes for
+// 32-bit sources is SWIZZLE_128B_BASE32B (layout type 1): 128-B rows along
+// M/N, 32-B chunks XOR-swizzled with the row index mod 4 (TMA swizzle
+// 128B_ATOM_32B), 4-k core groups 512 B apart (SBO), MN slices LBO apart.
+__device__ __forceinline__ uint64_t sdesc_mn_sw128_32b(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr & 0x3FFFFu) >> 4);  // start address [0,14)
+  d |= static_cast<uint64_t>(4096u >> 4) << 16;              // LBO [16,30): next MN slice
+  d |= static_cast<uint64_t>(512u >> 4) << 32;               // SBO [32,46): next 4-k group
+  d |= static_cast<uint64_t>(1u) << 46;                      // version = 1
+  d |= static_cast<uint64_t>(1u) << 61;                      // SWIZZLE_128B_BASE32B
+  return d;
+}
+
 // Operand-major bits of the instruction descriptor: bit 15 = A MN-major,
 // bit 16 = B MN-major (valid for tf32 and bf16 sources).
 __host__ __device__ constexpr uint32_t idesc_major(int a_mn, int b_mn) {

@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       // descriptor of an operand tile and its advance (16-B units) per k8
       // (fp32) / k16 (bf16) step: K-major moves 32 B along the swizzled row,
       // MN-major moves 8 (16) k rows = 1024 (2048) B
-      auto d32 = [](uint32_t a, int mn) { return mn ? sdesc_mn_sw128(a) : sdesc_k_sw128(a); };
+      auto d32 = [](uint32_t a, int mn) { return mn ? sdesc_mn_sw128_32b(a) : sdesc_k_sw128(a); };
       auto d16 = [](uint32_t a, int mn) { return mn ? sdesc_mn_sw128(a) : sdesc_k_sw64(a); };
       const uint64_t ia32 = ep.a_mn ? 64 : 2, ib32 = ep.b_mn ? 64 : 2;
       const uint64_t ia16 = ep.a_mn ? 128 : 2, ib16 = ep.b_mn ? 128 : 2;
@@ -572,7 +572,8 @@ EncodeTiledFn encode_fn() {
 //   K-major  (mn == false): [rows x K], row pitch `ld`; box 32 k x 128 rows --
 //            fp32 with the 128-B swizzle, bf16 with the 64-B swizzle;
 //   MN-major (mn == true) : [K x rows], row pitch `ld` (along M/N); box
-//            128 B along M/N (32 fp32 / 64 bf16) x 32 k, 128-B swizzle.
+//            128 B along M/N (32 fp32 / 64 bf16) x 32 k, 128-B swizzle (fp32:
+//            of 32-B atoms, the only MN-major 32-bit layout tcgen05 reads).
 // Out-of-range elements (edges of M, N, K) are zero-filled by the TMA.
 int make_operand_map(CUtensorMap* map, const void* base, int64_t rows, int64_t k, int64_t ld,
                      bool bf16, bool mn) {
@@ -586,7 +587,8 @@ int make_operand_map(CUtensorMap* map, const void* base, int64_t rows, int64_t k
   CUresult r = enc(map, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                    2, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   (bf16 && !mn) ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                   !mn ? (bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B)
+                       : (bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : -2;
 }
