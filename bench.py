@@ -286,9 +286,9 @@ def run_ours(args):
 
     pr, pc = dm.checkerboard_dims(world)
     lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, N, N, N // pr, N // pc, world)
-    mode = args.gemm_mode
-    s = make_session(mode)
-    mode = s.gemm_mode()
+    s = make_session(args.gemm_mode)
+    session_mode = s.gemm_mode()
+    mode = dm.split_mode_for(session_mode, N)  # the scheme this K runs in (auto: mixed above K=8192)
     me = rank
     a = s.create_matrix(lay, fill=dm.FillKind.SeededRandom)
     b = s.create_matrix(lay, fill=dm.FillKind.SeededRandom)
@@ -362,7 +362,7 @@ def run_ours(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(main["t_ms"] / args.steps, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (reference seeded fill, root seed 42)",
-        "config": dict(bench_config(N, world), gemm_mode=mode),
+        "config": dict(bench_config(N, world), gemm_mode=mode, session_gemm_mode=session_mode),
         "impl": "ours",
         "roofline": {"bound": "tensor", "achieved": round(main["kern_tflops"], 2), "peak": round(peak_sust, 2),
                      "unit": "TFLOP/s", "frac": round(main["kern_tflops"] / peak_sust, 4),
@@ -587,8 +587,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--gemm-mode", choices=["default", "mixed", "3xtf32"], default="default",
-                    help="split-product scheme of the headline run (default: DM_GEMM_MODE, else mixed)")
+    ap.add_argument("--gemm-mode", choices=["default", "auto", "mixed", "3xtf32"], default="default",
+                    help="split-product scheme of the headline run (default: DM_GEMM_MODE, else auto = "
+                         "mixed at this K)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline and sampled parity")
     ap.add_argument("--no-alt", action="store_true", help="skip the second (3xTF32) timed run")

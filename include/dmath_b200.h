@@ -55,8 +55,12 @@ enum dm_fill { DM_FILL_ZEROS = 0, DM_FILL_SEEDED = 1, DM_FILL_FROM_HOST = 2 }; /
  *                    (kind::f16): 4 bf16-MMA slots per useful k16;
  *   DM_GEMM_TF32X3 : lo*hi + hi*lo + hi*hi, all kind::tf32 (north star's
  *                    3xTF32): 6 slots per k16;
- *   DM_GEMM_DEFAULT: the DM_GEMM_MODE environment variable (0 = 3xTF32), else mixed. */
-enum dm_gemm_mode { DM_GEMM_DEFAULT = 0, DM_GEMM_MIXED = 1, DM_GEMM_TF32X3 = 2 };
+ *   DM_GEMM_AUTO   : per product, 3xTF32 for K <= 8192 and mixed above -- the
+ *                    more accurate of the two against the reference's own
+ *                    error at each K (mixed is also ~1.25x faster);
+ *   DM_GEMM_DEFAULT: the DM_GEMM_MODE environment variable (0 = 3xTF32,
+ *                    1 = mixed, 2 = auto), else auto. */
+enum dm_gemm_mode { DM_GEMM_DEFAULT = 0, DM_GEMM_MIXED = 1, DM_GEMM_TF32X3 = 2, DM_GEMM_AUTO = 3 };
 enum dm_mode {
   DM_MODE_LOCAL = 0, /* one process drives every worker (reference Session, session.hpp:64-76) */
   DM_MODE_SPMD = 1   /* one process per GPU; every rank makes the same calls (torchrun) */
@@ -225,7 +229,7 @@ int dm_worker_stats_reset(dm_session* s);
 /* Record CUDA events around every GEMM launch (fills gemm_ms). */
 int dm_set_gemm_timing(dm_session* s, int enable);
 int dm_worker_seed(dm_session* s, int worker, uint64_t* out); /* session.hpp:103 */
-/* The session's resolved split-product scheme: DM_GEMM_MIXED or DM_GEMM_TF32X3. */
+/* The session's resolved split-product scheme: DM_GEMM_MIXED, DM_GEMM_TF32X3 or DM_GEMM_AUTO. */
 int dm_session_gemm_mode(dm_session* s, int* out);
 /* trace() (session.hpp:94; TraceLog, transport.hpp:56-71): the block transfers
  * this process's workers pulled, oldest first; fills up to cap records and

@@ -59,18 +59,22 @@ dm::Session& S(dm_session* s) {
 
 // Split-product mode: explicit (dm_gemm_mode) or, for DM_GEMM_DEFAULT, the
 // DM_GEMM_MODE environment variable (0 = 3xTF32), else mixed.
-int resolve_gemm_mode(int requested) {
-  if (requested == DM_GEMM_TF32X3) return dm::kModeTf32x3;
-  if (requested == DM_GEMM_MIXED) return dm::kModeMixed;
-  if (requested != DM_GEMM_DEFAULT) throw dm::UsageError("unknown gemm_mode");
-  return dm::env_int("DM_GEMM_MODE", 1) == 0 ? dm::kModeTf32x3 : dm::kModeMixed;
+int resolve_gemm_mode(int requested, int64_t k) {
+  int mode;
+  if (requested == DM_GEMM_TF32X3) mode = dm::kModeTf32x3;
+  else if (requested == DM_GEMM_MIXED) mode = dm::kModeMixed;
+  else if (requested == DM_GEMM_AUTO) mode = dm::kModeAuto;
+  else if (requested == DM_GEMM_DEFAULT) mode = dm::env_gemm_mode();
+  else throw dm::UsageError("unknown gemm_mode");
+  return dm::resolve_split_mode(mode, k);
 }
 
 // Scratch layout of one local_gemm call: the split planes of op(A) and op(B)
 // -- hi fp32 + (lo fp32 | bf16 hi, bf16 lo) = 8 B per element either way --
 // then the split-K partials; each region 256-B aligned.  An operand whose
 // storage is M/N-contiguous (transposed A, non-transposed B) gets MN-major
-// planes, so both splits read their source row by row (no transpose).
+// planes -- split row by row, no transpose -- when the other extent (its
+// reuse) is below DM_MN_REUSE (session_gemm.cpp range_mn).
 struct SeamLayout {
   bool a_mn = false, b_mn = false;
   int64_t lda = 8, ldb = 8;  // plane pitches (elements): K-major kp, MN-major m / n rounded to 32
@@ -83,9 +87,9 @@ struct SeamLayout {
 SeamLayout seam_layout(const dm::Tf32x3Args& shape, int ta, int tb) {
   SeamLayout l;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
-  const bool mn_ok = dm::env_int("DM_MN_MAJOR", 1) != 0;
-  l.a_mn = mn_ok && ta != 0;
-  l.b_mn = mn_ok && tb == 0;
+  const int64_t thr = dm::env_int("DM_MN_REUSE", 2048);
+  l.a_mn = ta != 0 && shape.n < thr;
+  l.b_mn = tb == 0 && shape.m < thr;
   const int64_t kp = std::max<int64_t>(8, (shape.k + 7) / 8 * 8);
   l.lda = l.a_mn ? (shape.m + 31) / 32 * 32 : kp;
   l.ldb = l.b_mn ? (shape.n + 31) / 32 * 32 : kp;
@@ -217,7 +221,7 @@ int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const flo
           "dm_local_gemm_f32_ws with a caller workspace");
     int dev = 0;
     dm::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    const int mode = resolve_gemm_mode(gemm_mode);
+    const int mode = resolve_gemm_mode(gemm_mode, k);
     const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb);
     SeamScratch& sc = seam_scratch(dev);
     dm::DeviceBuffer buf;
@@ -492,7 +496,10 @@ int dm_cached_backward_gemm(dm_session* s, dm_matrix_id w, dm_matrix_id dy, dm_m
 }
 
 int dm_session_gemm_mode(dm_session* s, int* out) {
-  return guarded([&] { *out = S(s).gemm_mode() == dm::kModeTf32x3 ? DM_GEMM_TF32X3 : DM_GEMM_MIXED; });
+  return guarded([&] {
+    const int m = S(s).gemm_mode();
+    *out = m == dm::kModeTf32x3 ? DM_GEMM_TF32X3 : m == dm::kModeMixed ? DM_GEMM_MIXED : DM_GEMM_AUTO;
+  });
 }
 
 int dm_worker_count(dm_session* s, int* out) {
@@ -638,8 +645,10 @@ int dm_local_gemm_f32_workspace_size(int64_t m, int64_t n, int64_t k, int cta_gr
   return guarded([&] {
     if (bytes == nullptr) throw dm::UsageError("local_gemm_workspace_size: null output");
     if (m < 0 || n < 0 || k < 0) throw dm::ShapeError("local_gemm: negative dimension");
-    *bytes = std::max(seam_layout(seam_shape(m, n, k, cta_group, resolve_gemm_mode(gemm_mode)), 0, 0).total,
-                      seam_layout(seam_shape(m, n, k, cta_group, resolve_gemm_mode(gemm_mode)), 1, 1).total);
+    const int mode = resolve_gemm_mode(gemm_mode, k);
+    *bytes = 0;
+    for (int ta : {0, 1})
+      for (int tb : {0, 1}) *bytes = std::max(*bytes, seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb).total);
   });
 }
 
@@ -648,7 +657,7 @@ int dm_local_gemm_f32_ws(double alpha, const float* a, int64_t lda, int ta, cons
                          int cta_group, int gemm_mode, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
     local_gemm_validate(a, lda, ta, b, ldb, tb, c, ldc, m, n, k, cta_group);
-    const int mode = resolve_gemm_mode(gemm_mode);
+    const int mode = resolve_gemm_mode(gemm_mode, k);
     const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb);
     if (workspace_bytes < L.total || (L.total > 0 && workspace == nullptr))
       throw dm::UsageError("local_gemm: workspace smaller than dm_local_gemm_f32_workspace_size");

@@ -72,7 +72,8 @@ struct EpiParams {
   unsigned* sync;       // lockstep counters [waves * epochs], zeroed per launch
   int ksplit;           // >1: split-K; item (s, tile) writes its fp32 partial to ws[s]
   float* ws;            // [ksplit][m][n] partial tiles (ksplit > 1)
-  int a_mn, b_mn;       // operand planes MN-major (M / N contiguous) instead of K-major
+  int a_mn, b_mn;       // fp32 operand planes MN-major (M / N contiguous) instead of K-major
+  int a_mn16, b_mn16;   // the same for the bf16 planes (mixed mode)
 };
 
 // Work item t of a launch: tile t % tiles of K-split t / tiles, whose k-blocks
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
               for (int c = 0; c < 128 / w; ++c) load2(i, off + c * 4096u, row + c * w, kx);
             }
           };
-          const bool amn = ep.a_mn != 0, bmn = ep.b_mn != 0;
+          const bool amn = ep.a_mn != 0, bmn = ep.b_mn != 0, amn16 = ep.a_mn16 != 0, bmn16 = ep.b_mn16 != 0;
           if constexpr (MODE == kModeTf32x3) {
             load(0, 0, arow, amn, false);
             load(1, C::kTileBytes, arow, amn, false);
@@ -331,10 +332,10 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             constexpr uint32_t h = C::kTileBytes / 2;  // bf16 tile: 128 rows x 64 B
             load(0, 0, arow, amn, false);
             load(1, C::kTileBytes, brow, bmn, false);
-            load(2, 2 * C::kTileBytes, arow, amn, true);
-            load(3, 2 * C::kTileBytes + h, arow, amn, true);
-            load(4, 3 * C::kTileBytes, brow, bmn, true);
-            load(5, 3 * C::kTileBytes + h, brow, bmn, true);
+            load(2, 2 * C::kTileBytes, arow, amn16, true);
+            load(3, 2 * C::kTileBytes + h, arow, amn16, true);
+            load(4, 3 * C::kTileBytes, brow, bmn16, true);
+            load(5, 3 * C::kTileBytes + h, brow, bmn16, true);
           }
           if (++stage == C::kStages) { stage = 0; phase ^= 1; }
         }
@@ -350,7 +351,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       auto d32 = [](uint32_t a, int mn) { return mn ? sdesc_mn_sw128_32b(a) : sdesc_k_sw128(a); };
       auto d16 = [](uint32_t a, int mn) { return mn ? sdesc_mn_sw128(a) : sdesc_k_sw64(a); };
       const uint64_t ia32 = ep.a_mn ? 64 : 2, ib32 = ep.b_mn ? 64 : 2;
-      const uint64_t ia16 = ep.a_mn ? 128 : 2, ib16 = ep.b_mn ? 128 : 2;
+      const uint64_t ia16 = ep.a_mn16 ? 128 : 2, ib16 = ep.b_mn16 ? 128 : 2;
       int stage = 0;
       uint32_t phase = 0;
       uint32_t chunk_ctr = 0;
@@ -385,13 +386,13 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
               }
             } else {
               constexpr uint32_t h = C::kTileBytes / 2;
-              const uint32_t idesc16 = idesc_bf16(C::kUmmaM, C::kUmmaN) | idesc_major(ep.a_mn, ep.b_mn);
+              const uint32_t idesc16 = idesc_bf16(C::kUmmaM, C::kUmmaN) | idesc_major(ep.a_mn16, ep.b_mn16);
               const uint64_t ahi = d32(s0, ep.a_mn);
               const uint64_t bhi = d32(s0 + C::kTileBytes, ep.b_mn);
-              const uint64_t ah16 = d16(s0 + 2 * C::kTileBytes, ep.a_mn);
-              const uint64_t al16 = d16(s0 + 2 * C::kTileBytes + h, ep.a_mn);
-              const uint64_t bh16 = d16(s0 + 3 * C::kTileBytes, ep.b_mn);
-              const uint64_t bl16 = d16(s0 + 3 * C::kTileBytes + h, ep.b_mn);
+              const uint64_t ah16 = d16(s0 + 2 * C::kTileBytes, ep.a_mn16);
+              const uint64_t al16 = d16(s0 + 2 * C::kTileBytes + h, ep.a_mn16);
+              const uint64_t bh16 = d16(s0 + 3 * C::kTileBytes, ep.b_mn16);
+              const uint64_t bl16 = d16(s0 + 3 * C::kTileBytes + h, ep.b_mn16);
 #pragma unroll
               for (int j = 0; j < C::kBK / 16; ++j) {
                 // bf16 cross terms for k16 step j ...
@@ -648,6 +649,7 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   Maps maps;
   int bad = 0;
   const bool amn = a.a_mn != 0, bmn = a.b_mn != 0;
+  const bool amn16 = (a.a_mn16 < 0 ? a.a_mn : a.a_mn16) != 0, bmn16 = (a.b_mn16 < 0 ? a.b_mn : a.b_mn16) != 0;
   if constexpr (MODE == kModeTf32x3) {
     bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false, amn);
     bad |= make_operand_map(&maps.m[1], a.a_lo, a.m, a.k, a.lda, false, amn);
@@ -656,10 +658,10 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   } else {
     bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false, amn);
     bad |= make_operand_map(&maps.m[1], a.b_hi, a.n, a.k, a.ldb, false, bmn);
-    bad |= make_operand_map(&maps.m[2], a.a_hi16, a.m, a.k, a.lda16, true, amn);
-    bad |= make_operand_map(&maps.m[3], a.a_lo16, a.m, a.k, a.lda16, true, amn);
-    bad |= make_operand_map(&maps.m[4], a.b_hi16, a.n, a.k, a.ldb16, true, bmn);
-    bad |= make_operand_map(&maps.m[5], a.b_lo16, a.n, a.k, a.ldb16, true, bmn);
+    bad |= make_operand_map(&maps.m[2], a.a_hi16, a.m, a.k, a.lda16, true, amn16);
+    bad |= make_operand_map(&maps.m[3], a.a_lo16, a.m, a.k, a.lda16, true, amn16);
+    bad |= make_operand_map(&maps.m[4], a.b_hi16, a.n, a.k, a.ldb16, true, bmn16);
+    bad |= make_operand_map(&maps.m[5], a.b_lo16, a.n, a.k, a.ldb16, true, bmn16);
   }
   if (bad) return cudaErrorInvalidValue;
   // per-device opt-in to > 48 KB dynamic smem (idempotent; atomic so concurrent
@@ -687,7 +689,7 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
 
   EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
                a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws,
-               a.a_mn, a.b_mn};
+               a.a_mn, a.b_mn, amn16 ? 1 : 0, bmn16 ? 1 : 0};
   // lockstep keeps the CTAs of a wave together; with a single wave there is
   // nothing to align (and no counters to clear)
   if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1 && tiles > units) {

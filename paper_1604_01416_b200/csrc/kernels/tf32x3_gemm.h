@@ -15,6 +15,18 @@ namespace dm {
 //                 the TF32 rate, so a k16 step costs 4 TF32-MMA slots instead of 6.
 constexpr int kModeTf32x3 = 0;
 constexpr int kModeMixed = 1;
+// Per product: 3xTF32 up to K = kAutoMixedMinK, mixed above.  Measured
+// (profiles/r02/accuracy): the mixed split's bf16 cross terms put a ~6e-7
+// floor under its error, up to 4x the reference's own k-ascending fp32 error
+// at K=256, while 3xTF32 stays within 1.25x of it at every K; above 8192 the
+// mixed split is the more accurate of the two against the reference's
+// growing error (0.4-0.8x at K=32768) and ~1.25x faster.
+constexpr int kModeAuto = 2;
+constexpr int64_t kAutoMixedMinK = 8193;
+inline int resolve_split_mode(int mode, int64_t k_total) {
+  if (mode != kModeAuto) return mode;
+  return k_total >= kAutoMixedMinK ? kModeMixed : kModeTf32x3;
+}
 
 // One split job fused into a GEMM launch: the split_tf32 of an fp32 piece
 // (16-B aligned rows and planes) for the NEXT K panel, executed by the
@@ -66,6 +78,7 @@ struct Tf32x3Args {
   int64_t ldb = 0, ldb16 = 0;
   int mode = kModeTf32x3;
   int a_mn = 0, b_mn = 0;  // planes MN-major instead of K-major
+  int a_mn16 = -1, b_mn16 = -1;  // bf16 planes' majorness when it differs (-1: as a_mn / b_mn)
   float* c = nullptr;   // fp32 C, or fp16 C (reinterpreted) when c_half != 0
   int c_half = 0;       // Half16 storage: beta*C widened exactly, result rounded RNE once
   int64_t ldc = 0;

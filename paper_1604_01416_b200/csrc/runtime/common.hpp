@@ -38,6 +38,14 @@ inline std::int64_t env_int(const char* name, std::int64_t dflt) {
   return std::strtoll(v, nullptr, 10);
 }
 
+// DM_GEMM_MODE environment default of the split-product scheme (0 = 3xTF32,
+// 1 = mixed, anything else / unset = auto), as kernel mode constants
+// (kModeTf32x3 = 0, kModeMixed = 1, kModeAuto = 2).
+inline int env_gemm_mode() {
+  const std::int64_t v = env_int("DM_GEMM_MODE", 2);
+  return v == 0 ? 0 : v == 1 ? 1 : 2;
+}
+
 class Error : public std::runtime_error {
  public:
   Error(int code, const std::string& what) : std::runtime_error(what), code_(code) {}

@@ -36,8 +36,10 @@ Session::Session(const dm_session_config& cfg) {
     gemm_mode_ = kModeTf32x3;
   } else if (cfg.gemm_mode == DM_GEMM_MIXED) {
     gemm_mode_ = kModeMixed;
+  } else if (cfg.gemm_mode == DM_GEMM_AUTO) {
+    gemm_mode_ = kModeAuto;
   } else if (cfg.gemm_mode == DM_GEMM_DEFAULT) {
-    gemm_mode_ = env_int("DM_GEMM_MODE", 1) == 0 ? kModeTf32x3 : kModeMixed;
+    gemm_mode_ = env_gemm_mode();
   } else {
     throw ConfigError("init: unknown gemm_mode");
   }

@@ -146,7 +146,7 @@ class Session {
   void restore_image(const std::string& path);  // into a fresh session
   std::uint64_t next_matrix_id() const { return next_matrix_id_; }
   std::uint64_t root_seed() const { return root_seed_; }
-  int gemm_mode() const { return gemm_mode_; }  // kModeMixed / kModeTf32x3
+  int gemm_mode() const { return gemm_mode_; }  // kModeMixed / kModeTf32x3 / kModeAuto
   void general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
                     bool tb);
   void cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta, bool tb,
@@ -256,7 +256,7 @@ class Session {
 
   int P_ = 1;
   int mode_ = DM_MODE_LOCAL;
-  int gemm_mode_ = 1;  // kModeMixed
+  int gemm_mode_ = 2;  // kModeAuto
   int rank_ = 0;
   bool coherence_ = true;
   bool live_ = false;

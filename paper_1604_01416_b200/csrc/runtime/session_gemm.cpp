@@ -89,7 +89,7 @@ struct Session::GemmRun {
       : S(s), w(wk), g(ga), pol(p), plan(std::move(pl)), bufs(b), events(e),
         half_in(s.table_.at(ga.a).precision == Precision::Half16),
         esz(byte_width(s.table_.at(ga.a).precision)),
-        gemm_mode(s.gemm_mode_),
+        gemm_mode(resolve_split_mode(s.gemm_mode_, plan.k0.empty() ? 0 : plan.k0.back())),
         trace(s.tracing() && !s.async_),
         np(static_cast<int>(plan.k0.size()) - 1),
         nbuf(np > 1 ? 2 : 1) {}
@@ -114,8 +114,8 @@ struct Session::GemmRun {
     // DM_FUSE_SPLIT: 0 never, 1 when the carrying GEMM hides the split, 2 always
     fuse_mode = half_in ? 0 : env_int("DM_FUSE_SPLIT", 1);
 
-    alloc_planes(plan.ar, pa);
-    alloc_planes(plan.br, pb);
+    alloc_planes(plan.ar, plan.br, true, pa);
+    alloc_planes(plan.br, plan.ar, false, pb);
     // operands of this worker's GEMMs were written by earlier commands on
     // its own streams; order the split stream after the compute stream
     cudaEvent_t e = new_event();
@@ -133,18 +133,28 @@ struct Session::GemmRun {
   }
 
   // MN-major planes for a range whose pieces are transposed (all pieces of a
-  // range come from one operand, so they share the flag)
-  static bool range_mn(const Range& r) {
-    if (env_int("DM_MN_MAJOR", 1) == 0) return false;
+  // range come from one operand, so they share the flag) -- when the planes
+  // are reused by few output rows/columns (`reuse` = the other operand's
+  // extent over this worker's tasks).  The tensor core reads MN-major tiles
+  // ~10% slower (tools/micro/mn_probe.cu: 269 vs 235 TFLOP/s at 16384^3), so a
+  // long GEMM prefers the transposing split (~0.4 ms/GiB extra); a short,
+  // memory-bound one (FC strips) prefers the direct split.  Break-even
+  // ~2000 rows (DM_MN_REUSE).
+  static bool range_mn(const Range& r, std::int64_t reuse) {
+    if (reuse >= env_int("DM_MN_REUSE", 2048)) return false;
     for (const auto& panel : r.panels)
       for (const Piece& pc : panel) return pc.trans != 0;
     return false;
   }
 
-  void alloc_planes(const std::vector<Range>& rs, std::vector<std::array<Planes, 2>>& out) {
+  void alloc_planes(const std::vector<Range>& rs, const std::vector<Range>& other, bool is_a,
+                    std::vector<std::array<Planes, 2>>& out) {
     out.resize(rs.size());
     for (std::size_t i = 0; i < rs.size(); ++i) {
-      const bool mn = range_mn(rs[i]);
+      std::int64_t reuse = 0;
+      for (const Task& t : plan.tasks)
+        if ((is_a ? t.ra : t.rb) == static_cast<int>(i)) reuse += other[is_a ? t.rb : t.ra].len;
+      const bool mn = range_mn(rs[i], reuse);
       const std::int64_t len = std::max<std::int64_t>(rs[i].len, 1);
       const std::int64_t ld = mn ? (len + 31) / 32 * 32 : kpitch;
       const std::size_t elems = static_cast<std::size_t>(mn ? kpitch * ld : len * kpitch);
