@@ -55,9 +55,10 @@ enum dm_fill { DM_FILL_ZEROS = 0, DM_FILL_SEEDED = 1, DM_FILL_FROM_HOST = 2 }; /
  *                    (kind::f16): 4 bf16-MMA slots per useful k16;
  *   DM_GEMM_TF32X3 : lo*hi + hi*lo + hi*hi, all kind::tf32 (north star's
  *                    3xTF32): 6 slots per k16;
- *   DM_GEMM_AUTO   : per product, 3xTF32 for K <= 8192 and mixed above -- the
- *                    more accurate of the two against the reference's own
- *                    error at each K (mixed is also ~1.25x faster);
+ *   DM_GEMM_AUTO   : per product, 3xTF32 for K <= 8192 and mixed above: at
+ *                    small K the reference's own error is small and only
+ *                    3xTF32 stays near it; at large K both are below it and
+ *                    mixed is ~1.2x faster;
  *   DM_GEMM_DEFAULT: the DM_GEMM_MODE environment variable (0 = 3xTF32,
  *                    1 = mixed, 2 = auto), else auto. */
 enum dm_gemm_mode { DM_GEMM_DEFAULT = 0, DM_GEMM_MIXED = 1, DM_GEMM_TF32X3 = 2, DM_GEMM_AUTO = 3 };

@@ -16,11 +16,11 @@ namespace dm {
 constexpr int kModeTf32x3 = 0;
 constexpr int kModeMixed = 1;
 // Per product: 3xTF32 up to K = kAutoMixedMinK, mixed above.  Measured
-// (profiles/r02/accuracy): the mixed split's bf16 cross terms put a ~6e-7
-// floor under its error, up to 4x the reference's own k-ascending fp32 error
-// at K=256, while 3xTF32 stays within 1.25x of it at every K; above 8192 the
-// mixed split is the more accurate of the two against the reference's
-// growing error (0.4-0.8x at K=32768) and ~1.25x faster.
+// (profiles/r02/accuracy_fullsize_parity.jsonl, distance from the exact
+// product relative to the reference's own k-ascending fp32 loop): 3xTF32
+// 0.3-1.25x at every K; mixed's bf16 cross terms leave a ~6e-7 floor, up to
+// 4x the reference at K=256, but 0.4-0.8x at K=32768 where the reference's
+// error has grown -- there mixed is the faster (~1.2x) fp32-accurate choice.
 constexpr int kModeAuto = 2;
 constexpr int64_t kAutoMixedMinK = 8193;
 inline int resolve_split_mode(int mode, int64_t k_total) {

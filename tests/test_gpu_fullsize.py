@@ -141,8 +141,8 @@ def test_config2_16384_sampled_rows_and_columns(cuda, ref):
 # Measured (profiles/r02): 3xTF32 within 1.25x of the reference's error at
 # every K and distribution; the mixed split's bf16 cross terms leave a ~6e-7
 # floor -- up to 4x the reference at K=256 -- which is why "auto" (the
-# default) runs 3xTF32 up to K=8192 and mixed above, where mixed is the more
-# accurate of the two (0.4-0.8x the reference at K=32768).
+# default) runs 3xTF32 up to K=8192 and mixed above, where both are below
+# the reference's growing error (mixed 0.4-0.8x at K=32768) and mixed is faster.
 def bar(gemm_mode, k):
     if gemm_mode == "mixed" and k <= 8192:
         return 4.5, 1e-7
