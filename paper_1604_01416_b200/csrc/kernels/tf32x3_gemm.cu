@@ -31,6 +31,7 @@
 #include <atomic>
 #include <cstdio>
 
+#include "../runtime/common.hpp"
 #include "ptx.cuh"
 #include "split_common.cuh"
 #include "tf32x3_gemm.h"
@@ -646,6 +647,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int m,
 template <int CG, int MODE>
 cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   using C = Cfg<CG>;
+  HostScope hs("tf32x3_gemm launch (host)");
   Maps maps;
   int bad = 0;
   const bool amn = a.a_mn != 0, bmn = a.b_mn != 0;

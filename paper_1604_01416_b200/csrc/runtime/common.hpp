@@ -8,8 +8,13 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -37,6 +42,51 @@ inline std::int64_t env_int(const char* name, std::int64_t dflt) {
   if (v == nullptr || *v == 0) return dflt;
   return std::strtoll(v, nullptr, 10);
 }
+
+// Host-side phase timer (DM_HOST_PROF=1): accumulated wall time per named
+// phase of the command path, printed to stderr at exit.  Diagnostic only.
+struct HostProf {
+  struct Acc {
+    double us = 0;
+    long n = 0;
+  };
+  std::map<std::string, Acc> acc;
+  std::mutex mu;
+  static HostProf& get() {
+    static HostProf* p = new HostProf();  // leaked on purpose: printed from atexit
+    return *p;
+  }
+  static bool on() {
+    static const bool v = env_int("DM_HOST_PROF", 0) != 0;
+    return v;
+  }
+  ~HostProf() = default;
+};
+inline void host_prof_dump() {
+  HostProf& h = HostProf::get();
+  std::lock_guard<std::mutex> lk(h.mu);
+  for (const auto& [k, a] : h.acc)
+    std::fprintf(stderr, "[host-prof] %-28s %10.2f us/call  (%ld calls)\n", k.c_str(), a.us / std::max(1L, a.n), a.n);
+}
+struct HostScope {
+  const char* name;
+  std::chrono::steady_clock::time_point t0;
+  explicit HostScope(const char* n) : name(n) {
+    if (HostProf::on()) t0 = std::chrono::steady_clock::now();
+  }
+  ~HostScope() {
+    if (!HostProf::on()) return;
+    const double us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    HostProf& h = HostProf::get();
+    static bool registered = [] { return std::atexit(host_prof_dump) == 0; }();
+    (void)registered;
+    std::lock_guard<std::mutex> lk(h.mu);
+    auto& a = h.acc[name];
+    a.us += us;
+    a.n += 1;
+  }
+};
 
 // DM_GEMM_MODE environment default of the split-product scheme (0 = 3xTF32,
 // 1 = mixed, anything else / unset = auto), as kernel mode constants

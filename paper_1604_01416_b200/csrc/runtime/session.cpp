@@ -319,6 +319,7 @@ void Session::set_async(bool on) {
 
 void Session::end_command() {
   if (async_) return;  // stream-ordered; completed by barrier()/drain()
+  HostScope hs("end_command");
   sync_local();
   collect_timing();
   if (comm_) {
@@ -920,6 +921,7 @@ void Session::cache_foreign_a(const GemmArgs& g) {
 
 void Session::general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,
                            bool tb) {
+  HostScope hs("general_gemm (total)");
   require_live();
   op_tag_ = "general_gemm";
   GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, false);

@@ -589,7 +589,11 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     if (!wp) continue;
     Worker& w = *wp;
     DeviceGuard guard(w.device);
-    WorkerPlan plan = plan_worker(g, w.id, pol);
+    WorkerPlan plan;
+    {
+      HostScope hp("run_gemm: plan_worker");
+      plan = plan_worker(g, w.id, pol);
+    }
     if (async_) {
       // pulls start once A and B are written everywhere; C is overwritten only
       // after its previous writes and reads (e.g. an async gather) finished
@@ -607,7 +611,10 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     if (plan.tasks.empty()) continue;
     Live& lv = live[w.id];
     if (tracing() && !async_) w.trace_t0 = trace_event(w.stream);
-    GemmRun(*this, w, g, pol, std::move(plan), lv.bufs, lv.events).run();
+    {
+      HostScope hr("run_gemm: GemmRun");
+      GemmRun(*this, w, g, pol, std::move(plan), lv.bufs, lv.events).run();
+    }
     if (async_) {
       mark_write(w, w.stream, g.c);
       // A and B are read by the split stream and by the GEMMs' fused split warps
@@ -630,6 +637,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   // waits, or the landing flag the GEMM's split warps spin on), so that
   // stream draining means the command's buffers are free; end_command()
   // synchronises the remaining streams.
+  HostScope hsync("run_gemm: sync + release");
   for (auto& wp : workers_) {
     if (!wp) continue;
     DeviceGuard guard(wp->device);
