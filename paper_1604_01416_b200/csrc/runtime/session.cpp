@@ -110,6 +110,7 @@ Session::~Session() {
     }
     for (cudaEvent_t e : w->markers)
       if (e) cudaEventDestroy(e);
+    drop_graphs(*w, 0);
     w->owned.clear();
     w->cache.clear();
     w->replicas.clear();
@@ -141,6 +142,8 @@ void Session::shutdown() {
   arena_bytes_ = 0;
   for (auto& w : workers_) {
     if (!w) continue;
+    DeviceGuard g(w->device);
+    drop_graphs(*w, 0);
     w->owned.clear();
     w->cache.clear();
     w->replicas.clear();
@@ -439,6 +442,10 @@ void Session::destroy_matrix(MatrixId id) {
   }
   for (auto& w : workers_) {
     if (!w) continue;
+    {
+      DeviceGuard g(w->device);
+      drop_graphs(*w, id);
+    }
     for (auto* m : {&w->owned, &w->cache, &w->replicas}) {
       auto it = m->lower_bound({id, {0, 0}});
       while (it != m->end() && it->first.matrix == id) it = m->erase(it);
@@ -938,6 +945,7 @@ void Session::cyclic_gemm(double alpha, MatrixId a, MatrixId b, double beta, Mat
   SyncScope scope(this);
   op_tag_ = "cyclic_gemm";
   GemmArgs g = gemm_command(alpha, a, b, beta, c, ta, tb, cache_a);
+  g.plane_cache_a = cache_a;  // the FC weight: keep its split planes while its version holds
   validate_cyclic(g, nullptr);
   if (cache_a) {
     // Keep what you've seen (CyclicGemmExec::finish, ops.hpp:278-289): fill the
@@ -992,6 +1000,7 @@ void Session::cached_backward_gemm(MatrixId w_id, MatrixId dy, MatrixId dx) {
   if (!missing.empty())
     throw CacheMissError("cached_backward_gemm: blocks not cached at the current version",
                          {missing.begin(), missing.end()});
+  g.plane_cache_a = true;  // W's split planes serve every backward until W changes
   run_gemm(g, SourcePolicy::LocalOnly);
   bump_version(dx);
   end_command();

@@ -67,6 +67,9 @@ struct GemmArgs {
   double alpha = 1.0, beta = 0.0;
   MatrixId a = 0, b = 0, c = 0;
   bool trans_a = false, trans_b = false, cache_a = false;
+  // keep op(A)'s split planes across commands while A's version holds (the
+  // FC weight of cyclic_gemm(cache_a) / cached_backward_gemm)
+  bool plane_cache_a = false;
 };
 
 enum class SourcePolicy { Peer, LocalOnly };
@@ -108,6 +111,26 @@ struct Worker {
   std::map<BlockKey, StoredBlock> owned;
   std::map<BlockKey, StoredBlock> cache;
   std::map<BlockKey, StoredBlock> replicas;
+  // Split planes of an FC weight (GemmArgs::plane_cache_a), keyed by the
+  // operand geometry, valid while the matrix version equals `version`.
+  struct PlaneCache {
+    std::uint64_t version = 0;  // 0: not filled yet
+    DeviceBuffer hi, second;
+  };
+  std::map<std::vector<std::int64_t>, PlaneCache> plane_cache;
+  // Captured command graphs of small single-panel GEMMs (session_gemm.cpp):
+  // a repeated command replays one graph instead of re-issuing its launches.
+  struct GraphEntry {
+    std::vector<std::uint64_t> sig;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<DeviceBuffer> bufs;
+    dm_worker_stats delta{};
+    std::vector<std::pair<BlockKey, std::uint64_t>> pulls;
+    std::uint64_t last_use = 0;
+    MatrixId ids[3] = {0, 0, 0};
+  };
+  std::deque<GraphEntry> graphs;
+  std::uint64_t graph_clock = 0;
   DeviceBuffer pull_flag;  // landing-copy sequence number (written by the pull stream)
   unsigned pull_seq = 0;
   DeviceBuffer arena;  // exchange buffer peers read (row/col partials, narrowed reshape payloads)
@@ -244,6 +267,7 @@ class Session {
   const void* source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
                          bool* remote) const;
   void run_gemm(const GemmArgs& g, SourcePolicy pol);
+  void drop_graphs(Worker& w, MatrixId id);  // id 0: all
   struct GemmRun;  // one worker's K-panel pipeline of one GEMM command (session_gemm.cpp)
   friend struct GemmRun;
   void cache_foreign_a(const GemmArgs& g);

@@ -16,7 +16,9 @@
 // consumed it, planes[s % 2] until step s-2's GEMM read them.
 #include <algorithm>
 #include <array>
+#include <cstring>
 #include <deque>
+#include <functional>
 #include <map>
 
 #include "../kernels/tf32x3_gemm.h"
@@ -92,7 +94,11 @@ struct Session::GemmRun {
         gemm_mode(resolve_split_mode(s.gemm_mode_, plan.k0.empty() ? 0 : plan.k0.back())),
         trace(s.tracing() && !s.async_),
         np(static_cast<int>(plan.k0.size()) - 1),
-        nbuf(np > 1 ? 2 : 1) {}
+        nbuf(np > 1 ? 2 : 1) {
+    std::int64_t kmax = 0;
+    for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
+    kpitch = std::max<std::int64_t>(8, (kmax + 7) / 8 * 8);
+  }
 
   cudaEvent_t new_event() {
     cudaEvent_t e;
@@ -103,9 +109,6 @@ struct Session::GemmRun {
 
   // ------------------------------------------------------------ setup
   void setup() {
-    std::int64_t kmax = 0;
-    for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
-    kpitch = std::max<std::int64_t>(8, (kmax + 7) / 8 * 8);
     // Producer lockstep needs the GEMM's CTAs co-resident: off when another
     // local worker shares this device (its GEMMs run concurrently).
     int sharing = 0;
@@ -147,26 +150,127 @@ struct Session::GemmRun {
     return false;
   }
 
+  struct PlaneShape {
+    bool mn;
+    std::int64_t ld;
+    std::size_t elems;
+  };
+  PlaneShape plane_shape(const std::vector<Range>& rs, const std::vector<Range>& other, bool is_a,
+                         std::size_t i) const {
+    std::int64_t reuse = 0;
+    for (const Task& t : plan.tasks)
+      if ((is_a ? t.ra : t.rb) == static_cast<int>(i)) reuse += other[is_a ? t.rb : t.ra].len;
+    const bool mn = range_mn(rs[i], reuse);
+    const std::int64_t len = std::max<std::int64_t>(rs[i].len, 1);
+    const std::int64_t ld = mn ? (len + 31) / 32 * 32 : kpitch;
+    return {mn, ld, static_cast<std::size_t>(mn ? kpitch * ld : len * kpitch)};
+  }
+
+  // Plane-cache key of A range i (GemmArgs::plane_cache_a, single panel):
+  // everything the split planes' content and layout depend on but A's version.
+  bool plane_cacheable() const { return g.plane_cache_a && np == 1 && !half_in; }
+  std::vector<std::int64_t> plane_key(std::size_t i) const {
+    const PlaneShape sh = plane_shape(plan.ar, plan.br, true, i);
+    return {static_cast<std::int64_t>(g.a), g.trans_a ? 1 : 0, plan.ar[i].start, plan.ar[i].len, plan.k0.back(),
+            sh.mn ? 1 : 0, sh.ld, gemm_mode};
+  }
+  // Cached A planes of range i: the entry (or null) and whether it holds A's
+  // current version (its split can then be skipped).
+  Worker::PlaneCache* plane_entry(std::size_t i, bool* fresh) const {
+    *fresh = false;
+    if (!plane_cacheable()) return nullptr;
+    auto it = w.plane_cache.find(plane_key(i));
+    if (it == w.plane_cache.end()) return nullptr;
+    *fresh = it->second.version == S.table_.at(g.a).version;
+    return &it->second;
+  }
+  std::vector<char> a_fresh;  // per A range: planes served by the plane cache
+
   void alloc_planes(const std::vector<Range>& rs, const std::vector<Range>& other, bool is_a,
                     std::vector<std::array<Planes, 2>>& out) {
     out.resize(rs.size());
+    if (is_a) a_fresh.assign(rs.size(), 0);
     for (std::size_t i = 0; i < rs.size(); ++i) {
-      std::int64_t reuse = 0;
-      for (const Task& t : plan.tasks)
-        if ((is_a ? t.ra : t.rb) == static_cast<int>(i)) reuse += other[is_a ? t.rb : t.ra].len;
-      const bool mn = range_mn(rs[i], reuse);
-      const std::int64_t len = std::max<std::int64_t>(rs[i].len, 1);
-      const std::int64_t ld = mn ? (len + 31) / 32 * 32 : kpitch;
-      const std::size_t elems = static_cast<std::size_t>(mn ? kpitch * ld : len * kpitch);
+      const PlaneShape sh = plane_shape(rs, other, is_a, i);
       for (int b = 0; b < nbuf; ++b) {
-        bufs.push_back(w.pool->acquire(elems * 4));
-        float* hi = bufs.back().f32();
-        bufs.push_back(w.pool->acquire(elems * 4));
-        char* second = static_cast<char*>(bufs.back().data());
-        out[i][b] = gemm_mode == kModeMixed ? Planes{hi, nullptr, second, second + elems * 2, mn, ld}
-                                            : Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr, mn, ld};
+        float* hi;
+        char* second;
+        if (is_a && plane_cacheable()) {
+          Worker::PlaneCache& pc = w.plane_cache[plane_key(i)];
+          if (!pc.hi.data()) {
+            pc.hi = w.pool->acquire(sh.elems * 4);
+            pc.second = w.pool->acquire(sh.elems * 4);
+          }
+          a_fresh[i] = pc.version == S.table_.at(g.a).version ? 1 : 0;
+          hi = pc.hi.f32();
+          second = static_cast<char*>(pc.second.data());
+        } else {
+          bufs.push_back(w.pool->acquire(sh.elems * 4));
+          hi = bufs.back().f32();
+          bufs.push_back(w.pool->acquire(sh.elems * 4));
+          second = static_cast<char*>(bufs.back().data());
+        }
+        out[i][b] = gemm_mode == kModeMixed
+                        ? Planes{hi, nullptr, second, second + sh.elems * 2, sh.mn, sh.ld}
+                        : Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr, sh.mn, sh.ld};
       }
     }
+  }
+
+  // After this command's splits are enqueued (or its graph launched): the
+  // cached A planes hold A's current version.
+  void commit_plane_cache() {
+    if (!plane_cacheable()) return;
+    for (std::size_t i = 0; i < plan.ar.size(); ++i) {
+      auto it = w.plane_cache.find(plane_key(i));
+      if (it != w.plane_cache.end()) it->second.version = S.table_.at(g.a).version;
+    }
+  }
+
+  // Everything the captured launches of this command depend on (graph key):
+  // the command, the operand pieces' source pointers, the C blocks, the
+  // plane-cache state, the split scheme and the tuning knobs read while issuing.
+  std::vector<std::uint64_t> signature() const {
+    std::vector<std::uint64_t> sig;
+    auto put = [&](std::uint64_t v) { sig.push_back(v); };
+    auto putd = [&](double d) {
+      std::uint64_t u;
+      std::memcpy(&u, &d, 8);
+      put(u);
+    };
+    put(static_cast<std::uint64_t>(pol));
+    put(g.a);
+    put(g.b);
+    put(g.c);
+    put((g.trans_a ? 1u : 0u) | (g.trans_b ? 2u : 0u) | (g.plane_cache_a ? 4u : 0u));
+    putd(g.alpha);
+    putd(g.beta);
+    put(static_cast<std::uint64_t>(gemm_mode));
+    put(static_cast<std::uint64_t>(np));
+    static const char* knobs[] = {"DM_FUSE_SPLIT", "DM_CTA_GROUP", "DM_FLUSH_K", "DM_GROUP_M", "DM_L2_POLICY",
+                                  "DM_LOCKSTEP", "DM_MN_REUSE", "DM_PULL_CE", "DM_SPLIT_WARPS"};
+    for (const char* k : knobs) {
+      const char* v = std::getenv(k);
+      put(v ? std::hash<std::string>()(v) : 0);
+    }
+    for (const auto* ranges : {&plan.ar, &plan.br})
+      for (const Range& r : *ranges) {
+        put(static_cast<std::uint64_t>(r.start));
+        put(static_cast<std::uint64_t>(r.len));
+        for (const auto& panel : r.panels)
+          for (const Piece& pc : panel) {
+            bool remote = false;
+            put(reinterpret_cast<std::uintptr_t>(S.source_ptr(w, pc.matrix, pc.coord, pol, &remote)));
+            put(static_cast<std::uint64_t>(pc.src_off) * 2 + (remote ? 1 : 0));
+          }
+      }
+    for (const Task& t : plan.tasks) put(reinterpret_cast<std::uintptr_t>(w.owned.at({g.c, t.c}).mem.data()));
+    for (std::size_t i = 0; i < plan.ar.size(); ++i) {
+      bool fresh = false;
+      const Worker::PlaneCache* pc = plane_entry(i, &fresh);
+      put(pc ? reinterpret_cast<std::uintptr_t>(pc->hi.data()) * 2 + (fresh ? 1 : 0) : 0);
+    }
+    return sig;
   }
 
   template <class F>
@@ -258,7 +362,8 @@ struct Session::GemmRun {
     for (int ab = 0; ab < 2; ++ab) {
       const std::vector<Range>& rs = ab == 0 ? plan.ar : plan.br;
       const std::vector<std::array<Planes, 2>>& planes = ab == 0 ? pa : pb;
-      for (std::size_t i = 0; i < rs.size(); ++i)
+      for (std::size_t i = 0; i < rs.size(); ++i) {
+        if (ab == 0 && !a_fresh.empty() && a_fresh[i]) continue;  // planes already hold this version
         for (const Piece& pc : rs[i].panels[p]) {
           bool remote, cross;
           const void* src = resolve(pc, &remote, &cross);
@@ -315,6 +420,7 @@ struct Session::GemmRun {
           loff += land_bytes(pc);
           pulled += pc.bytes() / 4 * esz;
         }
+      }
     }
     if (!any) return;
     landed_ev[s] = new_event();
@@ -564,6 +670,7 @@ struct Session::GemmRun {
     setup();
     prepare(0);
     split_separate(0);
+    commit_plane_cache();
     for (int step = 0; step < np; ++step) {
       SplitJobs jobs;
       bool fused_next = false;
@@ -579,12 +686,57 @@ struct Session::GemmRun {
   }
 };
 
+void Session::drop_graphs(Worker& w, MatrixId id) {
+  for (auto it = w.graphs.begin(); it != w.graphs.end();) {
+    if (id == 0 || it->ids[0] == id || it->ids[1] == id || it->ids[2] == id) {
+      cudaGraphExecDestroy(it->exec);
+      it = w.graphs.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  if (id == 0) {
+    w.plane_cache.clear();
+  } else {
+    for (auto it = w.plane_cache.begin(); it != w.plane_cache.end();)
+      it = (!it->first.empty() && it->first[0] == static_cast<std::int64_t>(id)) ? w.plane_cache.erase(it) : ++it;
+  }
+}
+
+namespace {
+void add_stats(dm_worker_stats& a, const dm_worker_stats& d) {
+  a.peer_bytes_read += d.peer_bytes_read;
+  a.local_bytes_read += d.local_bytes_read;
+  a.gemm_launches += d.gemm_launches;
+  a.split_launches += d.split_launches;
+  a.gemm_flops += d.gemm_flops;
+}
+dm_worker_stats sub_stats(const dm_worker_stats& a, const dm_worker_stats& b) {
+  dm_worker_stats d{};
+  d.peer_bytes_read = a.peer_bytes_read - b.peer_bytes_read;
+  d.local_bytes_read = a.local_bytes_read - b.local_bytes_read;
+  d.gemm_launches = a.gemm_launches - b.gemm_launches;
+  d.split_launches = a.split_launches - b.split_launches;
+  d.gemm_flops = a.gemm_flops - b.gemm_flops;
+  return d;
+}
+}  // namespace
+
 void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   struct Live {
     std::vector<DeviceBuffer> bufs;
     std::vector<cudaEvent_t> events;
   };
   std::vector<Live> live(P_);
+  // Small single-panel commands are latency-bound: their per-worker launches
+  // (splits, tensor-map encoding, GEMM, events) cost more host time than the
+  // device spends on them.  A repeated command -- same operands, sources and
+  // knobs -- replays the graph captured the first time instead (buffers kept
+  // with the graph; a changed source pointer or plane-cache state is a new key).
+  const bool graphs_on = !async_ && !tracing() && !timing_ && env_int("DM_GRAPHS", 1) != 0 &&
+                         table_.at(g.a).precision != Precision::Double64;
+  const double graph_max_flops = static_cast<double>(env_int("DM_GRAPH_MAX_GFLOP", 64)) * 1e9;
+  const std::size_t graph_cap = static_cast<std::size_t>(std::max<std::int64_t>(1, env_int("DM_GRAPH_CACHE", 32)));
   for (auto& wp : workers_) {
     if (!wp) continue;
     Worker& w = *wp;
@@ -611,9 +763,69 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     if (plan.tasks.empty()) continue;
     Live& lv = live[w.id];
     if (tracing() && !async_) w.trace_t0 = trace_event(w.stream);
-    {
+    double work = 0;
+    for (const Task& t : plan.tasks) {
+      auto [mb, nb] = block_extent(table_.at(g.c).layout.grid, t.c);
+      work += 2.0 * mb * nb * static_cast<double>(plan.k0.back());
+    }
+    const bool use_graph = graphs_on && plan.k0.size() == 2 && work <= graph_max_flops;
+    GemmRun run(*this, w, g, pol, std::move(plan), lv.bufs, lv.events);
+    if (!use_graph) {
       HostScope hr("run_gemm: GemmRun");
-      GemmRun(*this, w, g, pol, std::move(plan), lv.bufs, lv.events).run();
+      run.run();
+    } else {
+      HostScope hr("run_gemm: graph");
+      std::vector<std::uint64_t> sig = run.signature();
+      Worker::GraphEntry* hit = nullptr;
+      for (auto& e : w.graphs)
+        if (e.sig == sig) {
+          hit = &e;
+          break;
+        }
+      if (hit == nullptr) {
+        // first time: capture the launches this command issues on the
+        // worker's streams (the split stream joins through its events)
+        const dm_worker_stats before = w.stats;
+        cuda_check(cudaStreamBeginCapture(w.stream, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+        cudaGraph_t graph = nullptr;
+        try {
+          run.run();
+        } catch (...) {
+          cudaStreamEndCapture(w.stream, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          throw;
+        }
+        cuda_check(cudaStreamEndCapture(w.stream, &graph), "cudaStreamEndCapture");
+        Worker::GraphEntry e;
+        const cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(ie, "cudaGraphInstantiate");
+        e.sig = std::move(sig);
+        e.delta = sub_stats(w.stats, before);
+        e.pulls.assign(run.pulled_blocks.begin(), run.pulled_blocks.end());
+        e.bufs = std::move(lv.bufs);
+        lv.bufs.clear();
+        e.ids[0] = g.a;
+        e.ids[1] = g.b;
+        e.ids[2] = g.c;
+        if (w.graphs.size() >= graph_cap) {  // evict the least recently used
+          auto lru = std::min_element(w.graphs.begin(), w.graphs.end(),
+                                      [](const auto& x, const auto& y) { return x.last_use < y.last_use; });
+          cudaGraphExecDestroy(lru->exec);
+          w.graphs.erase(lru);
+        }
+        w.graphs.push_back(std::move(e));
+        hit = &w.graphs.back();
+        for (cudaEvent_t ev : lv.events) cudaEventDestroy(ev);
+        lv.events.clear();
+      } else {
+        add_stats(w.stats, hit->delta);
+        for (const auto& [key, bytes] : hit->pulls)
+          log_transfer(table_.at(key.matrix).layout.owner(key.coord), w.id, key.matrix, key.coord, bytes);
+        run.commit_plane_cache();
+      }
+      hit->last_use = ++w.graph_clock;
+      cuda_check(cudaGraphLaunch(hit->exec, w.stream), "cudaGraphLaunch");
     }
     if (async_) {
       mark_write(w, w.stream, g.c);

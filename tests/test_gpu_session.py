@@ -361,3 +361,69 @@ def test_broadcast_gemm_keeps_the_fc_cache(cuda):
         assert r.cached_backward_gemm(rw, rdy, rdx) == 0
         s.cached_backward_gemm(w, dy, dx)  # raised CacheMissError while broadcast aliased cyclic
         assert relfro(s.gather(dx), r.gather_p(rdx)) <= TOL
+
+
+def test_graph_replay_follows_operand_contents(cuda, monkeypatch):
+    """Repeated small commands replay a captured graph (DM_GRAPHS): results
+    must follow every new scatter of the operands and C, bitwise equal to the
+    eager schedule, and the per-worker counters and trace() keep counting."""
+    n, P = 256, 4
+    rng = np.random.default_rng(3)
+    hosts = [rng.standard_normal((n, n)).astype(np.float32) for _ in range(6)]
+    outs = {}
+    for graphs in ("0", "1"):
+        monkeypatch.setenv("DM_GRAPHS", graphs)
+        with Session(Config(worker_count=P, root_seed=1, devices=[0] * P)) as s:
+            lay = make_layout(LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
+            a, b, c = (s.create_matrix(lay) for _ in range(3))
+            res = []
+            for i in range(3):
+                s.scatter(a, hosts[2 * i])
+                s.scatter(b, hosts[2 * i + 1])
+                s.scatter(c, hosts[(2 * i + 2) % 6])
+                s.reset_worker_stats()
+                n_trace = len(s.trace())
+                s.general_gemm(1.5, a, b, -0.5, c, i == 1, i == 2)
+                res.append(s.gather(c))
+                assert sum(s.worker_stats(w).gemm_launches for w in range(P)) == P
+                assert len(s.trace()) - n_trace == 4 * 2  # each worker: 1 foreign A + 1 foreign B block
+                want = ref_gemm(1.5, hosts[2 * i], i == 1, hosts[2 * i + 1], i == 2, -0.5, hosts[(2 * i + 2) % 6])
+                assert relfro(res[-1], want) <= TOL
+            # the same command again: a replay
+            s.general_gemm(1.5, a, b, -0.5, c, False, True)
+            res.append(s.gather(c))
+            s.destroy_matrix(b)  # drops the graphs that read it
+            b2 = s.create_matrix(lay, fill=FillKind.FromHost, host=hosts[5])
+            s.general_gemm(1.0, a, b2, 0.0, c)
+            res.append(s.gather(c))
+            outs[graphs] = res
+    for x, y in zip(outs["0"], outs["1"]):
+        assert x.tobytes() == y.tobytes()
+
+
+def test_fc_plane_cache_follows_weight_versions(cuda):
+    """cyclic_gemm(cache_a) / cached_backward_gemm keep W's split planes while
+    W's version holds; a new W (scatter -> version + 1) is re-split."""
+    P, fin, fout, batch = 4, 512, 384, 64
+    rng = np.random.default_rng(11)
+    Ws = [rng.standard_normal((fin, fout)).astype(np.float32) for _ in range(2)]
+    X = rng.standard_normal((fin, batch)).astype(np.float32)
+    dY = rng.standard_normal((fout, batch)).astype(np.float32)
+    with Session(Config(worker_count=P, root_seed=2, devices=[0] * P)) as s:
+        W = s.create_matrix(make_layout(0, fin, fout, fin // P, fout, P), fill=FillKind.FromHost, host=Ws[0])
+        x = s.create_matrix(make_layout(1, fin, batch, fin, batch // P, P), fill=FillKind.FromHost, host=X)
+        y = s.create_matrix(make_layout(1, fout, batch, fout, batch // P, P))
+        dy = s.create_matrix(make_layout(1, fout, batch, fout, batch // P, P), fill=FillKind.FromHost, host=dY)
+        dx = s.create_matrix(make_layout(1, fin, batch, fin, batch // P, P))
+        for step in range(4):
+            Wh = Ws[step // 2]
+            if step == 2:
+                s.scatter(W, Wh)  # new weights: version + 1
+            s.reset_worker_stats()
+            s.cyclic_gemm(1.0, W, x, 0.0, y, True, False, True)
+            fwd_splits = sum(s.worker_stats(w).split_launches for w in range(P))
+            assert relfro(s.gather(y), ref_gemm(1.0, Wh, True, X, False, 0.0, None)) <= TOL
+            s.cached_backward_gemm(W, dy, dx)
+            assert relfro(s.gather(dx), ref_gemm(1.0, Wh, False, dY, False, 0.0, None)) <= TOL
+            if step % 2 == 1:  # same W as the previous step: only X's pieces are split
+                assert fwd_splits == P
