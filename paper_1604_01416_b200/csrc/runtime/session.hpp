@@ -114,7 +114,8 @@ struct Worker {
   // Split planes of an FC weight (GemmArgs::plane_cache_a), keyed by the
   // operand geometry, valid while the matrix version equals `version`.
   struct PlaneCache {
-    std::uint64_t version = 0;  // 0: not filled yet
+    bool filled = false;  // holds the planes of `version`
+    std::uint64_t version = 0;
     DeviceBuffer hi, second;
   };
   std::map<std::vector<std::int64_t>, PlaneCache> plane_cache;

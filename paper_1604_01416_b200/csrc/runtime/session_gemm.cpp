@@ -181,7 +181,7 @@ struct Session::GemmRun {
     if (!plane_cacheable()) return nullptr;
     auto it = w.plane_cache.find(plane_key(i));
     if (it == w.plane_cache.end()) return nullptr;
-    *fresh = it->second.version == S.table_.at(g.a).version;
+    *fresh = it->second.filled && it->second.version == S.table_.at(g.a).version;
     return &it->second;
   }
   std::vector<char> a_fresh;  // per A range: planes served by the plane cache
@@ -201,7 +201,7 @@ struct Session::GemmRun {
             pc.hi = w.pool->acquire(sh.elems * 4);
             pc.second = w.pool->acquire(sh.elems * 4);
           }
-          a_fresh[i] = pc.version == S.table_.at(g.a).version ? 1 : 0;
+          a_fresh[i] = pc.filled && pc.version == S.table_.at(g.a).version ? 1 : 0;
           hi = pc.hi.f32();
           second = static_cast<char*>(pc.second.data());
         } else {
@@ -223,7 +223,10 @@ struct Session::GemmRun {
     if (!plane_cacheable()) return;
     for (std::size_t i = 0; i < plan.ar.size(); ++i) {
       auto it = w.plane_cache.find(plane_key(i));
-      if (it != w.plane_cache.end()) it->second.version = S.table_.at(g.a).version;
+      if (it != w.plane_cache.end()) {
+        it->second.version = S.table_.at(g.a).version;
+        it->second.filled = true;
+      }
     }
   }
 

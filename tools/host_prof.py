@@ -24,6 +24,7 @@ def wall(s, fn, reps=50):
     return (time.perf_counter() - t0) / reps * 1e6
 
 
+only = sys.argv[1] if len(sys.argv) > 1 else "all"
 ndev = torch.cuda.device_count()
 P = 4
 devs = [w % ndev for w in range(P)]
@@ -31,10 +32,12 @@ with dm.Session(dm.Config(worker_count=P, root_seed=42, devices=devs)) as s:
     n = 2048
     lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
     a, b, c = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(3))
-    print(f"config1 sync : {wall(s, lambda: s.general_gemm(1.0, a, b, 0.0, c)):.1f} us/call", flush=True)
-    s.set_async(True)
-    print(f"config1 async: {wall(s, lambda: s.general_gemm(1.0, a, b, 0.0, c)):.1f} us/call", flush=True)
-    s.set_async(False)
+    if only in ("all", "config1"):
+        print(f"config1 sync : {wall(s, lambda: s.general_gemm(1.0, a, b, 0.0, c)):.1f} us/call", flush=True)
+    if only in ("all", "config1async"):
+        s.set_async(True)
+        print(f"config1 async: {wall(s, lambda: s.general_gemm(1.0, a, b, 0.0, c)):.1f} us/call", flush=True)
+        s.set_async(False)
 with dm.Session(dm.Config(worker_count=P, root_seed=3, devices=devs)) as s:
     fin, fout, batch = 9216, 4096, 256
     strip = batch // P
@@ -44,7 +47,10 @@ with dm.Session(dm.Config(worker_count=P, root_seed=3, devices=devs)) as s:
     dY = s.create_matrix(dm.make_layout(1, fout, batch, fout, strip, P), fill=dm.FillKind.SeededRandom)
     dX = s.create_matrix(dm.make_layout(1, fin, batch, fin, strip, P))
     dW = s.create_matrix(dm.make_layout(0, fin, fout, fin // P, fout, P))
-    print(f"fc fwd cached: {wall(s, lambda: s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)):.1f} us/call")
-    print(f"fc bwd       : {wall(s, lambda: s.cached_backward_gemm(W, dY, dX)):.1f} us/call")
-    print(f"fc dW        : {wall(s, lambda: s.general_gemm(1.0, X, dY, 0.0, dW, False, True)):.1f} us/call",
-          flush=True)
+    if only in ("all", "fwd", "bwd"):
+        print(f"fc fwd cached: {wall(s, lambda: s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)):.1f} us/call")
+    if only in ("all", "bwd"):
+        print(f"fc bwd       : {wall(s, lambda: s.cached_backward_gemm(W, dY, dX)):.1f} us/call")
+    if only in ("all", "dw"):
+        print(f"fc dW        : {wall(s, lambda: s.general_gemm(1.0, X, dY, 0.0, dW, False, True)):.1f} us/call",
+              flush=True)
