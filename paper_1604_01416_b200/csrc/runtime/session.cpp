@@ -323,7 +323,8 @@ void Session::set_async(bool on) {
 void Session::end_command() {
   if (async_) return;  // stream-ordered; completed by barrier()/drain()
   HostScope hs("end_command");
-  sync_local();
+  if (!streams_drained_) sync_local();
+  streams_drained_ = false;
   collect_timing();
   if (comm_) {
     if (coherence_) {
@@ -898,6 +899,7 @@ void Session::flush_trace(const char* op) {
 
 void Session::cache_foreign_a(const GemmArgs& g) {
   const MatrixDescriptor& da = table_.at(g.a);
+  bool copied = false;
   for (auto& wp : workers_) {
     if (!wp) continue;
     Worker& w = *wp;
@@ -921,9 +923,10 @@ void Session::cache_foreign_a(const GemmArgs& g) {
       w.stats.peer_bytes_read += blk.bytes();
       log_transfer(da.layout.owner({r, 0}), w.id, g.a, {r, 0}, blk.bytes());
       w.cache[{g.a, {r, 0}}] = std::move(blk);
+      copied = true;
     }
   }
-  sync_local();
+  if (copied) sync_local();  // a fresh cache: the copies land before the GEMM reads them
 }
 
 void Session::general_gemm(double alpha, MatrixId a, MatrixId b, double beta, MatrixId c, bool ta,

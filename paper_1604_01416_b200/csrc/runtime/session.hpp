@@ -287,6 +287,10 @@ class Session {
   bool live_ = false;
   bool timing_ = false;
   bool async_ = false;
+  // Set when a command already drained every stream it used (run_gemm's
+  // per-worker sync: its split / pull streams all feed the GEMM stream), so
+  // end_command need not synchronise the idle ones again (~1.5 us each).
+  bool streams_drained_ = false;
   std::string trace_path_;
   std::uint64_t trace_cmd_ = 0;
   std::uint64_t root_seed_ = 0;

@@ -786,6 +786,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
           break;
         }
       if (hit == nullptr) {
+        HostScope hc("run_gemm: graph capture");
         // first time: capture the launches this command issues on the
         // worker's streams (the split stream joins through its events)
         const dm_worker_stats before = w.stats;
@@ -822,6 +823,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         for (cudaEvent_t ev : lv.events) cudaEventDestroy(ev);
         lv.events.clear();
       } else {
+        HostScope hc("run_gemm: graph replay");
         add_stats(w.stats, hit->delta);
         for (const auto& [key, bytes] : hit->pulls)
           log_transfer(table_.at(key.matrix).layout.owner(key.coord), w.id, key.matrix, key.coord, bytes);
@@ -860,6 +862,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     for (cudaEvent_t e : live[wp->id].events) cudaEventDestroy(e);
     live[wp->id].bufs.clear();
   }
+  streams_drained_ = true;
 }
 
 }  // namespace dm

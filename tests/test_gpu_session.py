@@ -386,7 +386,10 @@ def test_graph_replay_follows_operand_contents(cuda, monkeypatch):
                 s.general_gemm(1.5, a, b, -0.5, c, i == 1, i == 2)
                 res.append(s.gather(c))
                 assert sum(s.worker_stats(w).gemm_launches for w in range(P)) == P
-                assert len(s.trace()) - n_trace == 4 * 2  # each worker: 1 foreign A + 1 foreign B block
+                # one record per foreign block of each worker's pull plan
+                from paper_1604_01416_b200 import plan_general_gemm
+                want_recs = sum(plan_general_gemm(lay, i == 1, lay, i == 2, lay, w)[0] for w in range(P))
+                assert len(s.trace()) - n_trace == want_recs
                 want = ref_gemm(1.5, hosts[2 * i], i == 1, hosts[2 * i + 1], i == 2, -0.5, hosts[(2 * i + 2) % 6])
                 assert relfro(res[-1], want) <= TOL
             # the same command again: a replay

@@ -27,7 +27,8 @@ import paper_1604_01416_b200 as dm  # noqa: E402
 
 
 def timed(s, fn, reps):
-    fn()  # warm-up (allocations, first pulls)
+    for _ in range(3):  # warm-up: allocations, first pulls, graph captures (steady state after)
+        fn()
     s.barrier()
     t0 = time.perf_counter()
     s.marker_record(0, 4)
@@ -38,6 +39,32 @@ def timed(s, fn, reps):
     return s.marker_elapsed(0, 4, 5) / reps, wall * 1e3
 
 
+def peaks():
+    """Measured per-GPU peaks (MEASURED_PEAKS.json): HBM GB/s and the split
+    schemes' useful fp32 TFLOP/s (bf16 dense / 4 mixed, / 6 3xTF32)."""
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return p["hbm_gbs"], p["bf16_tflops_sustained"]
+    except Exception:
+        return 6500.0, 1400.0
+
+
+NVLINK_GBS = 750.0  # per-GPU peer read bandwidth used for the link bound (NVLink 5, one direction, measured ~700-800)
+
+
+def roofline(ms, flops_w, hbm_bytes_w, link_bytes_w, k):
+    """Per-op roofline of one worker's share (the workers run in parallel):
+    the slowest of tensor time (the split scheme auto picks at this K), HBM
+    bytes (raw fp32 operands read + C written) and NVLink bytes (pulled pieces)."""
+    hbm, bf16 = peaks()
+    tensor = bf16 / (4.0 if dm.split_mode_for("auto", k) == "mixed" else 6.0)
+    t = {"tensor": flops_w / (tensor * 1e12) * 1e3, "hbm": hbm_bytes_w / (hbm * 1e9) * 1e3,
+         "nvlink": link_bytes_w / (NVLINK_GBS * 1e9) * 1e3}
+    kind = max(t, key=t.get)
+    return {"bound": kind, "bound_ms": round(t[kind], 5), "frac": round(t[kind] / ms, 4),
+            "tensor_ms": round(t["tensor"], 5), "hbm_ms": round(t["hbm"], 5), "nvlink_ms": round(t["nvlink"], 5)}
+
+
 def cfg1(args, ndev):
     n, P = 2048, 4
     devs = [w % ndev for w in range(P)]
@@ -45,8 +72,10 @@ def cfg1(args, ndev):
         lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
         a, b, c = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(3))
         ms, wall = timed(s, lambda: s.general_gemm(1.0, a, b, 0.0, c), 20)
+        h = n // 2  # per worker: C block h x h over K = n; A row panel + B column panel, half of each remote
         out = {"config": 1, "workload": "general_gemm 2048^3, 2x2 checkerboard, P=4", "devices": devs,
-               "ms": round(ms, 4), "tflops": 2 * n ** 3 / ms / 1e9, "wall_ms": round(wall, 4)}
+               "ms": round(ms, 4), "tflops": 2 * n ** 3 / ms / 1e9, "wall_ms": round(wall, 4),
+               "roofline": roofline(ms, 2.0 * h * h * n, 4.0 * (2 * h * n + h * h), 4.0 * 2 * h * (n - h), n)}
         if args.ref:
             from oracle import RefOracle
             ro = RefOracle()
@@ -90,7 +119,7 @@ def cfg4(args, ndev):
             # forward without the block cache: every call pulls the foreign W blocks
             s.reset_worker_stats()
             fwd_pull_ms, _ = timed(s, lambda: s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, False), 10)
-            pulled = sum(s.worker_stats(w).peer_bytes_read for w in range(P)) // 11
+            pulled = sum(s.worker_stats(w).peer_bytes_read for w in range(P)) // 13
             # forward with cache_a: W pulled once, later calls read the fresh cache
             s.cyclic_gemm(1.0, W, X, 0.0, Y, True, False, True)
             s.reset_worker_stats()
@@ -114,14 +143,26 @@ def cfg4(args, ndev):
             ws_ms, _ = timed(s, lambda: s.general_gemm(1.0, Wc, Xr, 0.0, Yr, True, False), 20)
             ws_peer = sum(s.worker_stats(w).peer_bytes_read for w in range(P))
             fl = 2.0 * fin * fout * batch
-            fl_pull = fl = 2.0 * fin * fout * batch
+            fl_pull = fl
+            b = batch // P
+            # per worker: fwd / bwd read all of W + the X / dY strip, write the Y / dX strip;
+            # dW reads its X rows (all batch columns, 3/4 remote) and all of dY (3/4 remote)
+            rl = {"fwd_TN_pull": roofline(fwd_pull_ms, fl / P, 4.0 * (fin * fout + fin * b + fout * b),
+                                          4.0 * fin * fout * (P - 1) / P, fin),
+                  "fwd_TN_cached": roofline(fwd_ms, fl / P, 4.0 * (fin * fout + fin * b + fout * b), 0, fin),
+                  "bwd_NN_cached": roofline(bwd_ms, fl / P, 4.0 * (fin * fout + fout * b + fin * b), 0, fout),
+                  "dW_NT": roofline(dw_ms, fl / P, 4.0 * (fin // P * batch + fout * batch + fin // P * fout),
+                                    4.0 * (fin // P * batch + fout * batch) * (P - 1) / P, batch),
+                  "fwd_wstationary": roofline(ws_ms, fl / P, 4.0 * (fin * fout // P + fin * batch + fout // P * batch),
+                                              0, fin)}
             out = {"config": 4, "workload": f"FC {fin}->{fout}, batch {batch}, P={P}", "devices": devs,
                    "fwd_TN_pull_ms": round(fwd_pull_ms, 4), "fwd_pull_peer_bytes_per_call": int(pulled),
                    "fwd_TN_cached_ms": round(fwd_ms, 4), "fwd_cached_peer_bytes": int(fwd_cached_peer), "bwd_NN_cached_ms": round(bwd_ms, 4),
                    "bwd_peer_bytes": int(bwd_peer), "dW_NT_ms": round(dw_ms, 4),
                    "fwd_wstationary_ms": round(ws_ms, 4), "fwd_wstationary_peer_bytes": int(ws_peer),
                    "replicate_X_ms": round(rep_ms, 4),
-                   "fwd_pull_tflops": fl_pull / fwd_pull_ms / 1e9, "fwd_tflops": fl / fwd_ms / 1e9, "bwd_tflops": fl / bwd_ms / 1e9, "dW_tflops": fl / dw_ms / 1e9}
+                   "fwd_pull_tflops": fl_pull / fwd_pull_ms / 1e9, "fwd_tflops": fl / fwd_ms / 1e9, "bwd_tflops": fl / bwd_ms / 1e9, "dW_tflops": fl / dw_ms / 1e9,
+                   "roofline": rl}
             if args.ref:
                 from oracle import RefOracle
                 ro = RefOracle()
