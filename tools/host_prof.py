@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import paper_1604_01416_b200 as dm  # noqa: E402
 
 
-def wall(s, fn, reps=50):
+def wall(s, fn, reps=int(os.environ.get("HOST_PROF_REPS", "50"))):
     for _ in range(5):
         fn()
     s.barrier()
