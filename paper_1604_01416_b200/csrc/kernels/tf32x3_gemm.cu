@@ -532,6 +532,13 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   }
 }
 
+// All split jobs of a command in one launch (small, latency-bound commands:
+// one kernel instead of one per piece, every piece's tiles in flight at once).
+__global__ void __launch_bounds__(64) split_jobs_kernel(const __grid_constant__ SplitJobs sj) {
+  __shared__ float tile[32][128 + 4];
+  run_split_jobs(sj, tile, static_cast<int>(threadIdx.x));
+}
+
 // C <- alpha*0 + beta*C for K == 0 (no tensor-core work).
 __global__ void scale_c_kernel(float* c, int c_half, int64_t ldc, int m, int n, float alpha_zero,
                                float beta, int read_c) {
@@ -745,6 +752,16 @@ cudaError_t stream_write_flag(cudaStream_t stream, unsigned* addr, unsigned valu
   if (fn == nullptr) return cudaErrorNotSupported;
   return fn(stream, reinterpret_cast<CUdeviceptr>(addr), value, 0) == CUDA_SUCCESS ? cudaSuccess
                                                                                     : cudaErrorUnknown;
+}
+
+cudaError_t split_jobs(const SplitJobs& jobs, cudaStream_t stream) {
+  if (jobs.n <= 0 || jobs.t_end <= jobs.t_begin) return cudaSuccess;
+  for (int i = 0; i < jobs.n; ++i)
+    if (jobs.job[i].flag != nullptr || !split_job_fusable(jobs.job[i])) return cudaErrorInvalidValue;
+  const int64_t tiles = jobs.t_end - jobs.t_begin;
+  const int blocks = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
+  split_jobs_kernel<<<blocks, 64, 0, stream>>>(jobs);
+  return cudaGetLastError();
 }
 
 int64_t tf32x3_default_flush_k(int mode, int64_t k_total) {

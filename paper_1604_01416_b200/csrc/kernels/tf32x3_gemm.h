@@ -57,6 +57,9 @@ struct SplitJobs {
 int64_t split_job_tiles(const SplitJob& j);
 // can the GEMM's split warps run this job (fp32, aligned)?
 bool split_job_fusable(const SplitJob& j);
+// Run a list of split jobs (no landing flags, all fusable) as one kernel
+// launch over their concatenated tiles [t_begin, t_end).
+cudaError_t split_jobs(const SplitJobs& jobs, cudaStream_t stream);
 
 // C[m x n] (row pitch ldc) <- alpha * A B^T + beta * C, where A and B are
 // given as split planes, each either K-major -- A [m x k], B [n x k] (i.e.

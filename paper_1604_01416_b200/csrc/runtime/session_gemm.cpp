@@ -453,6 +453,14 @@ struct Session::GemmRun {
     if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_ev[s - nbuf], 0), "wait");  // planes free
     cudaEvent_t ta = trace ? S.trace_event(w.side) : nullptr;
     std::uint64_t bytes = 0;
+    // Small splits (a latency-bound command): every piece in one launch.
+    if (split_batched(s)) {
+      if (trace) w.trace.push_back({"split", order[s], 0, 0.0, ta, S.trace_event(w.side)});
+      split_ev[s] = new_event();
+      cuda_check(cudaEventRecord(split_ev[s], w.side), "event");
+      consumed_ev[s] = split_ev[s];
+      return;
+    }
     // local pieces first (no wait), then landed ones as their copies complete
     std::vector<const Item*> seq_items;
     for (const Item& it : items[s])
@@ -481,22 +489,25 @@ struct Session::GemmRun {
     consumed_ev[s] = split_ev[s];
   }
 
-  // Split jobs of step s for the split warps of step s-1's GEMM launches.
-  // Fused only when the carrying GEMM is long enough to hide the split: two
-  // warps per SM split ~150 GB/s of input beside a ~300 TFLOP/s GEMM (a
-  // narrow panel cannot hide a full panel's split -- that one runs as its own
-  // full-machine kernels instead).
-  bool fused_jobs(int s, SplitJobs* out) const {
-    if (fuse_mode == 0 || items[s].empty() || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs))
-      return false;
-    double bytes_in = 0, flops = 0;
-    for (const Item& it : items[s]) bytes_in += static_cast<double>(it.pc->bytes());
-    const std::int64_t kw = plan.k0[order[s - 1] + 1] - plan.k0[order[s - 1]];
-    for (const Task& t : plan.tasks) {
-      auto [mb, nb] = block_extent(S.table_.at(g.c).layout.grid, t.c);
-      flops += 2.0 * mb * nb * static_cast<double>(kw);
+  // One split_jobs launch for all items of step s when they are few, small
+  // (<= DM_BATCH_SPLIT_MB of input, default 64) and none waits on a landing.
+  bool split_batched(int s) {
+    if (half_in || items[s].empty() || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs)) return false;
+    double bytes_in = 0;
+    for (const Item& it : items[s]) {
+      if (it.landed) return false;
+      bytes_in += static_cast<double>(it.pc->bytes());
     }
-    if (fuse_mode == 1 && bytes_in / 150e9 > flops / 300e12) return false;
+    if (bytes_in > static_cast<double>(env_int("DM_BATCH_SPLIT_MB", 64)) * (1 << 20)) return false;
+    SplitJobs jobs;
+    if (!make_jobs(s, &jobs)) return false;
+    cuda_check(split_jobs(jobs, w.side), "split_jobs");
+    w.stats.split_launches += 1;
+    return true;
+  }
+
+  // Split jobs for the items of step s (false if a piece is not fusable).
+  bool make_jobs(int s, SplitJobs* out) const {
     out->n = 0;
     std::int64_t t = 0;
     for (const Item& it : items[s]) {
@@ -524,6 +535,25 @@ struct Session::GemmRun {
     out->t_begin = 0;
     out->t_end = t;
     return true;
+  }
+
+  // Split jobs of step s for the split warps of step s-1's GEMM launches.
+  // Fused only when the carrying GEMM is long enough to hide the split: two
+  // warps per SM split ~150 GB/s of input beside a ~300 TFLOP/s GEMM (a
+  // narrow panel cannot hide a full panel's split -- that one runs as its own
+  // full-machine kernels instead).
+  bool fused_jobs(int s, SplitJobs* out) const {
+    if (fuse_mode == 0 || items[s].empty() || items[s].size() > static_cast<std::size_t>(kMaxSplitJobs))
+      return false;
+    double bytes_in = 0, flops = 0;
+    for (const Item& it : items[s]) bytes_in += static_cast<double>(it.pc->bytes());
+    const std::int64_t kw = plan.k0[order[s - 1] + 1] - plan.k0[order[s - 1]];
+    for (const Task& t : plan.tasks) {
+      auto [mb, nb] = block_extent(S.table_.at(g.c).layout.grid, t.c);
+      flops += 2.0 * mb * nb * static_cast<double>(kw);
+    }
+    if (fuse_mode == 1 && bytes_in / 150e9 > flops / 300e12) return false;
+    return make_jobs(s, out);
   }
 
   // The GEMM launches of step `step` (one per owned C block), carrying the
