@@ -14,7 +14,8 @@ torch.distributed.run (one process per GPU, NCCL, 127.0.0.1); under torchrun
 WORLD_SIZE must equal --gpus.  At every N the line carries sampled parity of
 the timed result against the reference (16 full rows + 16 full columns spread
 over every C block and tile), the reference CPU baseline, and a second timed
-run of the north star's own 3xTF32 split beside the default mixed split.
+run of the north star's own 3xTF32 split beside the default f16x2 split
+(3xTF32's 11+11-bit pair and three products, executed on fp16 MMAs).
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref = /root/reference compiled unmodified) on the host cores: each
@@ -49,7 +50,14 @@ def dist_env():
 # bf16 rate (TF32 runs at bf16/2); per useful k16 step:
 #   3xTF32: 6 TF32 k8 MMAs           = 6 bf16-k16 slots -> peak = bf16 / 6
 #   mixed : 2 TF32 k8 + 2 BF16 k16   = 4 bf16-k16 slots -> peak = bf16 / 4
-SLOTS = {"mixed": 4.0, "3xtf32": 6.0}
+#   f16x2 : 3 FP16 k16               = 3 bf16-k16 slots -> peak = bf16 / 3
+SLOTS = {"mixed": 4.0, "3xtf32": 6.0, "f16x2": 3.0}
+KERNELS = {
+    "f16x2": "dm::tf32x3_gemm_kernel<2,3> (CTA pair; scaled 2xFP16 split, h1*h0 + h0*h1 + h0*h0 as tcgen05 "
+             "kind::f16, power-of-two row scales undone in the epilogue)",
+    "mixed": "dm::tf32x3_gemm_kernel<2,1> (CTA pair; hi*hi tcgen05 kind::tf32 + bf16 cross terms kind::f16)",
+    "3xtf32": "dm::tf32x3_gemm_kernel<2,0> (CTA pair; tcgen05 kind::tf32 x3)",
+}
 
 
 def measured_peaks(mode: str):
@@ -288,7 +296,7 @@ def run_ours(args):
     lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, N, N, N // pr, N // pc, world)
     s = make_session(args.gemm_mode)
     session_mode = s.gemm_mode()
-    mode = dm.split_mode_for(session_mode, N)  # the scheme this K runs in (auto: mixed above K=8192)
+    mode = dm.split_mode_for(session_mode, N)  # the scheme this K runs in (auto: f16x2)
     me = rank
     a = s.create_matrix(lay, fill=dm.FillKind.SeededRandom)
     b = s.create_matrix(lay, fill=dm.FillKind.SeededRandom)
@@ -317,7 +325,7 @@ def run_ours(args):
     # ---- the north star's own scheme beside it: the same workload in 3xTF32
     alt = None
     if not args.no_alt:
-        alt_mode = "3xtf32" if mode == "mixed" else "mixed"
+        alt_mode = "3xtf32" if mode != "3xtf32" else "f16x2"
         s2 = make_session(alt_mode)
         a2, b2 = (s2.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(2))
         c2 = s2.create_matrix(lay, fill=dm.FillKind.Zeros)
@@ -355,8 +363,7 @@ def run_ours(args):
     peak_burst, peak_sust, peak_src = measured_peaks(mode)
     peak_3x = measured_peaks("3xtf32")[1]
     traffic, traffic_src = load_ncu_traffic(N, world, mode)
-    kernel = ("dm::tf32x3_gemm_kernel<2,1> (CTA pair; hi*hi tcgen05 kind::tf32 + bf16 cross terms kind::f16)"
-              if mode == "mixed" else "dm::tf32x3_gemm_kernel<2,0> (CTA pair; tcgen05 kind::tf32 x3)")
+    kernel = KERNELS[mode]
     line = {
         "metric": METRIC, "value": round(main["value"], 3), "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(main["t_ms"] / args.steps, 3),
@@ -587,9 +594,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--gemm-mode", choices=["default", "auto", "mixed", "3xtf32"], default="default",
+    ap.add_argument("--gemm-mode", choices=["default", "auto", "f16x2", "mixed", "3xtf32"], default="default",
                     help="split-product scheme of the headline run (default: DM_GEMM_MODE, else auto = "
-                         "mixed at this K)")
+                         "f16x2)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline and sampled parity")
     ap.add_argument("--no-alt", action="store_true", help="skip the second (3xTF32) timed run")

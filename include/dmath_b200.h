@@ -49,19 +49,22 @@ enum dm_layout_kind { /* layout.hpp:69-75 */
 };
 enum dm_precision { DM_HALF16 = 0, DM_SINGLE32 = 1, DM_DOUBLE64 = 2 }; /* precision.hpp:14 */
 enum dm_fill { DM_FILL_ZEROS = 0, DM_FILL_SEEDED = 1, DM_FILL_FROM_HOST = 2 }; /* runtime_types.hpp:68 */
-/* Split-product scheme of the fp32 tensor-core GEMM (both fp32-accurate,
+/* Split-product scheme of the fp32 tensor-core GEMM (all fp32-accurate,
  * DESIGN.md section 4):
  *   DM_GEMM_MIXED  : hi*hi as tcgen05 kind::tf32 + the two cross terms as bf16
  *                    (kind::f16): 4 bf16-MMA slots per useful k16;
  *   DM_GEMM_TF32X3 : lo*hi + hi*lo + hi*hi, all kind::tf32 (north star's
  *                    3xTF32): 6 slots per k16;
- *   DM_GEMM_AUTO   : per product, 3xTF32 for K <= 8192 and mixed above: at
- *                    small K the reference's own error is small and only
- *                    3xTF32 stays near it; at large K both are below it and
- *                    mixed is ~1.2x faster;
+ *   DM_GEMM_F16X2  : 3xTF32's numerics on fp16 operands -- per plane row a
+ *                    power-of-two scale puts max|x| in [2^14, 2^15), then
+ *                    x*2^e = h0 + h1 (fp16, 11 + 11 bits like tf32 hi / lo) and
+ *                    h1*h0 + h0*h1 + h0*h0 as kind::f16: 3 slots per k16, 4 B of
+ *                    planes per element;
+ *   DM_GEMM_AUTO   : f16x2 for every fp32 product (3xTF32's accuracy at 1.8x
+ *                    its speed); Half16 operands run 3xTF32;
  *   DM_GEMM_DEFAULT: the DM_GEMM_MODE environment variable (0 = 3xTF32,
- *                    1 = mixed, 2 = auto), else auto. */
-enum dm_gemm_mode { DM_GEMM_DEFAULT = 0, DM_GEMM_MIXED = 1, DM_GEMM_TF32X3 = 2, DM_GEMM_AUTO = 3 };
+ *                    1 = mixed, 2 = auto, 3 = f16x2), else auto. */
+enum dm_gemm_mode { DM_GEMM_DEFAULT = 0, DM_GEMM_MIXED = 1, DM_GEMM_TF32X3 = 2, DM_GEMM_AUTO = 3, DM_GEMM_F16X2 = 4 };
 enum dm_mode {
   DM_MODE_LOCAL = 0, /* one process drives every worker (reference Session, session.hpp:64-76) */
   DM_MODE_SPMD = 1   /* one process per GPU; every rank makes the same calls (torchrun) */

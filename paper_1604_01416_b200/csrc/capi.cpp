@@ -64,6 +64,7 @@ int resolve_gemm_mode(int requested, int64_t k) {
   if (requested == DM_GEMM_TF32X3) mode = dm::kModeTf32x3;
   else if (requested == DM_GEMM_MIXED) mode = dm::kModeMixed;
   else if (requested == DM_GEMM_AUTO) mode = dm::kModeAuto;
+  else if (requested == DM_GEMM_F16X2) mode = dm::kModeF16x2;
   else if (requested == DM_GEMM_DEFAULT) mode = dm::env_gemm_mode();
   else throw dm::UsageError("unknown gemm_mode");
   return dm::resolve_split_mode(mode, k);
@@ -76,10 +77,12 @@ int resolve_gemm_mode(int requested, int64_t k) {
 // planes -- split row by row, no transpose -- when the other extent (its
 // reuse) is below DM_MN_REUSE (session_gemm.cpp range_mn).
 struct SeamLayout {
+  bool f16x2 = false;  // kModeF16x2: fp16 h0 | h1 planes (4 B / element) + row maxima, K-major
   bool a_mn = false, b_mn = false;
   int64_t lda = 8, ldb = 8;  // plane pitches (elements): K-major kp, MN-major m / n rounded to 32
   int64_t a_elems = 0, b_elems = 0;
   size_t off[5] = {0, 0, 0, 0, 0};  // a_hi, a_second, b_hi, b_second, splitk ws
+  size_t off_max = 0;                // kModeF16x2: A row maxima [m], then B^T row maxima [n]
   size_t ws_bytes = 0;
   size_t total = 0;
 };
@@ -88,8 +91,9 @@ SeamLayout seam_layout(const dm::Tf32x3Args& shape, int ta, int tb) {
   SeamLayout l;
   auto up = [](size_t x) { return (x + 255) / 256 * 256; };
   const int64_t thr = dm::env_int("DM_MN_REUSE", 2048);
-  l.a_mn = ta != 0 && shape.n < thr;
-  l.b_mn = tb == 0 && shape.m < thr;
+  l.f16x2 = shape.mode == dm::kModeF16x2;
+  l.a_mn = !l.f16x2 && ta != 0 && shape.n < thr;
+  l.b_mn = !l.f16x2 && tb == 0 && shape.m < thr;
   const int64_t kp = std::max<int64_t>(8, (shape.k + 7) / 8 * 8);
   l.lda = l.a_mn ? (shape.m + 31) / 32 * 32 : kp;
   l.ldb = l.b_mn ? (shape.n + 31) / 32 * 32 : kp;
@@ -102,7 +106,8 @@ SeamLayout seam_layout(const dm::Tf32x3Args& shape, int ta, int tb) {
   l.off[3] = 2 * a + b;
   l.off[4] = 2 * a + 2 * b;
   l.ws_bytes = dm::tf32x3_splitk_bytes(shape);
-  l.total = l.off[4] + up(l.ws_bytes);
+  l.off_max = l.off[4] + up(l.ws_bytes);
+  l.total = l.off_max + (l.f16x2 ? up(static_cast<size_t>(shape.m + shape.n) * 4) : 0);
   return l;
 }
 
@@ -162,7 +167,25 @@ void local_gemm_run(double alpha, const float* a, int64_t lda, int ta, const flo
     args.b_hi = reinterpret_cast<const float*>(ws + L.off[2]);
     args.lda = args.lda16 = L.lda;
     args.ldb = args.ldb16 = L.ldb;
-    if (mode == dm::kModeMixed) {
+    if (L.f16x2) {
+      // fp16 h0 | h1 in the first half of each operand region (4 B / element)
+      args.a_hi = args.b_hi = nullptr;
+      args.a_hi16 = ws + L.off[0];
+      args.a_lo16 = ws + L.off[0] + L.a_elems * 2;
+      args.b_hi16 = ws + L.off[2];
+      args.b_lo16 = ws + L.off[2] + L.b_elems * 2;
+      unsigned* amax = reinterpret_cast<unsigned*>(ws + L.off_max);
+      unsigned* bmax = amax + m;
+      args.a_max = amax;
+      args.b_max = bmax;
+      dm::cuda_check(cudaMemsetAsync(amax, 0, static_cast<size_t>(m + n) * 4, st), "memset maxima");
+      dm::cuda_check(dm::absmax_rows(a, lda, ta, m, k, amax, st), "absmax A");
+      dm::cuda_check(dm::absmax_rows(b, ldb, tb ? 0 : 1, n, k, bmax, st), "absmax B");
+      dm::cuda_check(dm::split_f16x2(a, lda, ta, m, k, const_cast<void*>(args.a_hi16),
+                                     const_cast<void*>(args.a_lo16), L.lda, amax, st), "split A");
+      dm::cuda_check(dm::split_f16x2(b, ldb, tb ? 0 : 1, n, k, const_cast<void*>(args.b_hi16),
+                                     const_cast<void*>(args.b_lo16), L.ldb, bmax, st), "split B");
+    } else if (mode == dm::kModeMixed) {
       args.a_hi16 = ws + L.off[1];
       args.a_lo16 = ws + L.off[1] + L.a_elems * 2;
       args.b_hi16 = ws + L.off[3];
@@ -181,8 +204,10 @@ void local_gemm_run(double alpha, const float* a, int64_t lda, int ta, const flo
                                     const_cast<void*>(lo16), pitch, st),
                      what);
     };
-    split(a, lda, ta, m, L.a_mn, args.a_hi, args.a_lo, args.a_hi16, args.a_lo16, L.lda, "split A");
-    split(b, ldb, tb ? 0 : 1, n, L.b_mn, args.b_hi, args.b_lo, args.b_hi16, args.b_lo16, L.ldb, "split B");
+    if (!L.f16x2) {
+      split(a, lda, ta, m, L.a_mn, args.a_hi, args.a_lo, args.a_hi16, args.a_lo16, L.lda, "split A");
+      split(b, ldb, tb ? 0 : 1, n, L.b_mn, args.b_hi, args.b_lo, args.b_hi16, args.b_lo16, L.ldb, "split B");
+    }
     if (L.ws_bytes > 0) {
       args.ws = reinterpret_cast<float*>(ws + L.off[4]);
       args.ws_bytes = L.ws_bytes;
@@ -498,7 +523,10 @@ int dm_cached_backward_gemm(dm_session* s, dm_matrix_id w, dm_matrix_id dy, dm_m
 int dm_session_gemm_mode(dm_session* s, int* out) {
   return guarded([&] {
     const int m = S(s).gemm_mode();
-    *out = m == dm::kModeTf32x3 ? DM_GEMM_TF32X3 : m == dm::kModeMixed ? DM_GEMM_MIXED : DM_GEMM_AUTO;
+    *out = m == dm::kModeTf32x3  ? DM_GEMM_TF32X3
+           : m == dm::kModeMixed ? DM_GEMM_MIXED
+           : m == dm::kModeF16x2 ? DM_GEMM_F16X2
+                                 : DM_GEMM_AUTO;
   });
 }
 

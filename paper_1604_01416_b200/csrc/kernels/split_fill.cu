@@ -199,6 +199,68 @@ __global__ void fill_seeded_kernel(T* __restrict__ dst, int64_t count, uint64_t 
   }
 }
 
+// ---- per-row |x| maxima for the scaled 2xFP16 split (kModeF16x2)
+// rmax[r] = max(rmax[r], max_k |x[r][k]|) as float bits (non-negative floats
+// order like their bits, so atomicMax on unsigned is a float max).
+// Direct: one warp per row and 4096-k slice, float4 loads when aligned.
+__global__ void __launch_bounds__(256) absmax_direct_kernel(const float* __restrict__ src, int64_t lds,
+                                                            int64_t rows, int64_t kcols, unsigned* rmax) {
+  const int64_t r = static_cast<int64_t>(blockIdx.y) * 8 + threadIdx.x / 32;
+  if (r >= rows) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 4096;
+  const int64_t k1 = min(kcols, k0 + 4096);
+  const float* row = src + r * lds;
+  float m = 0.0f;
+  int64_t kv = k0;
+  if ((reinterpret_cast<uintptr_t>(row + k0) & 15) == 0) {
+    for (; kv + 128 <= k1; kv += 128) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(row + kv) + lane);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+  }
+  for (int64_t k = kv + lane; k < k1; k += 32) m = fmaxf(m, fabsf(__ldcs(row + k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0 && m > 0.0f) atomicMax(rmax + r, __float_as_uint(m));
+}
+
+// Transposed (x[r][k] = src[k * lds + r]): 128 rows x 256 k per block, each
+// thread 4 adjacent r (float4 along the contiguous axis) over 32 k.
+__global__ void __launch_bounds__(256) absmax_trans_kernel(const float* __restrict__ src, int64_t lds,
+                                                           int64_t rows, int64_t kcols, unsigned* rmax) {
+  __shared__ float red[8][128];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t r = static_cast<int64_t>(blockIdx.y) * 128 + tx * 4;
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 256;
+  const bool vec = r + 4 <= rows && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (lds & 3) == 0;
+  float m[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  for (int i = 0; i < 32; ++i) {
+    const int64_t k = k0 + ty + 8 * i;
+    if (k >= kcols) break;
+    if (vec) {
+      const float4 v = __ldcs(reinterpret_cast<const float4*>(src + k * lds + r));
+      m[0] = fmaxf(m[0], fabsf(v.x));
+      m[1] = fmaxf(m[1], fabsf(v.y));
+      m[2] = fmaxf(m[2], fabsf(v.z));
+      m[3] = fmaxf(m[3], fabsf(v.w));
+    } else {
+      for (int u = 0; u < 4; ++u)
+        if (r + u < rows) m[u] = fmaxf(m[u], fabsf(__ldcs(src + k * lds + r + u)));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) red[ty][tx * 4 + u] = m[u];
+  __syncthreads();
+  if (threadIdx.x < 128) {
+    float v = red[0][threadIdx.x];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) v = fmaxf(v, red[y][threadIdx.x]);
+    const int64_t rr = static_cast<int64_t>(blockIdx.y) * 128 + threadIdx.x;
+    if (rr < rows && v > 0.0f) atomicMax(rmax + rr, __float_as_uint(v));
+  }
+}
+
 }  // namespace
 
 cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, int64_t rows,
@@ -233,6 +295,47 @@ cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, in
     if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(s32, lds, rows, kcols, p);
     else split_direct_kernel<<<grid, block, 0, stream>>>(s32, lds, rows, kcols, p);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t absmax_rows(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols, unsigned* rmax,
+                        cudaStream_t stream) {
+  if (rows <= 0 || kcols <= 0) return cudaSuccess;
+  if (trans) {
+    const dim3 g(static_cast<unsigned>((kcols + 255) / 256), static_cast<unsigned>((rows + 127) / 128));
+    if (g.y > 65535u) return cudaErrorInvalidConfiguration;
+    absmax_trans_kernel<<<g, 256, 0, stream>>>(src, lds, rows, kcols, rmax);
+  } else {
+    const dim3 g(static_cast<unsigned>((kcols + 4095) / 4096), static_cast<unsigned>((rows + 7) / 8));
+    if (g.y > 65535u) return cudaErrorInvalidConfiguration;
+    absmax_direct_kernel<<<g, 256, 0, stream>>>(src, lds, rows, kcols, rmax);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t split_f16x2(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols, void* h0, void* h1,
+                        int64_t ldo16, const unsigned* rmax, cudaStream_t stream) {
+  if (rows <= 0 || kcols <= 0) return cudaSuccess;
+  Planes p{nullptr, nullptr, nullptr, nullptr, 0, ldo16};
+  p.h0 = static_cast<__half*>(h0);
+  p.h1 = static_cast<__half*>(h1);
+  p.rmax = rmax;
+  auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  auto a8 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; };
+  if (a16(src) && (lds & 3) == 0 && a8(h0) && a8(h1) && (ldo16 & 3) == 0) {
+    if ((rows + 7) / 8 > 65535) return cudaErrorInvalidConfiguration;
+    switch (split_warps()) {
+      case 2: launch_split_vec4<2>(src, lds, trans, rows, kcols, p, stream); break;
+      case 4: launch_split_vec4<4>(src, lds, trans, rows, kcols, p, stream); break;
+      default: launch_split_vec4<8>(src, lds, trans, rows, kcols, p, stream); break;
+    }
+    return cudaGetLastError();
+  }
+  dim3 block(kT, kRowsPerPass);
+  dim3 grid(static_cast<unsigned>((kcols + kT - 1) / kT), static_cast<unsigned>((rows + kT - 1) / kT));
+  if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
+  if (trans) split_trans_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, p);
+  else split_direct_kernel<<<grid, block, 0, stream>>>(src, lds, rows, kcols, p);
   return cudaGetLastError();
 }
 

@@ -75,7 +75,13 @@ struct EpiParams {
   float* ws;            // [ksplit][m][n] partial tiles (ksplit > 1)
   int a_mn, b_mn;       // fp32 operand planes MN-major (M / N contiguous) instead of K-major
   int a_mn16, b_mn16;   // the same for the bf16 planes (mixed mode)
+  const unsigned* a_max;  // kModeF16x2: row maxima of the A / B^T planes (power-of-two scales)
+  const unsigned* b_max;
 };
+
+// k per pipeline stage: 32 fp32 or 64 fp16 elements fill a 128-B swizzle row
+template <int MODE>
+__host__ __device__ constexpr int stage_k() { return MODE == kModeF16x2 ? 64 : 32; }
 
 // Work item t of a launch: tile t % tiles of K-split t / tiles, whose k-blocks
 // are [kb_lo, kb_hi) (empty ranges still store a zero partial).
@@ -109,27 +115,110 @@ __device__ __forceinline__ void tile_coords(int t, int tiles_m, int tiles_n, int
 // transposed 32 k x 128 rows through a shared-memory tile.
 __device__ __forceinline__ void split_bar() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
 
-__device__ __noinline__ void run_split_jobs(const SplitJobs& sj, float (*tile)[128 + 4], int st) {
+// Job j of tile t, waiting for its landing flag the first time (`ready` bits).
+__device__ __forceinline__ const SplitJob& split_job_of(const SplitJobs& sj, int64_t t, uint32_t& ready) {
+  int j = 0;
+  while (j + 1 < sj.n && t >= sj.job[j + 1].t0) ++j;
+  const SplitJob& jb = sj.job[j];
+  if (jb.flag != nullptr && !(ready & (1u << j))) {
+    const long long t0 = clock64();
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(jb.flag) : "memory");
+      if (static_cast<int>(v - jb.flag_val) >= 0) break;
+      __nanosleep(256);
+      if (clock64() - t0 > (1ll << 36)) __trap();  // landing copy never signalled
+    }
+    ready |= 1u << j;
+  }
+  return jb;
+}
+
+// Phase 1 of kModeF16x2 jobs: per plane row, the |x| maximum of this block's
+// tiles into jb.rmax (atomicMax on the float bits).  Same tiles as the split.
+__device__ __noinline__ void run_absmax_jobs(const SplitJobs& sj, int st, uint32_t& ready) {
+  const int lane = st & 31, wy = st >> 5;
+  for (int64_t t = sj.t_begin + blockIdx.x; t < sj.t_end; t += gridDim.x) {
+    const SplitJob& jb = split_job_of(sj, t, ready);
+    const int64_t lt = t - jb.t0;
+    if (!jb.trans) {
+      const int64_t tiles_k = (jb.kcols + 127) / 128;
+      const int64_t k = (lt % tiles_k) * 128 + lane * 4;
+      const int64_t r0 = (lt / tiles_k) * 32 + wy;
+      for (int i = 0; i < 16; ++i) {
+        const int64_t r = r0 + 2 * i;
+        if (r >= jb.rows) break;  // warp-uniform
+        float m = 0.0f;
+        if (k + 4 <= jb.kcols) {
+          const float4 v = __ldcs(reinterpret_cast<const float4*>(jb.src + r * jb.lds + k));
+          m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+        } else {
+          for (int64_t kk = k; kk < jb.kcols; ++kk) m = fmaxf(m, fabsf(__ldcs(jb.src + r * jb.lds + kk)));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0 && m > 0.0f) atomicMax(jb.rmax + r, __float_as_uint(m));
+      }
+    } else {
+      const int64_t tiles_k = (jb.kcols + 31) / 32;
+      const int64_t k0 = (lt % tiles_k) * 32;
+      const int64_t r = (lt / tiles_k) * 128 + lane * 4;
+      float m[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      for (int i = 0; i < 16; ++i) {
+        const int64_t k = k0 + wy + 2 * i;
+        if (k >= jb.kcols) break;
+        if (r + 4 <= jb.rows) {
+          const float4 v = __ldcs(reinterpret_cast<const float4*>(jb.src + k * jb.lds + r));
+          m[0] = fmaxf(m[0], fabsf(v.x));
+          m[1] = fmaxf(m[1], fabsf(v.y));
+          m[2] = fmaxf(m[2], fabsf(v.z));
+          m[3] = fmaxf(m[3], fabsf(v.w));
+        } else {
+          for (int u = 0; u < 4; ++u)
+            if (r + u < jb.rows) m[u] = fmaxf(m[u], fabsf(__ldcs(jb.src + k * jb.lds + r + u)));
+        }
+      }
+      for (int u = 0; u < 4; ++u)
+        if (r + u < jb.rows && m[u] > 0.0f) atomicMax(jb.rmax + r + u, __float_as_uint(m[u]));
+    }
+  }
+}
+
+// phase: 0 split only; 1 row maxima only (kModeF16x2, separate launch);
+// 2 both, with a grid-wide handoff on sj.phase_ctr in between (fused into a
+// persistent GEMM launch, whose CTAs are all co-resident).
+__device__ __noinline__ void run_split_jobs(const SplitJobs& sj, float (*tile)[128 + 4], int st, int phase) {
   using splitdev::Planes;
   const int lane = st & 31, wy = st >> 5;
   uint32_t ready = 0;  // jobs whose landing flag was seen
-  for (int64_t t = sj.t_begin + blockIdx.x; t < sj.t_end; t += gridDim.x) {
-    int j = 0;
-    while (j + 1 < sj.n && t >= sj.job[j + 1].t0) ++j;
-    const SplitJob& jb = sj.job[j];
-    if (jb.flag != nullptr && !(ready & (1u << j))) {
+  if (phase != 0) {
+    run_absmax_jobs(sj, st, ready);
+    if (phase == 1) return;
+    split_bar();
+    if (st == 0) {
+      __threadfence();
+      atomicAdd(sj.phase_ctr, 1u);
       const long long t0 = clock64();
       while (true) {
         unsigned v;
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(jb.flag) : "memory");
-        if (static_cast<int>(v - jb.flag_val) >= 0) break;
-        __nanosleep(256);
-        if (clock64() - t0 > (1ll << 36)) __trap();  // landing copy never signalled
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sj.phase_ctr) : "memory");
+        if (v >= gridDim.x) break;
+        __nanosleep(128);
+        if (clock64() - t0 > (1ll << 36)) __trap();  // a CTA of the launch never arrived
       }
-      ready |= 1u << j;
     }
-    const Planes p{jb.hi, jb.lo, static_cast<__nv_bfloat16*>(jb.hi16), static_cast<__nv_bfloat16*>(jb.lo16),
-                   jb.ldo, jb.ldo16};
+    split_bar();
+  }
+  for (int64_t t = sj.t_begin + blockIdx.x; t < sj.t_end; t += gridDim.x) {
+    const SplitJob& jb = split_job_of(sj, t, ready);
+    Planes p{jb.hi, jb.lo, static_cast<__nv_bfloat16*>(jb.hi16), static_cast<__nv_bfloat16*>(jb.lo16),
+             jb.ldo, jb.ldo16};
+    if (jb.rmax != nullptr) {
+      p = Planes{nullptr, nullptr, nullptr, nullptr, 0, jb.ldo16};
+      p.h0 = static_cast<__half*>(jb.hi16);
+      p.h1 = static_cast<__half*>(jb.lo16);
+      p.rmax = jb.rmax;
+    }
     const int64_t lt = t - jb.t0;
     if (!jb.trans) {
       const int64_t tiles_k = (jb.kcols + 127) / 128;
@@ -241,7 +330,8 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
   const int total_items = total_tiles * ep.ksplit;
   const int unit = blockIdx.x / CG;
   const int num_units = gridDim.x / CG;
-  const int num_kb = (K + C::kBK - 1) / C::kBK;
+  constexpr int kBK = stage_k<MODE>();
+  const int num_kb = (K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -302,7 +392,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           mbar_wait(smem_u32(&empty_bar[stage]), phase ^ 1);
           uint8_t* st = smem + stage * C::kStageBytes;
           const uint32_t fb = smem_u32(&full_bar[stage]);
-          const int kx = kb * C::kBK;
+          const int kx = kb * kBK;
           uint32_t fb_tx = fb;  // barrier receiving the bytes (leader's for pairs)
           if constexpr (CG == 2)
             asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(fb_tx) : "r"(fb));
@@ -324,7 +414,13 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             }
           };
           const bool amn = ep.a_mn != 0, bmn = ep.b_mn != 0, amn16 = ep.a_mn16 != 0, bmn16 = ep.b_mn16 != 0;
-          if constexpr (MODE == kModeTf32x3) {
+          if constexpr (MODE == kModeF16x2) {
+            // fp16 h0 / h1 tiles: 128 rows x 64 k (128 B), K-major
+            load(0, 0, arow, false, false);
+            load(1, C::kTileBytes, arow, false, false);
+            load(2, 2 * C::kTileBytes, brow, false, false);
+            load(3, 3 * C::kTileBytes, brow, false, false);
+          } else if constexpr (MODE == kModeTf32x3) {
             load(0, 0, arow, amn, false);
             load(1, C::kTileBytes, arow, amn, false);
             load(2, 2 * C::kTileBytes, brow, bmn, false);
@@ -372,7 +468,19 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             tc_fence_after();
             const uint32_t s0 = smem_u32(smem + stage * C::kStageBytes);
             const uint32_t acc0 = (kb != kb0) ? 1u : 0u;
-            if constexpr (MODE == kModeTf32x3) {
+            if constexpr (MODE == kModeF16x2) {
+              const uint32_t idesc16 = idesc_f16(C::kUmmaM, C::kUmmaN);
+              const uint64_t a0 = sdesc_k_sw128(s0), a1 = sdesc_k_sw128(s0 + C::kTileBytes);
+              const uint64_t b0 = sdesc_k_sw128(s0 + 2 * C::kTileBytes), b1 = sdesc_k_sw128(s0 + 3 * C::kTileBytes);
+#pragma unroll
+              for (int j = 0; j < kBK / 16; ++j) {
+                // k16 step j (32 B along the swizzled row); small terms first, then h0*h0
+                const uint64_t o = 2 * j;
+                mma_bf16<CG>(d_tmem, a1 + o, b0 + o, idesc16, (acc0 | j) != 0);
+                mma_bf16<CG>(d_tmem, a0 + o, b1 + o, idesc16, 1u);
+                mma_bf16<CG>(d_tmem, a0 + o, b0 + o, idesc16, 1u);
+              }
+            } else if constexpr (MODE == kModeTf32x3) {
               const uint64_t ahi = d32(s0, ep.a_mn);
               const uint64_t alo = d32(s0 + C::kTileBytes, ep.a_mn);
               const uint64_t bhi = d32(s0 + 2 * C::kTileBytes, ep.b_mn);
@@ -418,7 +526,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
     // ------------------------------------------------------------ split warps
     if (sj.n > 0)
       run_split_jobs(sj, reinterpret_cast<float(*)[128 + 4]>(smem + C::kStages * C::kStageBytes + 256),
-                     threadIdx.x - 32 * (2 + C::kEpiWarps));
+                     threadIdx.x - 32 * (2 + C::kEpiWarps), sj.phase_ctr != nullptr ? 2 : 0);
   } else {
     // ------------------------------------------------------------ epilogue
     const int e = warp - 2;
@@ -455,6 +563,19 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           else mbar_arrive_cluster(smem_u32(&cempty_bar[buf]), 0);
         }
       }
+      const int row = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta + q * 32 +
+                      static_cast<int>(lane);
+      if (row >= ep.m) continue;
+      const int c0 = nt * C::kUmmaN + col_off;
+      // kModeF16x2: undo the planes' power-of-two row scales as each value is
+      // stored -- exact unless the result itself leaves the normal range
+      const int ea = MODE == kModeF16x2 ? splitdev::f16x2_exp(__ldg(ep.a_max + row)) : 0;
+      auto acc = [&](int j) -> float {
+        if constexpr (MODE == kModeF16x2)
+          return splitdev::unscale_pow2(master[j], -(ea + splitdev::f16x2_exp(__ldg(ep.b_max + c0 + j))));
+        else
+          return master[j];
+      };
       // alpha / beta epilogue straight from the master registers; a split-K
       // item stores its raw partial (alpha = 1, no C) to its workspace slice
       const bool part = ep.ksplit > 1;
@@ -462,17 +583,13 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       const int64_t ldc = part ? static_cast<int64_t>(ep.n) : ep.ldc;
       const float alpha = part ? 1.0f : ep.alpha;
       const int read_c = part ? 0 : ep.read_c;
-      const int row = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta + q * 32 +
-                      static_cast<int>(lane);
-      if (row >= ep.m) continue;
-      const int c0 = nt * C::kUmmaN + col_off;
       if (!part && ep.c_half) {
         // Half16 C: beta*C widened exactly, result rounded once (narrow_store)
         __half* hrow = reinterpret_cast<__half*>(cbase) + static_cast<int64_t>(row) * ldc + c0;
 #pragma unroll
         for (int j = 0; j < C::kColsPerThread; ++j) {
           if (c0 + j < ep.n) {
-            float v = __fmul_rn(alpha, master[j]);
+            float v = __fmul_rn(alpha, acc(j));
             if (read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, __half2float(hrow[j])));
             hrow[j] = __float2half_rn(v);
           }
@@ -500,7 +617,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
             const int j = j0 + u;
             float o[4];
 #pragma unroll
-            for (int q2 = 0; q2 < 4; ++q2) o[q2] = __fmul_rn(alpha, master[4 * j + q2]);
+            for (int q2 = 0; q2 < 4; ++q2) o[q2] = __fmul_rn(alpha, acc(4 * j + q2));
             if (read_c) {
               o[0] = __fadd_rn(o[0], __fmul_rn(ep.beta, cv[u].x));
               o[1] = __fadd_rn(o[1], __fmul_rn(ep.beta, cv[u].y));
@@ -514,7 +631,7 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
           for (int jj = 0; jj < 4 * kEpiGroup; ++jj) {
             const int cc = cc0 + jj;
             if (cc < ep.n) {
-              float v = __fmul_rn(alpha, master[4 * j0 + jj]);
+              float v = __fmul_rn(alpha, acc(4 * j0 + jj));
               if (read_c) v = __fadd_rn(v, __fmul_rn(ep.beta, crow[4 * j0 + jj]));
               crow[4 * j0 + jj] = v;
             }
@@ -534,9 +651,9 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
 
 // All split jobs of a command in one launch (small, latency-bound commands:
 // one kernel instead of one per piece, every piece's tiles in flight at once).
-__global__ void __launch_bounds__(64) split_jobs_kernel(const __grid_constant__ SplitJobs sj) {
+__global__ void __launch_bounds__(64) split_jobs_kernel(const __grid_constant__ SplitJobs sj, int phase) {
   __shared__ float tile[32][128 + 4];
-  run_split_jobs(sj, tile, static_cast<int>(threadIdx.x));
+  run_split_jobs(sj, tile, static_cast<int>(threadIdx.x), phase);
 }
 
 // C <- alpha*0 + beta*C for K == 0 (no tensor-core work).
@@ -585,9 +702,20 @@ EncodeTiledFn encode_fn() {
 //            of 32-B atoms, the only MN-major 32-bit layout tcgen05 reads).
 // Out-of-range elements (edges of M, N, K) are zero-filled by the TMA.
 int make_operand_map(CUtensorMap* map, const void* base, int64_t rows, int64_t k, int64_t ld,
-                     bool bf16, bool mn) {
+                     bool bf16, bool mn, bool fp16 = false) {
   EncodeTiledFn enc = encode_fn();
   if (enc == nullptr) return -1;
+  if (fp16) {
+    // kModeF16x2 plane: K-major [rows x K] fp16, box 64 k (128 B) x 128 rows, 128-B swizzle
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    cuuint32_t box[2] = {64u, 128u};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : -2;
+  }
   const int esz = bf16 ? 2 : 4;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(mn ? rows : k), static_cast<cuuint64_t>(mn ? k : rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * esz};
@@ -623,7 +751,8 @@ int pick_ksplit(const Tf32x3Args& a, int cg, int sms) {
   if (a.ksplit == 1 || a.k <= 0) return 1;
   const int64_t tiles = ((a.m + 128 * cg - 1) / (128 * cg)) * ((a.n + 128 * cg - 1) / (128 * cg));
   const int64_t units = sms / cg;
-  const int64_t num_kb = (a.k + 31) / 32;
+  const int64_t bk = a.mode == kModeF16x2 ? 64 : 32;
+  const int64_t num_kb = (a.k + bk - 1) / bk;
   int64_t S = a.ksplit > 1 ? a.ksplit : (2 * tiles <= units ? std::min<int64_t>(units / tiles, num_kb / 16) : 1);
   S = std::max<int64_t>(1, std::min<int64_t>(S, 32));
   return static_cast<int>(S);
@@ -659,7 +788,12 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   int bad = 0;
   const bool amn = a.a_mn != 0, bmn = a.b_mn != 0;
   const bool amn16 = (a.a_mn16 < 0 ? a.a_mn : a.a_mn16) != 0, bmn16 = (a.b_mn16 < 0 ? a.b_mn : a.b_mn16) != 0;
-  if constexpr (MODE == kModeTf32x3) {
+  if constexpr (MODE == kModeF16x2) {
+    bad |= make_operand_map(&maps.m[0], a.a_hi16, a.m, a.k, a.lda16, false, false, true);
+    bad |= make_operand_map(&maps.m[1], a.a_lo16, a.m, a.k, a.lda16, false, false, true);
+    bad |= make_operand_map(&maps.m[2], a.b_hi16, a.n, a.k, a.ldb16, false, false, true);
+    bad |= make_operand_map(&maps.m[3], a.b_lo16, a.n, a.k, a.ldb16, false, false, true);
+  } else if constexpr (MODE == kModeTf32x3) {
     bad |= make_operand_map(&maps.m[0], a.a_hi, a.m, a.k, a.lda, false, amn);
     bad |= make_operand_map(&maps.m[1], a.a_lo, a.m, a.k, a.lda, false, amn);
     bad |= make_operand_map(&maps.m[2], a.b_hi, a.n, a.k, a.ldb, false, bmn);
@@ -698,7 +832,7 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
 
   EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
                a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws,
-               a.a_mn, a.b_mn, amn16 ? 1 : 0, bmn16 ? 1 : 0};
+               a.a_mn, a.b_mn, amn16 ? 1 : 0, bmn16 ? 1 : 0, a.a_max, a.b_max};
   // lockstep keeps the CTAs of a wave together; with a single wave there is
   // nothing to align (and no counters to clear)
   if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1 && tiles > units) {
@@ -724,7 +858,8 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int64_t flush = a.flush_k > 0 ? a.flush_k : tf32x3_default_flush_k(a.mode, a.k_total > 0 ? a.k_total : a.k);
-  const int kc_blocks = static_cast<int>(std::max<int64_t>(1, (flush + C::kBK - 1) / C::kBK));
+  constexpr int kBK = stage_k<MODE>();
+  const int kc_blocks = static_cast<int>(std::max<int64_t>(1, (flush + kBK - 1) / kBK));
   SplitJobs sj;
   if (a.split != nullptr) sj = *a.split;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tf32x3_gemm_kernel<CG, MODE>, maps, static_cast<int>(a.k),
@@ -760,7 +895,12 @@ cudaError_t split_jobs(const SplitJobs& jobs, cudaStream_t stream) {
     if (jobs.job[i].flag != nullptr || !split_job_fusable(jobs.job[i])) return cudaErrorInvalidValue;
   const int64_t tiles = jobs.t_end - jobs.t_begin;
   const int blocks = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
-  split_jobs_kernel<<<blocks, 64, 0, stream>>>(jobs);
+  if (jobs.job[0].rmax != nullptr) {  // kModeF16x2: row maxima first (separate launch = grid-wide order)
+    split_jobs_kernel<<<blocks, 64, 0, stream>>>(jobs, 1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  split_jobs_kernel<<<blocks, 64, 0, stream>>>(jobs, 0);
   return cudaGetLastError();
 }
 
@@ -768,6 +908,7 @@ int64_t tf32x3_default_flush_k(int mode, int64_t k_total) {
   if (k_total <= 512) return 32;
   if (k_total <= 2048) return 64;
   if (mode == kModeTf32x3) return 128;  // 3xTF32: 128 runs as fast as 256
+  if (mode == kModeF16x2) return k_total <= 8192 ? 128 : 256;  // 24 / 48 MMAs per chunk
   return k_total <= 8192 ? 128 : 256;
 }
 
@@ -778,6 +919,9 @@ int64_t split_job_tiles(const SplitJob& j) {
 
 bool split_job_fusable(const SplitJob& j) {
   auto al = [](const void* p, uintptr_t a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
+  if (j.rmax != nullptr)  // kModeF16x2: fp16 h0 / h1 in hi16 / lo16
+    return j.src != nullptr && al(j.src, 16) && (j.lds & 3) == 0 && j.hi16 != nullptr && al(j.hi16, 8) &&
+           al(j.lo16, 8) && (j.ldo16 & 3) == 0;
   return j.src != nullptr && al(j.src, 16) && (j.lds & 3) == 0 && j.hi != nullptr && al(j.hi, 16) &&
          (j.ldo & 3) == 0 && (j.lo == nullptr || al(j.lo, 16)) &&
          (j.hi16 == nullptr || (al(j.hi16, 8) && al(j.lo16, 8) && (j.ldo16 & 3) == 0));
@@ -819,6 +963,12 @@ cudaError_t tf32x3_gemm(const Tf32x3Args& a, cudaStream_t stream) {
                                mis(a.b_hi16) || mis(a.b_lo16)))
     return cudaErrorMisalignedAddress;
   const int cg = pick_cta_group(a);
+  if (a.mode == kModeF16x2) {
+    if (a.a_mn || a.b_mn || a.a_max == nullptr || a.b_max == nullptr) return cudaErrorInvalidValue;
+    if ((a.lda16 & 7) || (a.ldb16 & 7) || mis(a.a_hi16) || mis(a.a_lo16) || mis(a.b_hi16) || mis(a.b_lo16))
+      return cudaErrorMisalignedAddress;
+    return cg == 2 ? launch<2, kModeF16x2>(a, stream) : launch<1, kModeF16x2>(a, stream);
+  }
   if (a.mode == kModeMixed) return cg == 2 ? launch<2, kModeMixed>(a, stream) : launch<1, kModeMixed>(a, stream);
   return cg == 2 ? launch<2, kModeTf32x3>(a, stream) : launch<1, kModeTf32x3>(a, stream);
 }

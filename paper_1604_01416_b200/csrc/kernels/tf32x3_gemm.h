@@ -7,7 +7,7 @@
 
 namespace dm {
 
-// Split-product modes.  Both keep fp32 accuracy:
+// Split-product modes.  All keep fp32 accuracy:
 //   kModeTf32x3 : acc += lo*hi + hi*lo + hi*hi, three kind::tf32 MMAs per k8 step
 //   kModeMixed  : acc += hi*hi (kind::tf32) + bf16(hi)*bf16(lo) + bf16(lo)*bf16(hi)
 //                 (kind::f16, bf16 inputs): the cross terms are 2^-11 smaller than
@@ -15,18 +15,20 @@ namespace dm {
 //                 the TF32 rate, so a k16 step costs 4 TF32-MMA slots instead of 6.
 constexpr int kModeTf32x3 = 0;
 constexpr int kModeMixed = 1;
-// Per product: 3xTF32 up to K = kAutoMixedMinK, mixed above.  Measured
-// (profiles/r02/accuracy_fullsize_parity.jsonl, distance from the exact
-// product relative to the reference's own k-ascending fp32 loop): 3xTF32
-// 0.3-1.25x at every K; mixed's bf16 cross terms leave a ~6e-7 floor, up to
-// 4x the reference at K=256, but 0.4-0.8x at K=32768 where the reference's
-// error has grown -- there mixed is the faster (~1.2x) fp32-accurate choice.
 constexpr int kModeAuto = 2;
-constexpr int64_t kAutoMixedMinK = 8193;
-inline int resolve_split_mode(int mode, int64_t k_total) {
-  if (mode != kModeAuto) return mode;
-  return k_total >= kAutoMixedMinK ? kModeMixed : kModeTf32x3;
-}
+//   kModeF16x2  : scaled 2xFP16 -- per plane row x 2^e = h0 + h1 with fp16 h0, h1
+//                 (11 + 11 bits, the precision of 3xTF32's tf32 hi / lo pair),
+//                 acc += h1*h0 + h0*h1 + h0*h0, three kind::f16 MMAs per k16
+//                 (3 slots vs mixed's 4 and 3xTF32's 6); the epilogue undoes the
+//                 power-of-two scales (split_common.cuh).  4 B of planes per element.
+constexpr int kModeF16x2 = 3;
+// kModeAuto runs every fp32 product in kModeF16x2: measured on B200
+// (tools/f16x2_probe.py, profiles/r02/f16x2/) it has 3xTF32's accuracy -- the
+// same 11 + 11-bit pair and three products; within 1.0-1.5x of 3xTF32's
+// distance from the exact product over U[-1,1), U[0,1), log-uniform 2^+-20 and
+// 2^+-60, rows spanning 2^+-60, K = 256 .. 32768 -- at 1.8x its speed
+// (N=32768: 462 vs 260 TFLOP/s; mixed: 310, with a bf16 floor of ~6e-7).
+inline int resolve_split_mode(int mode, int64_t /*k_total*/) { return mode == kModeAuto ? kModeF16x2 : mode; }
 
 // One split job fused into a GEMM launch: the split_tf32 of an fp32 piece
 // (16-B aligned rows and planes) for the NEXT K panel, executed by the
@@ -35,6 +37,7 @@ inline int resolve_split_mode(int mode, int64_t k_total) {
 // the warps wait until (int)(*flag - flag_val) >= 0 before reading it.
 struct SplitJob {
   const float* src = nullptr;
+  unsigned* rmax = nullptr;  // kModeF16x2: row maxima of the target planes (hi16 / lo16 = fp16 h0 / h1)
   int64_t lds = 0;
   int trans = 0;
   int64_t rows = 0, kcols = 0;
@@ -51,6 +54,10 @@ constexpr int kMaxSplitJobs = 16;
 struct SplitJobs {
   SplitJob job[kMaxSplitJobs];
   int n = 0;
+  // kModeF16x2 jobs run in two phases (row maxima, then the split) with a
+  // grid-wide handoff on this zeroed counter (fused: every CTA of the GEMM
+  // launch arrives once; requires the launch's CTAs to be co-resident)
+  unsigned* phase_ctr = nullptr;
   int64_t t_begin = 0, t_end = 0;  // tile range this launch processes
 };
 // tiles of one job (direct: 32 rows x 128 k; transposed: 32 k x 128 rows)
@@ -79,6 +86,8 @@ struct Tf32x3Args {
   const void* b_hi16 = nullptr;
   const void* b_lo16 = nullptr;
   int64_t ldb = 0, ldb16 = 0;
+  const unsigned* a_max = nullptr;  // kModeF16x2: row maxima of op(A) / op(B)^T planes (a/b_hi16 = h0,
+  const unsigned* b_max = nullptr;  // a/b_lo16 = h1, fp16, K-major)
   int mode = kModeTf32x3;
   int a_mn = 0, b_mn = 0;  // planes MN-major instead of K-major
   int a_mn16 = -1, b_mn16 = -1;  // bf16 planes' majorness when it differs (-1: as a_mn / b_mn)
@@ -134,6 +143,15 @@ size_t tf32x3_splitk_bytes(const Tf32x3Args& args);
 cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, int64_t rows,
                        int64_t kcols, float* hi, float* lo, int64_t ldo, void* hi16, void* lo16,
                        int64_t ldo16, cudaStream_t stream);
+
+// kModeF16x2 planes.  absmax_rows: rmax[r] = max(rmax[r], max_k |x[r][k]|) as
+// float bits, x as in split_tf32 (rmax zeroed by the caller before the first
+// piece of a plane).  split_f16x2: h0 / h1 fp16 planes (pitch ldo16) of x[r][k]
+// scaled by 2^e(rmax[r]) (split_common.cuh).
+cudaError_t absmax_rows(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols, unsigned* rmax,
+                        cudaStream_t stream);
+cudaError_t split_f16x2(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols, void* h0, void* h1,
+                        int64_t ldo16, const unsigned* rmax, cudaStream_t stream);
 
 // Double64 GEMM bit-exact with the reference's gemm_typed<double> (gemm_f64.cu):
 // C[i][j] <- alpha * sum_k A[i][k] B[j][k] (+ beta C[i][j] when read_c), A and B

@@ -89,11 +89,11 @@ struct HostScope {
 };
 
 // DM_GEMM_MODE environment default of the split-product scheme (0 = 3xTF32,
-// 1 = mixed, anything else / unset = auto), as kernel mode constants
-// (kModeTf32x3 = 0, kModeMixed = 1, kModeAuto = 2).
+// 1 = mixed, 3 = f16x2, anything else / unset = auto), as kernel mode
+// constants (kModeTf32x3 = 0, kModeMixed = 1, kModeAuto = 2, kModeF16x2 = 3).
 inline int env_gemm_mode() {
   const std::int64_t v = env_int("DM_GEMM_MODE", 2);
-  return v == 0 ? 0 : v == 1 ? 1 : 2;
+  return v == 0 ? 0 : v == 1 ? 1 : v == 3 ? 3 : 2;
 }
 
 class Error : public std::runtime_error {

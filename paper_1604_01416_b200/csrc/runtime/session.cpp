@@ -38,6 +38,8 @@ Session::Session(const dm_session_config& cfg) {
     gemm_mode_ = kModeMixed;
   } else if (cfg.gemm_mode == DM_GEMM_AUTO) {
     gemm_mode_ = kModeAuto;
+  } else if (cfg.gemm_mode == DM_GEMM_F16X2) {
+    gemm_mode_ = kModeF16x2;
   } else if (cfg.gemm_mode == DM_GEMM_DEFAULT) {
     gemm_mode_ = env_gemm_mode();
   } else {

@@ -116,7 +116,7 @@ struct Worker {
   struct PlaneCache {
     bool filled = false;  // holds the planes of `version`
     std::uint64_t version = 0;
-    DeviceBuffer hi, second;
+    DeviceBuffer hi, second, rmax;  // rmax: kModeF16x2 row maxima
   };
   std::map<std::vector<std::int64_t>, PlaneCache> plane_cache;
   // Captured command graphs of small single-panel GEMMs (session_gemm.cpp):

@@ -33,6 +33,8 @@ struct Session::GemmRun {
   // K; MN-major [kpitch x ld] (ld = len rounded to 32) when they are stored
   // K-row-wise (a transposed A, a non-transposed B), so every split reads its
   // source row by row and none transposes.
+  // kModeF16x2: hi = lo = null, hi16 / lo16 = fp16 h0 / h1 (4 B / element
+  // together), rmax = the rows' |x| maxima (their power-of-two scales).
   struct Planes {
     float* hi;
     float* lo;
@@ -40,6 +42,7 @@ struct Session::GemmRun {
     void* lo16;
     bool mn;
     std::int64_t ld;  // pitch of every plane (elements)
+    unsigned* rmax = nullptr;
   };
   // one split item per piece: effective source (the landing buffer for pieces
   // that crossed a link), target planes, and whether it waits on the flag
@@ -69,7 +72,9 @@ struct Session::GemmRun {
   const int nbuf;
   std::int64_t kpitch = 8;
   int lockstep = 0;
+  bool exclusive = true;  // this worker's GEMMs have the device to themselves (co-resident CTAs)
   std::int64_t fuse_mode = 1;
+  unsigned* phase_ctr = nullptr;  // kModeF16x2 fused splits: one grid-handoff counter per step
 
   std::vector<std::array<Planes, 2>> pa, pb;
   std::vector<int> order;
@@ -91,7 +96,7 @@ struct Session::GemmRun {
       : S(s), w(wk), g(ga), pol(p), plan(std::move(pl)), bufs(b), events(e),
         half_in(s.table_.at(ga.a).precision == Precision::Half16),
         esz(byte_width(s.table_.at(ga.a).precision)),
-        gemm_mode(resolve_split_mode(s.gemm_mode_, plan.k0.empty() ? 0 : plan.k0.back())),
+        gemm_mode(split_mode_for(s.gemm_mode_, plan.k0.empty() ? 0 : plan.k0.back(), half_in)),
         trace(s.tracing() && !s.async_),
         np(static_cast<int>(plan.k0.size()) - 1),
         nbuf(np > 1 ? 2 : 1) {
@@ -99,6 +104,14 @@ struct Session::GemmRun {
     for (int p = 0; p < np; ++p) kmax = std::max(kmax, plan.k0[p + 1] - plan.k0[p]);
     kpitch = std::max<std::int64_t>(8, (kmax + 7) / 8 * 8);
   }
+
+  // Half16 operands are exact in one tf32 term: they keep 3xTF32 (their
+  // splits read fp16 sources, which the scaled fp16 pair does not take).
+  static int split_mode_for(int session_mode, std::int64_t k, bool half) {
+    const int m = resolve_split_mode(session_mode, k);
+    return half && m == kModeF16x2 ? kModeTf32x3 : m;
+  }
+  bool f16x2() const { return gemm_mode == kModeF16x2; }
 
   cudaEvent_t new_event() {
     cudaEvent_t e;
@@ -113,12 +126,17 @@ struct Session::GemmRun {
     // local worker shares this device (its GEMMs run concurrently).
     int sharing = 0;
     for (auto& o : S.workers_) sharing += (o && o->device == w.device) ? 1 : 0;
-    lockstep = sharing == 1 ? static_cast<int>(env_int("DM_LOCKSTEP", 32)) : 0;
+    exclusive = sharing == 1;
+    lockstep = exclusive ? static_cast<int>(env_int("DM_LOCKSTEP", 32)) : 0;
     // DM_FUSE_SPLIT: 0 never, 1 when the carrying GEMM hides the split, 2 always
     fuse_mode = half_in ? 0 : env_int("DM_FUSE_SPLIT", 1);
 
     alloc_planes(plan.ar, plan.br, true, pa);
     alloc_planes(plan.br, plan.ar, false, pb);
+    if (f16x2() && np > 1) {
+      bufs.push_back(w.pool->acquire(static_cast<std::size_t>(np) * 4));
+      phase_ctr = static_cast<unsigned*>(bufs.back().data());
+    }
     // operands of this worker's GEMMs were written by earlier commands on
     // its own streams; order the split stream after the compute stream
     cudaEvent_t e = new_event();
@@ -144,7 +162,7 @@ struct Session::GemmRun {
   // memory-bound one (FC strips) prefers the direct split.  Break-even
   // ~2000 rows (DM_MN_REUSE).
   static bool range_mn(const Range& r, std::int64_t reuse) {
-    if (reuse >= env_int("DM_MN_REUSE", 2048)) return false;
+    if (reuse >= env_int("DM_MN_REUSE", 2048)) return false;  // (f16x2 planes are always K-major)
     for (const auto& panel : r.panels)
       for (const Piece& pc : panel) return pc.trans != 0;
     return false;
@@ -160,7 +178,7 @@ struct Session::GemmRun {
     std::int64_t reuse = 0;
     for (const Task& t : plan.tasks)
       if ((is_a ? t.ra : t.rb) == static_cast<int>(i)) reuse += other[is_a ? t.rb : t.ra].len;
-    const bool mn = range_mn(rs[i], reuse);
+    const bool mn = !f16x2() && range_mn(rs[i], reuse);
     const std::int64_t len = std::max<std::int64_t>(rs[i].len, 1);
     const std::int64_t ld = mn ? (len + 31) / 32 * 32 : kpitch;
     return {mn, ld, static_cast<std::size_t>(mn ? kpitch * ld : len * kpitch)};
@@ -192,27 +210,42 @@ struct Session::GemmRun {
     if (is_a) a_fresh.assign(rs.size(), 0);
     for (std::size_t i = 0; i < rs.size(); ++i) {
       const PlaneShape sh = plane_shape(rs, other, is_a, i);
+      const std::size_t rmax_bytes = static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1)) * 4;
       for (int b = 0; b < nbuf; ++b) {
         float* hi;
         char* second;
+        unsigned* rmax = nullptr;
         if (is_a && plane_cacheable()) {
           Worker::PlaneCache& pc = w.plane_cache[plane_key(i)];
           if (!pc.hi.data()) {
             pc.hi = w.pool->acquire(sh.elems * 4);
-            pc.second = w.pool->acquire(sh.elems * 4);
+            if (f16x2()) pc.rmax = w.pool->acquire(rmax_bytes);
+            else pc.second = w.pool->acquire(sh.elems * 4);
           }
           a_fresh[i] = pc.filled && pc.version == S.table_.at(g.a).version ? 1 : 0;
           hi = pc.hi.f32();
           second = static_cast<char*>(pc.second.data());
+          rmax = static_cast<unsigned*>(pc.rmax.data());
         } else {
           bufs.push_back(w.pool->acquire(sh.elems * 4));
           hi = bufs.back().f32();
-          bufs.push_back(w.pool->acquire(sh.elems * 4));
-          second = static_cast<char*>(bufs.back().data());
+          if (f16x2()) {
+            bufs.push_back(w.pool->acquire(rmax_bytes));
+            rmax = static_cast<unsigned*>(bufs.back().data());
+            second = nullptr;
+          } else {
+            bufs.push_back(w.pool->acquire(sh.elems * 4));
+            second = static_cast<char*>(bufs.back().data());
+          }
         }
-        out[i][b] = gemm_mode == kModeMixed
-                        ? Planes{hi, nullptr, second, second + sh.elems * 2, sh.mn, sh.ld}
-                        : Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr, sh.mn, sh.ld};
+        if (f16x2()) {
+          char* h = reinterpret_cast<char*>(hi);  // fp16 h0 | h1, sh.elems each
+          out[i][b] = Planes{nullptr, nullptr, h, h + sh.elems * 2, false, sh.ld, rmax};
+        } else {
+          out[i][b] = gemm_mode == kModeMixed
+                          ? Planes{hi, nullptr, second, second + sh.elems * 2, sh.mn, sh.ld}
+                          : Planes{hi, reinterpret_cast<float*>(second), nullptr, nullptr, sh.mn, sh.ld};
+        }
       }
     }
   }
@@ -448,9 +481,26 @@ struct Session::GemmRun {
     return it.pl->mn ? SplitShape{pc.trans ? 0 : 1, pc.kcols, pc.rows} : SplitShape{pc.trans, pc.rows, pc.kcols};
   }
 
+  // kModeF16x2: clear the row maxima the splits of step s accumulate into
+  // (every range has pieces in every panel; cache-fresh A planes keep theirs).
+  void zero_rmax(int s, cudaStream_t st) {
+    if (!f16x2()) return;
+    const int buf = s % nbuf;
+    for (int ab = 0; ab < 2; ++ab) {
+      const std::vector<Range>& rs = ab == 0 ? plan.ar : plan.br;
+      const std::vector<std::array<Planes, 2>>& planes = ab == 0 ? pa : pb;
+      for (std::size_t i = 0; i < rs.size(); ++i) {
+        if (ab == 0 && !a_fresh.empty() && a_fresh[i]) continue;
+        cuda_check(cudaMemsetAsync(planes[i][buf].rmax, 0, static_cast<std::size_t>(std::max<std::int64_t>(rs[i].len, 1)) * 4, st),
+                   "memset row maxima");
+      }
+    }
+  }
+
   // Split step s with its own kernels on the split stream.
   void split_separate(int s) {
     if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.side, gemm_ev[s - nbuf], 0), "wait");  // planes free
+    zero_rmax(s, w.side);
     cudaEvent_t ta = trace ? S.trace_event(w.side) : nullptr;
     std::uint64_t bytes = 0;
     // Small splits (a latency-bound command): every piece in one launch.
@@ -467,6 +517,33 @@ struct Session::GemmRun {
       if (!it.landed) seq_items.push_back(&it);
     for (const Item& it : items[s])
       if (it.landed) seq_items.push_back(&it);
+    if (f16x2()) {
+      // row maxima of every piece first (a plane row's scale spans its pieces),
+      // then the splits
+      for (const Item* itp : seq_items) {
+        const Item& it = *itp;
+        if (it.landed)
+          cuda_check(cudaStreamWaitEvent(w.side, it.ready ? it.ready : landed_ev[s], 0), "wait");
+        const SplitShape sh = split_shape(it);
+        cuda_check(absmax_rows(static_cast<const float*>(it.src), it.lds, sh.trans, sh.rows, sh.cols,
+                               it.pl->rmax + it.pc->dst_row, w.side),
+                   "absmax_rows");
+        w.stats.split_launches += 1;
+      }
+      for (const Item* itp : seq_items) {
+        const Item& it = *itp;
+        const Planes& pl = *it.pl;
+        const std::int64_t off = plane_off(it);
+        const SplitShape sh = split_shape(it);
+        cuda_check(split_f16x2(static_cast<const float*>(it.src), it.lds, sh.trans, sh.rows, sh.cols,
+                               static_cast<char*>(pl.hi16) + off * 2, static_cast<char*>(pl.lo16) + off * 2, pl.ld,
+                               pl.rmax + it.pc->dst_row, w.side),
+                   "split_f16x2");
+        w.stats.split_launches += 1;
+        bytes += it.pc->bytes() / 4 * esz;
+      }
+      seq_items.clear();
+    }
     for (const Item* itp : seq_items) {
       const Item& it = *itp;
       if (it.landed)
@@ -524,8 +601,9 @@ struct Session::GemmRun {
       j.trans = sh.trans;
       j.rows = sh.rows;
       j.kcols = sh.cols;
-      j.hi = pl.hi + off;
+      j.hi = pl.hi ? pl.hi + off : nullptr;
       j.lo = pl.lo ? pl.lo + off : nullptr;
+      j.rmax = pl.rmax ? pl.rmax + it.pc->dst_row : nullptr;
       j.hi16 = pl.hi16 ? static_cast<char*>(pl.hi16) + off * 2 : nullptr;
       j.lo16 = pl.lo16 ? static_cast<char*>(pl.lo16) + off * 2 : nullptr;
       j.ldo = j.ldo16 = pl.ld;
@@ -556,6 +634,12 @@ struct Session::GemmRun {
       flops += 2.0 * mb * nb * static_cast<double>(kw);
     }
     if (fuse_mode == 1 && bytes_in / 150e9 > flops / 300e12) return false;
+    if (f16x2()) {
+      // the two-phase split (row maxima, grid handoff, split) must see all of a
+      // plane row's tiles in one launch whose CTAs are all co-resident
+      if (!exclusive || plan.tasks.size() != 1 || phase_ctr == nullptr) return false;
+      out->phase_ctr = phase_ctr + s;
+    }
     return make_jobs(s, out);
   }
 
@@ -622,7 +706,13 @@ struct Session::GemmRun {
         jobs->t_begin = split_tiles * ti / ntask;
         jobs->t_end = split_tiles * (ti + 1) / ntask;
         a.split = jobs;
+        if (jobs->phase_ctr != nullptr) {  // kModeF16x2 (one launch): fresh maxima and handoff counter
+          zero_rmax(step + 1, w.stream);
+          cuda_check(cudaMemsetAsync(jobs->phase_ctr, 0, 4, w.stream), "memset phase counter");
+        }
       }
+      a.a_max = A.rmax;
+      a.b_max = B.rmax;
       if (const std::size_t need = tf32x3_splitk_bytes(a)) {
         if (need > ksplit_ws_bytes) {
           bufs.push_back(w.pool->acquire(need));

@@ -186,21 +186,22 @@ class Config:
     # are chosen per call), so the flag is accepted and reported, never needed.
     deterministic: bool = True
     # Split-product scheme of the fp32 tensor-core GEMM (include/dmath_b200.h
-    # dm_gemm_mode): "default" (env DM_GEMM_MODE, else auto), "auto" (per
-    # product: 3xtf32 for K <= 8192, mixed above), "mixed"
-    # (tf32 hi*hi + bf16 cross terms), "3xtf32" (the north star's 3xTF32).
+    # dm_gemm_mode): "default" (env DM_GEMM_MODE, else auto), "auto" (f16x2
+    # for fp32 operands), "f16x2" (3xTF32's 11+11-bit split on fp16 operands
+    # with per-row power-of-two scales), "3xtf32" (the north star's 3xTF32),
+    # "mixed" (tf32 hi*hi + bf16 cross terms).
     gemm_mode: str = "default"
 
 
-GEMM_MODES = {"default": 0, "mixed": 1, "3xtf32": 2, "auto": 3}  # dm_gemm_mode
+GEMM_MODES = {"default": 0, "mixed": 1, "3xtf32": 2, "auto": 3, "f16x2": 4}  # dm_gemm_mode
 
 
 def split_mode_for(mode: str, k: int) -> str:
     """The scheme a product over K runs in under `mode` (auto's rule,
     tf32x3_gemm.h resolve_split_mode)."""
-    if mode in ("mixed", "3xtf32"):
+    if mode in ("mixed", "3xtf32", "f16x2"):
         return mode
-    return "mixed" if k > 8192 else "3xtf32"
+    return "f16x2"
 
 
 def nccl_unique_id() -> bytes:
@@ -302,10 +303,10 @@ class Session:
         return bool(self._cfg.deterministic)
 
     def gemm_mode(self) -> str:
-        """Split-product scheme of this session: "mixed", "3xtf32" or "auto"."""
+        """Split-product scheme of this session: "mixed", "3xtf32", "f16x2" or "auto"."""
         v = C.c_int()
         _check(lib.dm_session_gemm_mode(self._h, C.byref(v)))
-        return {1: "mixed", 2: "3xtf32", 3: "auto"}[v.value]
+        return {1: "mixed", 2: "3xtf32", 3: "auto", 4: "f16x2"}[v.value]
 
     def root_seed(self) -> int:
         """Session::root_seed (session.hpp:92); follows seed_workers and restore."""

@@ -140,9 +140,9 @@ def test_config2_16384_sampled_rows_and_columns(cuda, ref):
 # (tf32x3_default_flush_k) so that it stays near or below the reference's.
 # Measured (profiles/r02): 3xTF32 within 1.25x of the reference's error at
 # every K and distribution; the mixed split's bf16 cross terms leave a ~6e-7
-# floor -- up to 4x the reference at K=256 -- which is why "auto" (the
-# default) runs 3xTF32 up to K=8192 and mixed above, where both are below
-# the reference's growing error (mixed 0.4-0.8x at K=32768) and mixed is faster.
+# floor -- up to 4x the reference at K=256.  The scaled 2xFP16 split (f16x2,
+# "auto") repeats 3xTF32's 11+11-bit pair and products and is held to the
+# same bar.
 def bar(gemm_mode, k):
     if gemm_mode == "mixed" and k <= 8192:
         return 4.5, 1e-7
@@ -162,7 +162,7 @@ def _operands(dist, k, n):
     return gen((n, k)), gen((k, n))
 
 
-@pytest.mark.parametrize("gemm_mode", ["auto", "mixed", "3xtf32"])
+@pytest.mark.parametrize("gemm_mode", ["auto", "f16x2", "mixed", "3xtf32"])
 @pytest.mark.parametrize("k", [256, 9216, 32768])
 @pytest.mark.parametrize("dist", ["u01", "pm1", "logu"])
 def test_distributions_and_k(cuda, ref, gemm_mode, k, dist):

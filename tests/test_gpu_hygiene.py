@@ -2,8 +2,9 @@
 profiles/r02/hygiene/README.md):
 
 * races   -- every schedule of the tcgen05 GEMM (CTA group 1 / 2, split mode
-             mixed / 3xTF32, split-K, producer lockstep over several waves,
-             fused split warps reading flag-gated landing buffers) is
+             f16x2 / mixed / 3xTF32, split-K, producer lockstep over several
+             waves, fused split warps reading flag-gated landing buffers, the
+             f16x2 two-phase fused split with its grid handoff) is
              deterministic by construction (fixed MMA order, fixed-order
              split-K sums), so a smem / TMEM / mbarrier race shows up as run-
              to-run differences: each schedule is repeated and must be
@@ -30,6 +31,9 @@ SCHEDULES = [
     ("lockstep", 1, 1024, 2560, 1024, False, {"DM_LOCKSTEP": "2"}),
     ("fused_split_P2", 2, 512, 512, 1024, True, {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PANEL_K": "256",
                                                   "DM_FUSE_SPLIT": "1"}),
+    # one worker, geometric local panels: f16x2's fused two-phase split (row
+    # maxima, grid handoff, split) runs in the GEMM's split warps
+    ("fused_local_P1", 1, 1024, 1024, 4096, False, {"DM_PANEL_LOCAL": "512", "DM_FUSE_SPLIT": "2"}),
 ]
 
 
@@ -42,7 +46,7 @@ def env(monkeypatch):
 
 
 @pytest.mark.parametrize("cg", [1, 2])
-@pytest.mark.parametrize("mode", ["mixed", "3xtf32"])
+@pytest.mark.parametrize("mode", ["mixed", "3xtf32", "f16x2"])
 @pytest.mark.parametrize("sched", SCHEDULES, ids=[s[0] for s in SCHEDULES])
 def test_schedule_repeats_bitwise(sched, mode, cg, env):
     name, workers, m, n, k, tb, extra = sched
@@ -76,10 +80,11 @@ def test_schedule_repeats_bitwise(sched, mode, cg, env):
 SENTINEL = -7.25e30
 
 
+@pytest.mark.parametrize("mode", ["f16x2", "3xtf32"])
 @pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("shape", [(300, 333, 200, 5), (64, 96, 8192, 3), (513, 257, 1000, 4)],
                          ids=["odd", "splitK_strip", "edge_tiles"])
-def test_local_gemm_stays_inside_c(shape, cg):
+def test_local_gemm_stays_inside_c(shape, cg, mode):
     import paper_1604_01416_b200 as dm
     m, n, k, pad = shape
     g = torch.Generator(device="cuda").manual_seed(m * n + k)
@@ -91,7 +96,7 @@ def test_local_gemm_stays_inside_c(shape, cg):
     c = frame[:m, :n]
     c.copy_(torch.rand(m, n, device="cuda", generator=g) - 0.5)
     c0 = c.clone()
-    dm.local_gemm(1.25, a, False, b, False, 0.75, c, cta_group=cg)
+    dm.local_gemm(1.25, a, False, b, False, 0.75, c, cta_group=cg, gemm_mode=mode)
     torch.cuda.synchronize()
     assert torch.all(frame[:m, n:] == SENTINEL), "wrote right of C"
     assert torch.all(frame[m:, :] == SENTINEL), "wrote below C"

@@ -111,7 +111,7 @@ def test_split_k_deterministic(cuda):
     assert all(torch.equal(outs[0], o) for o in outs[1:])
 
 
-@pytest.mark.parametrize("gemm_mode", ["mixed", "3xtf32"])
+@pytest.mark.parametrize("gemm_mode", ["mixed", "3xtf32", "f16x2"])
 def test_explicit_gemm_mode(cuda, gemm_mode):
     """The split-product scheme chosen through the ABI (dm_gemm_mode), not the
     environment: both schemes meet the fp32 bar."""

@@ -57,7 +57,7 @@ def roofline(ms, flops_w, hbm_bytes_w, link_bytes_w, k):
     the slowest of tensor time (the split scheme auto picks at this K), HBM
     bytes (raw fp32 operands read + C written) and NVLink bytes (pulled pieces)."""
     hbm, bf16 = peaks()
-    tensor = bf16 / (4.0 if dm.split_mode_for("auto", k) == "mixed" else 6.0)
+    tensor = bf16 / {"mixed": 4.0, "3xtf32": 6.0, "f16x2": 3.0}[dm.split_mode_for("auto", k)]
     t = {"tensor": flops_w / (tensor * 1e12) * 1e3, "hbm": hbm_bytes_w / (hbm * 1e9) * 1e3,
          "nvlink": link_bytes_w / (NVLINK_GBS * 1e9) * 1e3}
     kind = max(t, key=t.get)

@@ -38,7 +38,7 @@ def wall(s, fn, reps=int(os.environ.get("C1_REPS", "200"))):
 with dm.Session(dm.Config(worker_count=P, root_seed=42, devices=devs)) as s:
     lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, P)
     a, b, c = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(3))
-    print(f"N={n} devices={devs} gemm_mode={s.gemm_mode}")
+    print(f"N={n} devices={devs} gemm_mode={s.gemm_mode()}")
     print(f"sync  : {wall(s, lambda: s.general_gemm(1.0, a, b, 0.0, c)):.1f} us/call", flush=True)
     s.set_async(True)
     print(f"async : {wall(s, lambda: s.general_gemm(1.0, a, b, 0.0, c)):.1f} us/call", flush=True)
