@@ -633,7 +633,10 @@ struct Session::GemmRun {
       auto [mb, nb] = block_extent(S.table_.at(g.c).layout.grid, t.c);
       flops += 2.0 * mb * nb * static_cast<double>(kw);
     }
-    if (fuse_mode == 1 && bytes_in / 150e9 > flops / 300e12) return false;
+    // split-warp input rate and GEMM rate (DM_FUSE_SPLIT_GBS / DM_FUSE_GEMM_TFLOPS)
+    const double split_bps = static_cast<double>(env_int("DM_FUSE_SPLIT_GBS", 150)) * 1e9;
+    const double gemm_fps = static_cast<double>(env_int("DM_FUSE_GEMM_TFLOPS", f16x2() ? 450 : 300)) * 1e12;
+    if (fuse_mode == 1 && bytes_in / split_bps > flops / gemm_fps) return false;
     if (f16x2()) {
       // the two-phase split (row maxima, grid handoff, split) must see all of a
       // plane row's tiles in one launch whose CTAs are all co-resident

@@ -34,9 +34,10 @@ def _pipeline_on(monkeypatch):
     monkeypatch.setenv("DM_PIPELINE_MIN_GFLOP", "0")
 
 
-def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77, devices=None):
+def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77, devices=None, gemm_mode="default"):
     ta, tb = bool(trans & 1), bool(trans & 2)
-    with Session(Config(worker_count=P, root_seed=seed + trans, devices=devices or [0] * P)) as s:
+    with Session(Config(worker_count=P, root_seed=seed + trans, devices=devices or [0] * P,
+                        gemm_mode=gemm_mode)) as s:
         lay = make_layout(LayoutKind.Checkerboard2D, n, n, blk[0], blk[1], P)
         a, b, c = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(3))
         A, B, C0 = s.gather(a), s.gather(b), s.gather(c)
@@ -47,17 +48,36 @@ def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77, devices=None):
         return relfro(got, ref_gemm(alpha, A, ta, B, tb, beta, C0)), splits
 
 
+@pytest.mark.parametrize("gemm_mode", ["f16x2", "mixed", "3xtf32"])
 @pytest.mark.parametrize("trans", [0, 1, 2, 3])
 @pytest.mark.parametrize("lead", [0, 128])
-def test_panels_fused_vs_separate(cuda, monkeypatch, trans, lead):
+def test_panels_fused_vs_separate(cuda, monkeypatch, trans, lead, gemm_mode):
     monkeypatch.setenv("DM_PANEL_K", "512")
     monkeypatch.setenv("DM_LEAD_PANEL_K", str(lead))
     res = {}
     for fuse in (2, 0):  # 2: fuse even where the GEMM is too short to hide it
         monkeypatch.setenv("DM_FUSE_SPLIT", str(fuse))
-        res[fuse] = run_case(4, 1536, (768, 768), trans)
+        res[fuse] = run_case(4, 1536, (768, 768), trans, gemm_mode=gemm_mode)
         assert res[fuse][0] <= TOL, (fuse, res[fuse])
-    # fused panels are split inside the GEMM launches: fewer split kernels
+    if gemm_mode == "f16x2":
+        # the two-phase fused split (row maxima, grid handoff, split) needs all
+        # CTAs of its launch co-resident: never fused while 4 workers share the GPU
+        assert res[2][1] == res[0][1]
+    else:
+        # fused panels are split inside the GEMM launches: fewer split kernels
+        assert res[2][1] < res[0][1]
+
+
+@pytest.mark.parametrize("trans", [0, 1, 2, 3])
+def test_f16x2_fused_two_phase_split(cuda, monkeypatch, trans):
+    # one worker owning its GPU, geometric local panels: panels after the first
+    # are split by the GEMM's split warps in two phases (fewer split kernels)
+    monkeypatch.setenv("DM_PANEL_LOCAL", "256")
+    res = {}
+    for fuse in (2, 0):
+        monkeypatch.setenv("DM_FUSE_SPLIT", str(fuse))
+        res[fuse] = run_case(1, 1280, (1280, 1280), trans, gemm_mode="f16x2")
+        assert res[fuse][0] <= TOL, (fuse, res[fuse])
     assert res[2][1] < res[0][1]
 
 

@@ -24,10 +24,17 @@ def test_launch_shares_reproduce(tmp_path):
 
 
 def test_traffic_summary_is_the_bench_kernel():
-    d = json.load(open(os.path.join(ROOT, "profiles", "ncu_gemm_summary.json")))
-    assert "32768^3" in d["problem"] and "tf32x3_gemm_kernel<2, 1>" in d["kernel"]
-    m = d["metrics"]
-    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Tbyte": 1e12, "byte": 1}
-    dram = sum(float(m[k]["value"]) * scale[m[k]["unit"]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-    assert abs(dram - d["dram_bytes_per_launch"]) / dram < 1e-6
-    assert d["algorithmic_bytes_per_launch"] == 8 * 2 * 32768 ** 2 + 4 * 32768 ** 2
+    """profiles/ncu_gemm_summary.json is the default (f16x2) N=32768 launch; the
+    mixed and 3xTF32 captures sit beside it (ncu_gemm_summary_<mode>.json)."""
+    for name, mode, tmpl, plane in [("ncu_gemm_summary.json", "f16x2", "<2, 3>", 4),
+                                    ("ncu_gemm_summary_mixed.json", "mixed", "<2, 1>", 8),
+                                    ("ncu_gemm_summary_3xtf32.json", "3xtf32", "<2, 0>", 8)]:
+        d = json.load(open(os.path.join(ROOT, "profiles", name)))
+        assert "32768^3" in d["problem"] and "tf32x3_gemm_kernel" + tmpl in d["kernel"], name
+        assert d["mode"] == mode and d["N"] == 32768
+        m = d["metrics"]
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Tbyte": 1e12, "byte": 1}
+        dram = sum(float(m[k]["value"]) * scale[m[k]["unit"]]
+                   for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+        assert abs(dram - d["dram_bytes_per_launch"]) / dram < 1e-6
+        assert d["algorithmic_bytes_per_launch"] == plane * 2 * 32768 ** 2 + 4 * 32768 ** 2

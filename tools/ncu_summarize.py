@@ -35,15 +35,16 @@ def full(rep, out, n, command, capture):
         return float(m[k]["value"]) * SCALE[m[k]["unit"]]
 
     n = int(n)
-    mixed = "1>" in name or "ILi1EE" in name or ", 1>" in name
-    d = {"capture": capture, "command": command,
-         "kernel": name + (" (mixed split)" if mixed else ""),
+    # split mode from the kernel's template argument <CG, MODE>
+    mode = {"0": "3xtf32", "1": "mixed", "3": "f16x2"}[name.split("<")[1].split(">")[0].split(",")[1].strip()]
+    plane_bytes = 4 if mode == "f16x2" else 8  # fp16 h0 + h1, else fp32 hi + (fp32 lo | 2 bf16)
+    d = {"N": n, "world": 1, "mode": mode, "capture": capture, "command": command,
+         "kernel": name + f" ({mode} split)",
          "problem": f"{n}^3 fp32, 1 GPU (the bench workload)",
-         "algorithmic_bytes_per_launch": 0,
+         # planes of A and B read once + C written (beta = 0)
+         "algorithmic_bytes_per_launch": plane_bytes * 2 * n * n + 4 * n * n,
          "dram_bytes_per_launch": nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"),
          "metrics": m}
-    # planes: 8 B per element of A and B read once + C written (beta = 0)
-    d["algorithmic_bytes_per_launch"] = 8 * 2 * n * n + 4 * n * n
     with open(out, "w") as f:
         json.dump(d, f, indent=1)
     print(json.dumps({k: d[k] for k in ("kernel", "dram_bytes_per_launch")}))
