@@ -89,8 +89,16 @@ __device__ __forceinline__ void split_store4_f16x2(float4 x, int e, const Planes
   __stcs(reinterpret_cast<uint2*>(p.h1 + r * p.ldo16 + k), lv);
 }
 
-__device__ __forceinline__ void split_store(float x, const Planes& p, int64_t r, int64_t k) {
-  if (p.rmax != nullptr) return split_store_f16x2(x, f16x2_exp(__ldcg(p.rmax + r)), p, r, k);
+// Scale exponent of plane row r (kModeF16x2; 0 otherwise).  Callers load it
+// once per row, ahead of the row's stores: an L2 round trip per store would
+// serialise the split behind the loads.
+__device__ __forceinline__ int row_exp(const Planes& p, int64_t r) {
+  return p.rmax != nullptr ? f16x2_exp(__ldcg(p.rmax + r)) : 0;
+}
+
+// e: row_exp(p, r)
+__device__ __forceinline__ void split_store(float x, const Planes& p, int64_t r, int64_t k, int e) {
+  if (p.rmax != nullptr) return split_store_f16x2(x, e, p, r, k);
   const float h = tf32_rne(x);
   const float l = x - h;  // exact
   __stcs(p.hi + r * p.ldo + k, h);
@@ -102,8 +110,8 @@ __device__ __forceinline__ void split_store(float x, const Planes& p, int64_t r,
 }
 
 // four consecutive k of one row (16-B / 8-B aligned plane rows)
-__device__ __forceinline__ void split_store4(float4 x, const Planes& p, int64_t r, int64_t k) {
-  if (p.rmax != nullptr) return split_store4_f16x2(x, f16x2_exp(__ldcg(p.rmax + r)), p, r, k);
+__device__ __forceinline__ void split_store4(float4 x, const Planes& p, int64_t r, int64_t k, int e) {
+  if (p.rmax != nullptr) return split_store4_f16x2(x, e, p, r, k);
   const float v[4] = {x.x, x.y, x.z, x.w};
   float h[4], l[4];
 #pragma unroll

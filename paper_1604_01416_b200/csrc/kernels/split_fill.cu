@@ -45,7 +45,7 @@ __global__ void split_direct_kernel(const T* __restrict__ src, int64_t lds, int6
 #pragma unroll
   for (int i = 0; i < kT; i += kRowsPerPass) {
     const int64_t r = r0 + threadIdx.y + i;
-    if (r < rows) split_store(load_widen(src + r * lds + k), p, r, k);
+    if (r < rows) split_store(load_widen(src + r * lds + k), p, r, k, splitdev::row_exp(p, r));
   }
 }
 
@@ -66,7 +66,7 @@ __global__ void split_trans_kernel(const T* __restrict__ src, int64_t lds, int64
 #pragma unroll
   for (int i = 0; i < kT; i += kRowsPerPass) {
     const int64_t r = r0 + threadIdx.y + i, k = k0 + threadIdx.x;
-    if (k < kcols && r < rows) split_store(tile[threadIdx.x][threadIdx.y + i], p, r, k);
+    if (k < kcols && r < rows) split_store(tile[threadIdx.x][threadIdx.y + i], p, r, k, splitdev::row_exp(p, r));
   }
 }
 
@@ -89,14 +89,20 @@ __global__ void __launch_bounds__(32 * WY, 48 / WY) split_direct_vec4_kernel(con
     const int64_t r = r0 + threadIdx.y + WY * i;
     if (r < rows && full) v[i] = __ldg(reinterpret_cast<const float4*>(src + r * lds + k));
   }
+  int e[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + threadIdx.y + WY * i;
+    e[i] = r < rows ? splitdev::row_exp(p, r) : 0;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t r = r0 + threadIdx.y + WY * i;
     if (r >= rows) continue;
     if (full) {
-      split_store4(v[i], p, r, k);
+      split_store4(v[i], p, r, k, e[i]);
     } else {
-      for (int64_t kk = k; kk < kcols; ++kk) split_store(__ldg(src + r * lds + kk), p, r, kk);
+      for (int64_t kk = k; kk < kcols; ++kk) split_store(__ldg(src + r * lds + kk), p, r, kk, e[i]);
     }
   }
 }
@@ -142,6 +148,7 @@ __global__ void __launch_bounds__(32 * WY, 24 / WY) split_trans_vec4_kernel(cons
   for (int rl = t >> 1; rl < 128; rl += 16 * WY) {
     const int64_t ro = r0 + rl;
     if (ro >= rows) break;
+    const int e = splitdev::row_exp(p, ro);
 #pragma unroll
     for (int j = 0; j < kTransK / 8; ++j) {
       const int kl = 8 * j + 4 * (t & 1);
@@ -149,9 +156,9 @@ __global__ void __launch_bounds__(32 * WY, 24 / WY) split_trans_vec4_kernel(cons
       if (k >= kcols) continue;
       if (k + 4 <= kcols) {
         split_store4(make_float4(tile[kl][rl], tile[kl + 1][rl], tile[kl + 2][rl], tile[kl + 3][rl]), p,
-                     ro, k);
+                     ro, k, e);
       } else {
-        for (int u = 0; k + u < kcols; ++u) split_store(tile[kl + u][rl], p, ro, k + u);
+        for (int u = 0; k + u < kcols; ++u) split_store(tile[kl + u][rl], p, ro, k + u, e);
       }
     }
   }

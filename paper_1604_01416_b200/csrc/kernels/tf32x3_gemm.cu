@@ -232,14 +232,21 @@ __device__ __noinline__ void run_split_jobs(const SplitJobs& sj, float (*tile)[1
         const int64_t r = r0 + 2 * i;
         if (r < jb.rows && full) v[i] = __ldcs(reinterpret_cast<const float4*>(jb.src + r * jb.lds + k));
       }
+      int e[16];  // kModeF16x2 row exponents, loaded together ahead of the stores
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int64_t r = r0 + 2 * i;
+        e[i] = r < jb.rows ? splitdev::row_exp(p, r) : 0;
+      }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int64_t r = r0 + 2 * i;
         if (r >= jb.rows) break;
         if (full) {
-          splitdev::split_store4(v[i], p, r, k);
+          splitdev::split_store4(v[i], p, r, k, e[i]);
         } else {
-          for (int64_t kk = k; kk < jb.kcols; ++kk) splitdev::split_store(__ldcs(jb.src + r * jb.lds + kk), p, r, kk);
+          for (int64_t kk = k; kk < jb.kcols; ++kk)
+            splitdev::split_store(__ldcs(jb.src + r * jb.lds + kk), p, r, kk, e[i]);
         }
       }
     } else {
@@ -268,6 +275,7 @@ __device__ __noinline__ void run_split_jobs(const SplitJobs& sj, float (*tile)[1
       for (int rl = st >> 1; rl < 128; rl += 32) {
         const int64_t ro = rb + rl;
         if (ro >= jb.rows) break;
+        const int e = splitdev::row_exp(p, ro);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int kl = (st & 1) * 16 + 4 * q;
@@ -275,9 +283,9 @@ __device__ __noinline__ void run_split_jobs(const SplitJobs& sj, float (*tile)[1
           if (k >= jb.kcols) break;
           if (k + 4 <= jb.kcols) {
             splitdev::split_store4(make_float4(tile[kl][rl], tile[kl + 1][rl], tile[kl + 2][rl], tile[kl + 3][rl]),
-                                   p, ro, k);
+                                   p, ro, k, e);
           } else {
-            for (int u = 0; k + u < jb.kcols; ++u) splitdev::split_store(tile[kl + u][rl], p, ro, k + u);
+            for (int u = 0; k + u < jb.kcols; ++u) splitdev::split_store(tile[kl + u][rl], p, ro, k + u, e);
           }
         }
       }
