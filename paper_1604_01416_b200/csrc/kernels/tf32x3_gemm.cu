@@ -77,6 +77,7 @@ struct EpiParams {
   int a_mn16, b_mn16;   // the same for the bf16 planes (mixed mode)
   const unsigned* a_max;  // kModeF16x2: row maxima of the A / B^T planes (power-of-two scales)
   const unsigned* b_max;
+  int c_prefetch;         // beta != 0: prefetch the tile's C rows into L2 this many chunks before its end (0 off)
 };
 
 // k per pipeline stage: 32 fp32 or 64 fp16 elements fill a 128-B swizzle row
@@ -548,11 +549,27 @@ __global__ void __launch_bounds__(Cfg<CG>::kThreads, 1)
       item_range(t, total_tiles, num_kb, ep.ksplit, tile, split, kb_lo, kb_hi);
       tile_coords<CG>(tile, tiles_m, tiles_n, ep.group_m, mt, nt);
       const int num_chunks = (kb_hi - kb_lo + kc_blocks - 1) / kc_blocks;
+      // beta != 0: this thread's C row segment is read right after the last
+      // chunk; pulling it into L2 a chunk earlier keeps those reads off the
+      // DRAM latency path (the MMA has only two chunk buffers of slack)
+      const int pf_chunk = (ep.c_prefetch > 0 && ep.read_c && ep.ksplit <= 1 && !ep.c_half)
+                               ? max(0, num_chunks - ep.c_prefetch) : -1;
       float master[C::kColsPerThread];
 #pragma unroll
       for (int j = 0; j < C::kColsPerThread; ++j) master[j] = 0.0f;
       for (int ch = 0; ch < num_chunks; ++ch, ++chunk_ctr) {
         const int buf = chunk_ctr & 1;
+        if (ch == pf_chunk) {
+          const int prow_i = mt * C::kUmmaM + static_cast<int>(cta_rank) * C::kRowsPerCta + q * 32 +
+                             static_cast<int>(lane);
+          const int pc0 = nt * C::kUmmaN + col_off;
+          if (prow_i < ep.m) {
+            const float* prow = ep.c + static_cast<int64_t>(prow_i) * ep.ldc + pc0;
+#pragma unroll
+            for (int l = 0; l < C::kColsPerThread / 32; ++l)
+              if (pc0 + 32 * l < ep.n) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(prow + 32 * l));
+          }
+        }
         mbar_wait(smem_u32(&cfull_bar[buf]), (chunk_ctr >> 1) & 1);
         tc_fence_after();
         const uint32_t taddr = tmem_base + static_cast<uint32_t>(buf * C::kAccCols + col_off) + lane_addr;
@@ -840,7 +857,8 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
 
   EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
                a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws,
-               a.a_mn, a.b_mn, amn16 ? 1 : 0, bmn16 ? 1 : 0, a.a_max, a.b_max};
+               a.a_mn, a.b_mn, amn16 ? 1 : 0, bmn16 ? 1 : 0, a.a_max, a.b_max,
+               a.c_prefetch >= 0 ? a.c_prefetch : 1};
   // lockstep keeps the CTAs of a wave together; with a single wave there is
   // nothing to align (and no counters to clear)
   if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1 && tiles > units) {

@@ -117,6 +117,9 @@ Session::~Session() {
     w->cache.clear();
     w->replicas.clear();
     w->arena = DeviceBuffer();
+    w->plane_arena = DeviceBuffer();
+    for (cudaEvent_t e : {w->plane_reads, w->presplit_done, w->presplit_order})
+      if (e) cudaEventDestroy(e);
     w->pull_flag = DeviceBuffer();
     w->inflight.clear();
     for (auto* v : {&w->event_pool, &w->events_used})
@@ -697,7 +700,7 @@ void Session::add_range_pieces(Range& rg, const MatrixDescriptor& d, bool trans,
     }
 }
 
-Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy pol) const {
+Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy pol, bool presplit) const {
   const MatrixDescriptor& da = table_.at(g.a);
   const MatrixDescriptor& db = table_.at(g.b);
   const MatrixDescriptor& dc = table_.at(g.c);
@@ -738,6 +741,33 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
             source_ptr(*local(w), pc.matrix, pc.coord, pol, &remote);
             if (remote) plan.has_remote = true;
           }
+  }
+  if (presplit) {
+    // Panels never straddle a K-block boundary of A or B: every piece then
+    // covers its panel's full width, so each plane row of a panel comes from
+    // one owner block, whose split (and row scale) the owner made once.
+    // Segments wider than DM_PRESPLIT_PANEL are cut evenly (256-aligned).
+    std::vector<std::int64_t> cuts = {0, K};
+    auto add_cuts = [&](const BlockGrid& gr, bool k_on_rows) {
+      const std::int64_t step = k_on_rows ? gr.block_rows : gr.block_cols;
+      for (std::int64_t k = step; step > 0 && k < K; k += step) cuts.push_back(k);
+    };
+    add_cuts(da.layout.grid, g.trans_a);
+    add_cuts(db.layout.grid, !g.trans_b);
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    const std::int64_t maxw = std::max<std::int64_t>(256, env_int("DM_PRESPLIT_PANEL", 8192));
+    plan.k0.clear();
+    for (std::size_t i = 0; i + 1 < cuts.size(); ++i) {
+      const std::int64_t len = cuts[i + 1] - cuts[i];
+      const std::int64_t n = (len + maxw - 1) / maxw;
+      const std::int64_t width = ((len + n - 1) / n + 255) / 256 * 256;
+      for (std::int64_t k = cuts[i]; k < cuts[i + 1]; k += width) plan.k0.push_back(k);
+    }
+    plan.k0.push_back(K);
+    for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
+    for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
+    return plan;
   }
   const std::int64_t target = env_int("DM_PANEL_K", 8192);
   const std::int64_t local_lead = env_int("DM_PANEL_LOCAL", 0);

@@ -135,6 +135,15 @@ struct Worker {
   DeviceBuffer pull_flag;  // landing-copy sequence number (written by the pull stream)
   unsigned pull_seq = 0;
   DeviceBuffer arena;  // exchange buffer peers read (row/col partials, narrowed reshape payloads)
+  // Owner-split planes (scaled fp16 pair) of this worker's A / B blocks for a
+  // pipelined GEMM: peers pull plane rectangles from it instead of splitting
+  // fp32 pieces themselves (session_gemm.cpp, "presplit").  `plane_reads`:
+  // this worker's last GEMM that (with its pulls) read any worker's plane
+  // arena -- the owner split of the next such command waits for it.
+  DeviceBuffer plane_arena;
+  cudaEvent_t plane_reads = nullptr;
+  cudaEvent_t presplit_done = nullptr;  // this command's owner split (+ barrier) finished
+  cudaEvent_t presplit_order = nullptr;  // sync commands: the owner split after the compute stream
   std::uint64_t seed = 0;
   dm_worker_stats stats{};
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timing_events;
@@ -262,7 +271,21 @@ class Session {
   void validate_general(const GemmArgs& g) const;
   void validate_cyclic(const GemmArgs& g, std::vector<WorkerId>* strip_owners) const;
 
-  WorkerPlan plan_worker(const GemmArgs& g, int w, SourcePolicy pol) const;
+  WorkerPlan plan_worker(const GemmArgs& g, int w, SourcePolicy pol, bool presplit = false) const;
+  // Presplit GEMM (scaled fp16 pair, pipelined): every owner splits its own A
+  // and B blocks once into its plane arena; consumers pull plane rectangles.
+  // Decided from replicated state only (every rank agrees: it adds a barrier).
+  bool presplit_eligible(const GemmArgs& g, SourcePolicy pol) const;
+  struct ArenaBlock {  // one owned block's planes in its owner's plane arena
+    std::size_t h0 = 0, h1 = 0, rmax = 0;  // byte offsets
+    std::int64_t oprows = 0, kext = 0, ld = 0;
+    int trans = 0;
+  };
+  // role 0: A blocks (op(A) rows), role 1: B blocks (op(B)^T rows)
+  std::map<std::pair<int, BlockKey>, ArenaBlock> plane_arena_map(const GemmArgs& g, int owner,
+                                                                 std::size_t* total) const;
+  void ensure_plane_arenas(std::size_t bytes);
+  void presplit_owners(const GemmArgs& g);
   void add_range_pieces(Range& rg, const MatrixDescriptor& d, bool op_rows_trans, bool is_a,
                         const std::vector<std::int64_t>& k0) const;
   const void* source_ptr(const Worker& reader, MatrixId m, BlockCoord c, SourcePolicy pol,
@@ -317,6 +340,8 @@ class Session {
  private:
   std::size_t arena_bytes_ = 0;               // replicated: every worker's arena size
   std::vector<void*> arena_ptrs_;             // per worker (peer-readable)
+  std::size_t plane_arena_bytes_ = 0;         // same for the presplit plane arenas
+  std::vector<char*> plane_arena_ptrs_;
   std::unique_ptr<Comm> comm_;
 };
 

@@ -68,6 +68,7 @@ struct Session::GemmRun {
   const std::size_t esz;
   const int gemm_mode;
   const bool trace;
+  const bool presplit;  // planes come split from their owners' plane arenas (session_presplit.cpp)
   const int np;
   const int nbuf;
   std::int64_t kpitch = 8;
@@ -77,6 +78,7 @@ struct Session::GemmRun {
   unsigned* phase_ctr = nullptr;  // kModeF16x2 fused splits: one grid-handoff counter per step
 
   std::vector<std::array<Planes, 2>> pa, pb;
+  std::vector<std::vector<Planes>> spa, spb;  // presplit: per step, per range (an arena alias or pa / pb)
   std::vector<int> order;
   bool use_ce = false;
   char* landing[2] = {nullptr, nullptr};
@@ -92,12 +94,13 @@ struct Session::GemmRun {
   std::size_t ksplit_ws_bytes = 0;
 
   GemmRun(Session& s, Worker& wk, const GemmArgs& ga, SourcePolicy p, WorkerPlan pl, std::vector<DeviceBuffer>& b,
-          std::vector<cudaEvent_t>& e)
+          std::vector<cudaEvent_t>& e, bool presplit_cmd = false)
       : S(s), w(wk), g(ga), pol(p), plan(std::move(pl)), bufs(b), events(e),
         half_in(s.table_.at(ga.a).precision == Precision::Half16),
         esz(byte_width(s.table_.at(ga.a).precision)),
         gemm_mode(split_mode_for(s.gemm_mode_, plan.k0.empty() ? 0 : plan.k0.back(), half_in)),
         trace(s.tracing() && !s.async_),
+        presplit(presplit_cmd),
         np(static_cast<int>(plan.k0.size()) - 1),
         nbuf(np > 1 ? 2 : 1) {
     std::int64_t kmax = 0;
@@ -128,12 +131,16 @@ struct Session::GemmRun {
     for (auto& o : S.workers_) sharing += (o && o->device == w.device) ? 1 : 0;
     exclusive = sharing == 1;
     lockstep = exclusive ? static_cast<int>(env_int("DM_LOCKSTEP", 32)) : 0;
-    // DM_FUSE_SPLIT: 0 never, 1 when the carrying GEMM hides the split, 2 always
-    fuse_mode = half_in ? 0 : env_int("DM_FUSE_SPLIT", 1);
+    // DM_FUSE_SPLIT: 0 never, 1 when the carrying GEMM hides the split, 2 always.
+    // Not by default for the scaled fp16 pair: its two-phase fused split slows
+    // the carrying GEMM by ~4 ms per GiB (9.9 -> 13.8 ms per 8192-wide panel at
+    // 4 GPUs), while its own kernels split a GiB in ~0.65 ms between the
+    // GEMMs (4 GPUs: 1543 vs 1260 TFLOP/s, profiles/r02/fuse_ab/).
+    fuse_mode = (half_in || presplit) ? 0 : env_int("DM_FUSE_SPLIT", f16x2() ? 0 : 1);
 
     alloc_planes(plan.ar, plan.br, true, pa);
     alloc_planes(plan.br, plan.ar, false, pb);
-    if (f16x2() && np > 1) {
+    if (f16x2() && np > 1 && !presplit) {
       bufs.push_back(w.pool->acquire(static_cast<std::size_t>(np) * 4));
       phase_ctr = static_cast<unsigned*>(bufs.back().data());
     }
@@ -144,7 +151,17 @@ struct Session::GemmRun {
     cuda_check(cudaStreamWaitEvent(w.side, e, 0), "wait");
 
     order_panels();
-    setup_landing();
+    if (presplit) {
+      // every owner's planes (this command's owner splits, then the barrier)
+      for (auto& o : S.workers_)
+        if (o && o->presplit_done)
+          for (cudaStream_t st : {w.pull, w.stream})
+            cuda_check(cudaStreamWaitEvent(st, o->presplit_done, 0), "wait presplit");
+      spa.assign(np, {});
+      spb.assign(np, {});
+    } else {
+      setup_landing();
+    }
     landed_ev.assign(np, nullptr);
     consumed_ev.assign(np, nullptr);
     split_ev.assign(np, nullptr);
@@ -284,7 +301,7 @@ struct Session::GemmRun {
     put(static_cast<std::uint64_t>(gemm_mode));
     put(static_cast<std::uint64_t>(np));
     static const char* knobs[] = {"DM_FUSE_SPLIT", "DM_CTA_GROUP", "DM_FLUSH_K", "DM_GROUP_M", "DM_L2_POLICY",
-                                  "DM_LOCKSTEP", "DM_MN_REUSE", "DM_PULL_CE", "DM_SPLIT_WARPS"};
+                                  "DM_LOCKSTEP", "DM_MN_REUSE", "DM_PULL_CE", "DM_SPLIT_WARPS", "DM_C_PREFETCH"};
     for (const char* k : knobs) {
       const char* v = std::getenv(k);
       put(v ? std::hash<std::string>()(v) : 0);
@@ -464,6 +481,107 @@ struct Session::GemmRun {
     cuda_check(stream_write_flag(w.pull, flag, seq[s]), "cuStreamWriteValue32");
     cuda_check(cudaEventRecord(landed_ev[s], w.pull), "event");
     if (trace) w.trace.push_back({"pull", p, pulled, 0.0, tp, S.trace_event(w.pull)});
+  }
+
+  // ------------------------------------------------------------ presplit
+  // Where piece `pc` (role 0: A, 1: B) lies in its owner's plane arena.
+  struct Loc {
+    const char* base;
+    const ArenaBlock* ab;
+    std::int64_t o, q;  // plane row and k offset inside the owner block
+    int owner;
+  };
+  std::map<int, std::map<std::pair<int, BlockKey>, ArenaBlock>> arena_maps;
+  Loc locate(int role, const Piece& pc) {
+    const int owner = S.table_.at(pc.matrix).layout.owner(pc.coord);
+    auto it = arena_maps.find(owner);
+    if (it == arena_maps.end()) {
+      std::size_t t = 0;
+      it = arena_maps.emplace(owner, S.plane_arena_map(g, owner, &t)).first;
+    }
+    const ArenaBlock& ab = it->second.at({role, BlockKey{pc.matrix, pc.coord}});
+    if (ab.trans != pc.trans) throw ProtocolError("presplit: piece orientation differs from its arena planes");
+    const std::int64_t a = pc.src_off / pc.lds, b = pc.src_off % pc.lds;
+    return {S.plane_arena_ptrs_.at(owner), &ab, pc.trans ? b : a, pc.trans ? a : b, owner};
+  }
+
+  // Planes of step s: a range whose panel is one whole local piece aliases
+  // the owner arena (no copy); every other range gets its pieces' plane
+  // rectangles and row maxima copied into its panel buffer on the copy
+  // engines (peer arenas over NVLink).
+  void prepare_presplit(int s) {
+    const int p = order[s];
+    const int buf = s % nbuf;
+    bool any = false;
+    cudaEvent_t tp = nullptr;
+    std::uint64_t pulled = 0;
+    for (int ab = 0; ab < 2; ++ab) {
+      const std::vector<Range>& rs = ab == 0 ? plan.ar : plan.br;
+      const std::vector<std::array<Planes, 2>>& planes = ab == 0 ? pa : pb;
+      std::vector<Planes>& sp = (ab == 0 ? spa : spb)[s];
+      sp.resize(rs.size());
+      for (std::size_t i = 0; i < rs.size(); ++i) {
+        const std::vector<Piece>& pieces = rs[i].panels[p];
+        if (pieces.size() == 1) {
+          const Piece& pc = pieces[0];
+          const Loc L = locate(ab, pc);
+          if (L.owner == w.id && pc.rows == rs[i].len && L.q % 8 == 0) {
+            const std::int64_t off = (L.o * L.ab->ld + L.q) * 2;
+            char* base = const_cast<char*>(L.base);
+            sp[i] = Planes{nullptr, nullptr, base + L.ab->h0 + off, base + L.ab->h1 + off, false, L.ab->ld,
+                           reinterpret_cast<unsigned*>(base + L.ab->rmax) + L.o};
+            w.stats.local_bytes_read += pc.bytes();
+            continue;
+          }
+        }
+        const Planes& dst = planes[i][buf];
+        sp[i] = dst;
+        for (const Piece& pc : pieces) {
+          const Loc L = locate(ab, pc);
+          if (!any) {
+            any = true;
+            // planes[buf] was last read by the GEMM of step s - nbuf
+            if (s >= nbuf) cuda_check(cudaStreamWaitEvent(w.pull, gemm_ev[s - nbuf], 0), "wait");
+            if (trace) tp = S.trace_event(w.pull);
+          }
+          for (int h = 0; h < 2; ++h) {
+            const char* src = L.base + (h ? L.ab->h1 : L.ab->h0) + (L.o * L.ab->ld + L.q) * 2;
+            char* d = static_cast<char*>(h ? dst.lo16 : dst.hi16) + (pc.dst_row * dst.ld + pc.dst_k) * 2;
+            cuda_check(cudaMemcpy2DAsync(d, dst.ld * 2, src, L.ab->ld * 2, pc.kcols * 2, pc.rows, cudaMemcpyDefault,
+                                         w.pull),
+                       "cudaMemcpy2DAsync(planes)");
+          }
+          cuda_check(cudaMemcpyAsync(dst.rmax + pc.dst_row, L.base + L.ab->rmax + L.o * 4, pc.rows * 4,
+                                     cudaMemcpyDefault, w.pull),
+                     "cudaMemcpyAsync(row maxima)");
+          if (L.owner != w.id) {
+            w.stats.peer_bytes_read += pc.bytes();
+            pulled_blocks[{pc.matrix, pc.coord}] += pc.bytes();
+            pulled += pc.bytes();
+          } else {
+            w.stats.local_bytes_read += pc.bytes();
+          }
+        }
+      }
+    }
+    if (!any) return;
+    landed_ev[s] = new_event();
+    cuda_check(cudaEventRecord(landed_ev[s], w.pull), "event");
+    split_ev[s] = landed_ev[s];  // the GEMM of step s waits for its planes
+    if (trace) w.trace.push_back({"pull", p, pulled, 0.0, tp, S.trace_event(w.pull)});
+  }
+
+  void run_presplit() {
+    setup();
+    prepare_presplit(0);
+    for (int step = 0; step < np; ++step) {
+      if (step + 1 < np) prepare_presplit(step + 1);
+      gemm_step(step, nullptr);
+    }
+    // the next presplit command's owner splits wait for these reads
+    if (!w.plane_reads) cuda_check(cudaEventCreateWithFlags(&w.plane_reads, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(w.plane_reads, w.stream), "event");
+    log_pulls();
   }
 
   std::int64_t plane_off(const Item& it) const {
@@ -661,8 +779,8 @@ struct Session::GemmRun {
     for (std::int64_t ti = 0; ti < ntask; ++ti) {
       const Task& t = plan.tasks[ti];
       StoredBlock& cb = w.owned.at({g.c, t.c});
-      const Planes& A = pa[t.ra][buf];
-      const Planes& B = pb[t.rb][buf];
+      const Planes& A = presplit ? spa[step][t.ra] : pa[t.ra][buf];
+      const Planes& B = presplit ? spb[step][t.rb] : pb[t.rb][buf];
       Tf32x3Args a;
       a.mode = gemm_mode;
       a.a_mn = A.mn ? 1 : 0;
@@ -693,6 +811,7 @@ struct Session::GemmRun {
       a.k_total = plan.k0.back();  // the chunk length follows the whole product's K
       a.group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
       a.l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
+      a.c_prefetch = static_cast<int>(env_int("DM_C_PREFETCH", -1));
       a.lockstep = lockstep;
       if (lockstep > 0) {
         const std::size_t need = tf32x3_sync_bytes(a);
@@ -796,6 +915,7 @@ struct Session::GemmRun {
       run_f64();
       return log_pulls();
     }
+    if (presplit) return run_presplit();
     setup();
     prepare(0);
     split_separate(0);
@@ -862,7 +982,46 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   // device spends on them.  A repeated command -- same operands, sources and
   // knobs -- replays the graph captured the first time instead (buffers kept
   // with the graph; a changed source pointer or plane-cache state is a new key).
-  const bool graphs_on = !async_ && !tracing() && !timing_ && env_int("DM_GRAPHS", 1) != 0 &&
+  // Presplit (session_presplit.cpp): the owners split their A / B blocks
+  // first -- after the asynchronous preamble, which then runs for every
+  // worker here instead of in the loop below.
+  const bool presplit = presplit_eligible(g, pol);
+  if (presplit) {
+    for (auto& wp : workers_) {
+      if (!wp) continue;
+      Worker& w = *wp;
+      DeviceGuard guard(w.device);
+      if (tracing() && !async_) w.trace_t0 = trace_event(w.stream);
+      if (async_) {
+        bound_inflight(w);
+        wait_writes(w.side, g.a);
+        wait_writes(w.side, g.b);
+        wait_all(w.side, g.c);
+        // the previous presplit command's plane reads, everywhere, end before
+        // any owner overwrites its arena (this barrier orders them)
+        for (auto& o : workers_)
+          if (o && o->plane_reads) cuda_check(cudaStreamWaitEvent(w.side, o->plane_reads, 0), "wait plane readers");
+        device_barrier(w.side, 1);
+        wait_all(w.stream, g.c);
+      } else {
+        // operands were written by earlier commands on the compute stream
+        if (!w.presplit_order)
+          cuda_check(cudaEventCreateWithFlags(&w.presplit_order, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(w.presplit_order, w.stream), "event");
+        cuda_check(cudaStreamWaitEvent(w.side, w.presplit_order, 0), "wait");
+      }
+    }
+    HostScope hp("run_gemm: presplit owners");
+    presplit_owners(g);
+    // the compute stream covers the owner split even on a worker without C
+    // blocks (a synchronous command ends by draining the compute streams)
+    for (auto& wp : workers_)
+      if (wp) {
+        DeviceGuard guard(wp->device);
+        cuda_check(cudaStreamWaitEvent(wp->stream, wp->presplit_done, 0), "wait presplit");
+      }
+  }
+  const bool graphs_on = !async_ && !tracing() && !timing_ && !presplit && env_int("DM_GRAPHS", 1) != 0 &&
                          table_.at(g.a).precision != Precision::Double64;
   const double graph_max_flops = static_cast<double>(env_int("DM_GRAPH_MAX_GFLOP", 64)) * 1e9;
   const std::size_t graph_cap = static_cast<std::size_t>(std::max<std::int64_t>(1, env_int("DM_GRAPH_CACHE", 32)));
@@ -873,9 +1032,9 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     WorkerPlan plan;
     {
       HostScope hp("run_gemm: plan_worker");
-      plan = plan_worker(g, w.id, pol);
+      plan = plan_worker(g, w.id, pol, presplit);
     }
-    if (async_) {
+    if (async_ && !presplit) {
       // pulls start once A and B are written everywhere; C is overwritten only
       // after its previous writes and reads (e.g. an async gather) finished
       bound_inflight(w);
@@ -891,20 +1050,24 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
     }
     if (plan.tasks.empty()) continue;
     Live& lv = live[w.id];
-    if (tracing() && !async_) w.trace_t0 = trace_event(w.stream);
+    if (tracing() && !async_ && !presplit) w.trace_t0 = trace_event(w.stream);
     double work = 0;
     for (const Task& t : plan.tasks) {
       auto [mb, nb] = block_extent(table_.at(g.c).layout.grid, t.c);
       work += 2.0 * mb * nb * static_cast<double>(plan.k0.back());
     }
     const bool use_graph = graphs_on && plan.k0.size() == 2 && work <= graph_max_flops;
-    GemmRun run(*this, w, g, pol, std::move(plan), lv.bufs, lv.events);
+    GemmRun run(*this, w, g, pol, std::move(plan), lv.bufs, lv.events, presplit);
     if (!use_graph) {
       HostScope hr("run_gemm: GemmRun");
       run.run();
     } else {
       HostScope hr("run_gemm: graph");
-      std::vector<std::uint64_t> sig = run.signature();
+      std::vector<std::uint64_t> sig;
+      {
+        HostScope hs("run_gemm: graph signature");
+        sig = run.signature();
+      }
       Worker::GraphEntry* hit = nullptr;
       for (auto& e : w.graphs)
         if (e.sig == sig) {
@@ -956,6 +1119,7 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
         run.commit_plane_cache();
       }
       hit->last_use = ++w.graph_clock;
+      HostScope hl("run_gemm: cudaGraphLaunch");
       cuda_check(cudaGraphLaunch(hit->exec, w.stream), "cudaGraphLaunch");
     }
     if (async_) {

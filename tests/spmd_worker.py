@@ -43,8 +43,12 @@ def main():
     A, B, C0 = s.gather(a), s.gather(b), s.gather(c)   # root 0 assembles (others untouched)
     # default schedule, then the K-panel pipeline forced on at this small size:
     # copy-engine landing + stream flags + split warps fused into the GEMM
-    forced = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PANEL_K": "512", "DM_FUSE_SPLIT": "2", "DM_PULL_CHUNK_MB": "1"}
-    for tag, env in (("", {}), ("ce_", forced)):
+    forced = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PANEL_K": "512", "DM_FUSE_SPLIT": "2", "DM_PULL_CHUNK_MB": "1",
+              "DM_PRESPLIT": "0"}
+    # ... and the owner-split schedule: plane rectangles pulled from the owners'
+    # IPC-mapped plane arenas (session_presplit.cpp), narrow panels
+    presplit = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PRESPLIT": "1", "DM_PRESPLIT_PANEL": "256"}
+    for tag, env in (("", {}), ("ce_", forced), ("ps_", presplit)):
         os.environ.update(env)
         for trans in range(4):
             ta, tb = bool(trans & 1), bool(trans & 2)
@@ -165,28 +169,32 @@ def main():
 
     # 5. asynchronous command mode, K-panel pipeline forced: a GEMM output
     #    feeds the next GEMM as a peer operand, then is overwritten while
-    #    peers may still be pulling its panels (write-after-read across ranks)
-    os.environ.update(forced)
-    s = session(55)
-    n = 1024
-    lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // pr, n // pc, world)
-    a, b, c, d, e = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(5))
-    A, B, D = s.gather(a), s.gather(b), s.gather(d)
-    s.set_async(True)
-    s.general_gemm(1.0, a, b, 0.0, c)      # C1 = A B
-    s.general_gemm(1.0, c, d, 0.0, e)      # E = C1 D: every rank pulls C1 panels
-    s.general_gemm(-1.0, a, b, 0.0, c)     # overwrite C while those pulls may run
-    s.barrier()
-    s.set_async(False)
-    Eg, Cg = s.gather(e), s.gather(c)
-    if rank == 0:
-        c1 = A.astype(np.float64) @ B.astype(np.float64)
-        want_e = c1 @ D.astype(np.float64)
-        results["async_chain_e"] = float(np.linalg.norm(Eg - want_e) / np.linalg.norm(want_e))
-        results["async_chain_c"] = float(np.linalg.norm(Cg + c1) / np.linalg.norm(c1))
-    s.close()
-    for k in forced:
-        del os.environ[k]
+    #    peers may still be pulling its panels (write-after-read across ranks);
+    #    owner-split: the next command's owner splits overwrite the plane
+    #    arenas peers pulled from
+    for tag, env in (("", forced), ("ps_", presplit)):
+        os.environ.update(env)
+        s = session(55)
+        n = 1024
+        lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // pr, n // pc, world)
+        a, b, c, d, e = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(5))
+        A, B, D = s.gather(a), s.gather(b), s.gather(d)
+        s.set_async(True)
+        for _ in range(2):
+            s.general_gemm(1.0, a, b, 0.0, c)      # C1 = A B
+            s.general_gemm(1.0, c, d, 0.0, e)      # E = C1 D: every rank pulls C1 panels
+            s.general_gemm(-1.0, a, b, 0.0, c)     # overwrite C while those pulls may run
+        s.barrier()
+        s.set_async(False)
+        Eg, Cg = s.gather(e), s.gather(c)
+        if rank == 0:
+            c1 = A.astype(np.float64) @ B.astype(np.float64)
+            want_e = c1 @ D.astype(np.float64)
+            results[f"async_chain_{tag}e"] = float(np.linalg.norm(Eg - want_e) / np.linalg.norm(want_e))
+            results[f"async_chain_{tag}c"] = float(np.linalg.norm(Cg + c1) / np.linalg.norm(c1))
+        s.close()
+        for k in env:
+            del os.environ[k]
 
     allres = [None] * world
     dist.all_gather_object(allres, results)

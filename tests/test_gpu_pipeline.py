@@ -32,6 +32,8 @@ def ref_gemm(alpha, A, ta, B, tb, beta, C0):
 def _pipeline_on(monkeypatch):
     # these sizes are below the work threshold that turns the K pipeline on
     monkeypatch.setenv("DM_PIPELINE_MIN_GFLOP", "0")
+    # the consumer-split schedules (the owner-split one: test_gpu_presplit.py)
+    monkeypatch.setenv("DM_PRESPLIT", "0")
 
 
 def run_case(P, n, blk, trans, alpha=1.5, beta=-0.5, seed=77, devices=None, gemm_mode="default"):

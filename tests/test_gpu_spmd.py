@@ -38,6 +38,7 @@ def test_spmd_parity(cuda):
     for t in range(4):
         assert res[f"general_t{t}"] <= 1e-5
         assert res[f"general_ce_t{t}"] <= 1e-5  # copy-engine landing + fused split pipeline
+        assert res[f"general_ps_t{t}"] <= 1e-5  # owner-split planes pulled from peer arenas
     assert res["A_bitexact"]
     assert all(res[f"own_blocks_r{r}"] for r in range(n))
     # 2-D pull: every rank reads exactly its off-owner A row panel + B column panel
@@ -48,6 +49,7 @@ def test_spmd_parity(cuda):
         want = 4 * (N // pr) * (N - N // pc) + 4 * (N // pc) * (N - N // pr)
         assert all(res[f"peer_bytes_r{r}_t0"] == want for r in range(n))
         assert all(res[f"peer_bytes_ce_r{r}_t0"] == want for r in range(n))
+        assert all(res[f"peer_bytes_ps_r{r}_t0"] == want for r in range(n))
     assert res["sweep_worst"] <= 1e-5
     assert res["fc_fwd"] <= 1e-5 and res["fc_bwd"] <= 1e-5
     assert all(res[f"bwd_peer_bytes_r{r}"] == 0 for r in range(n))
@@ -55,3 +57,4 @@ def test_spmd_parity(cuda):
     assert all(res[f"replica_ok_r{r}"] for r in range(n))
     # async chained GEMMs with the pipeline forced (cross-rank write-after-read)
     assert res["async_chain_e"] <= 1e-5 and res["async_chain_c"] <= 1e-5
+    assert res["async_chain_ps_e"] <= 1e-5 and res["async_chain_ps_c"] <= 1e-5
