@@ -59,7 +59,7 @@ dm::Session& S(dm_session* s) {
 
 // Split-product mode: explicit (dm_gemm_mode) or, for DM_GEMM_DEFAULT, the
 // DM_GEMM_MODE environment variable (0 = 3xTF32), else mixed.
-int resolve_gemm_mode(int requested, int64_t k) {
+int resolve_gemm_mode(int requested, int64_t m, int64_t n, int64_t k) {
   int mode;
   if (requested == DM_GEMM_TF32X3) mode = dm::kModeTf32x3;
   else if (requested == DM_GEMM_MIXED) mode = dm::kModeMixed;
@@ -67,7 +67,7 @@ int resolve_gemm_mode(int requested, int64_t k) {
   else if (requested == DM_GEMM_F16X2) mode = dm::kModeF16x2;
   else if (requested == DM_GEMM_DEFAULT) mode = dm::env_gemm_mode();
   else throw dm::UsageError("unknown gemm_mode");
-  return dm::resolve_split_mode(mode, k);
+  return dm::resolve_split_mode(mode, k, 2.0 * static_cast<double>(m) * static_cast<double>(n) * static_cast<double>(k));
 }
 
 // Scratch layout of one local_gemm call: the split planes of op(A) and op(B)
@@ -246,7 +246,7 @@ int local_gemm_impl(double alpha, const float* a, int64_t lda, int ta, const flo
           "dm_local_gemm_f32_ws with a caller workspace");
     int dev = 0;
     dm::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
-    const int mode = resolve_gemm_mode(gemm_mode, k);
+    const int mode = resolve_gemm_mode(gemm_mode, m, n, k);
     const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb);
     SeamScratch& sc = seam_scratch(dev);
     dm::DeviceBuffer buf;
@@ -673,7 +673,7 @@ int dm_local_gemm_f32_workspace_size(int64_t m, int64_t n, int64_t k, int cta_gr
   return guarded([&] {
     if (bytes == nullptr) throw dm::UsageError("local_gemm_workspace_size: null output");
     if (m < 0 || n < 0 || k < 0) throw dm::ShapeError("local_gemm: negative dimension");
-    const int mode = resolve_gemm_mode(gemm_mode, k);
+    const int mode = resolve_gemm_mode(gemm_mode, m, n, k);
     *bytes = 0;
     for (int ta : {0, 1})
       for (int tb : {0, 1}) *bytes = std::max(*bytes, seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb).total);
@@ -685,7 +685,7 @@ int dm_local_gemm_f32_ws(double alpha, const float* a, int64_t lda, int ta, cons
                          int cta_group, int gemm_mode, void* workspace, size_t workspace_bytes, void* stream) {
   return guarded([&] {
     local_gemm_validate(a, lda, ta, b, ldb, tb, c, ldc, m, n, k, cta_group);
-    const int mode = resolve_gemm_mode(gemm_mode, k);
+    const int mode = resolve_gemm_mode(gemm_mode, m, n, k);
     const SeamLayout L = seam_layout(seam_shape(m, n, k, cta_group, mode), ta, tb);
     if (workspace_bytes < L.total || (L.total > 0 && workspace == nullptr))
       throw dm::UsageError("local_gemm: workspace smaller than dm_local_gemm_f32_workspace_size");

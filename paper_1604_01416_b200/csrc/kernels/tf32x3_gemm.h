@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 namespace dm {
 
@@ -28,7 +29,20 @@ constexpr int kModeF16x2 = 3;
 // distance from the exact product over U[-1,1), U[0,1), log-uniform 2^+-20 and
 // 2^+-60, rows spanning 2^+-60, K = 256 .. 32768 -- at 1.8x its speed
 // (N=32768: 462 vs 260 TFLOP/s; mixed: 310, with a bf16 floor of ~6e-7).
-inline int resolve_split_mode(int mode, int64_t /*k_total*/) { return mode == kModeAuto ? kModeF16x2 : mode; }
+// Except for latency-bound products: below DM_F16X2_MIN_GFLOP (default 64)
+// of work, auto runs 3xTF32, whose one-pass split beats f16x2's row-maxima
+// pass + split where the GEMM itself takes microseconds (BASELINE config 1,
+// 2048^3 on 4 GPUs: f16x2 splits 95 us vs the batched 3xTF32 split's 27 us).
+// `work` = 2 m n k of the launch / worker (< 0: unknown, treated as large).
+inline int resolve_split_mode(int mode, int64_t /*k_total*/, double work = -1.0) {
+  if (mode != kModeAuto) return mode;
+  if (work >= 0.0) {
+    const char* v = std::getenv("DM_F16X2_MIN_GFLOP");
+    const double min_gflop = (v != nullptr && *v != 0) ? std::strtod(v, nullptr) : 64.0;
+    if (work < min_gflop * 1e9) return kModeTf32x3;
+  }
+  return kModeF16x2;
+}
 
 // One split job fused into a GEMM launch: the split_tf32 of an fp32 piece
 // (16-B aligned rows and planes) for the NEXT K panel, executed by the

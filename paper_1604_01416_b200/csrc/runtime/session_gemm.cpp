@@ -98,7 +98,7 @@ struct Session::GemmRun {
       : S(s), w(wk), g(ga), pol(p), plan(std::move(pl)), bufs(b), events(e),
         half_in(s.table_.at(ga.a).precision == Precision::Half16),
         esz(byte_width(s.table_.at(ga.a).precision)),
-        gemm_mode(split_mode_for(s.gemm_mode_, plan.k0.empty() ? 0 : plan.k0.back(), half_in)),
+        gemm_mode(split_mode_for(s.gemm_mode_, plan.k0.empty() ? 0 : plan.k0.back(), half_in, work_of(s, ga, plan))),
         trace(s.tracing() && !s.async_),
         presplit(presplit_cmd),
         np(static_cast<int>(plan.k0.size()) - 1),
@@ -110,11 +110,21 @@ struct Session::GemmRun {
 
   // Half16 operands are exact in one tf32 term: they keep 3xTF32 (their
   // splits read fp16 sources, which the scaled fp16 pair does not take).
-  static int split_mode_for(int session_mode, std::int64_t k, bool half) {
-    const int m = resolve_split_mode(session_mode, k);
+  static int split_mode_for(int session_mode, std::int64_t k, bool half, double work) {
+    const int m = resolve_split_mode(session_mode, k, work);
     return half && m == kModeF16x2 ? kModeTf32x3 : m;
   }
   bool f16x2() const { return gemm_mode == kModeF16x2; }
+  // 2 m n K over this worker's C blocks
+  static double work_of(const Session& s, const GemmArgs& g, const WorkerPlan& p) {
+    double work = 0;
+    const BlockGrid& gc = s.table_.at(g.c).layout.grid;
+    for (const Task& t : p.tasks) {
+      auto [mb, nb] = block_extent(gc, t.c);
+      work += 2.0 * mb * nb * static_cast<double>(p.k0.empty() ? 0 : p.k0.back());
+    }
+    return work;
+  }
 
   cudaEvent_t new_event() {
     cudaEvent_t e;

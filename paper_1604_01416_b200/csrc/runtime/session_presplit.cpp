@@ -40,7 +40,7 @@ bool Session::presplit_eligible(const GemmArgs& g, SourcePolicy pol) const {
   for (const MatrixDescriptor* d : {&da, &db, &dc})
     if (d->precision != Precision::Single32) return false;
   const std::int64_t K = g.trans_a ? da.layout.grid.global_rows : da.layout.grid.global_cols;
-  if (K <= 512 || resolve_split_mode(gemm_mode_, K) != kModeF16x2) return false;
+  if (K <= 512) return false;
   // every source must be the owner's block: fresh caches / replicas (read in
   // place by the consumer split path) keep that path
   if (da.replicated || db.replicated) return false;
@@ -62,7 +62,7 @@ bool Session::presplit_eligible(const GemmArgs& g, SourcePolicy pol) const {
       work += 2.0 * mb * nb * static_cast<double>(K);
     }
     if (work == 0) continue;
-    if (work < min_work) return false;
+    if (work < min_work || resolve_split_mode(gemm_mode_, K, work) != kModeF16x2) return false;
     any = true;
   }
   return any;

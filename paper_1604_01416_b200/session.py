@@ -8,6 +8,7 @@ tests.  Every call goes through libdmath_b200.so; nothing here computes.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import enum
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -196,11 +197,14 @@ class Config:
 GEMM_MODES = {"default": 0, "mixed": 1, "3xtf32": 2, "auto": 3, "f16x2": 4}  # dm_gemm_mode
 
 
-def split_mode_for(mode: str, k: int) -> str:
-    """The scheme a product over K runs in under `mode` (auto's rule,
-    tf32x3_gemm.h resolve_split_mode)."""
+def split_mode_for(mode: str, k: int, work: float = -1.0) -> str:
+    """The scheme a product over K with `work` = 2 m n k flops per worker
+    (< 0: large) runs in under `mode` (auto's rule, tf32x3_gemm.h
+    resolve_split_mode: f16x2, except 3xTF32 below DM_F16X2_MIN_GFLOP)."""
     if mode in ("mixed", "3xtf32", "f16x2"):
         return mode
+    if work >= 0 and work < float(os.environ.get("DM_F16X2_MIN_GFLOP") or 64) * 1e9:
+        return "3xtf32"
     return "f16x2"
 
 

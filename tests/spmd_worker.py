@@ -47,7 +47,8 @@ def main():
               "DM_PRESPLIT": "0"}
     # ... and the owner-split schedule: plane rectangles pulled from the owners'
     # IPC-mapped plane arenas (session_presplit.cpp), narrow panels
-    presplit = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PRESPLIT": "1", "DM_PRESPLIT_PANEL": "256"}
+    presplit = {"DM_PIPELINE_MIN_GFLOP": "0", "DM_PRESPLIT": "1", "DM_PRESPLIT_PANEL": "256",
+                "DM_F16X2_MIN_GFLOP": "0"}
     for tag, env in (("", {}), ("ce_", forced), ("ps_", presplit)):
         os.environ.update(env)
         for trans in range(4):
