@@ -60,8 +60,10 @@ enum dm_fill { DM_FILL_ZEROS = 0, DM_FILL_SEEDED = 1, DM_FILL_FROM_HOST = 2 }; /
  *                    x*2^e = h0 + h1 (fp16, 11 + 11 bits like tf32 hi / lo) and
  *                    h1*h0 + h0*h1 + h0*h0 as kind::f16: 3 slots per k16, 4 B of
  *                    planes per element;
- *   DM_GEMM_AUTO   : f16x2 for every fp32 product (3xTF32's accuracy at 1.8x
- *                    its speed); Half16 operands run 3xTF32;
+ *   DM_GEMM_AUTO   : f16x2 (3xTF32's accuracy at 1.8x its speed), except for
+ *                    latency-bound products -- below DM_F16X2_MIN_GFLOP
+ *                    (default 64) GFLOP per worker / call -- which run 3xTF32
+ *                    (one-pass split); Half16 operands run 3xTF32;
  *   DM_GEMM_DEFAULT: the DM_GEMM_MODE environment variable (0 = 3xTF32,
  *                    1 = mixed, 2 = auto, 3 = f16x2), else auto. */
 enum dm_gemm_mode { DM_GEMM_DEFAULT = 0, DM_GEMM_MIXED = 1, DM_GEMM_TF32X3 = 2, DM_GEMM_AUTO = 3, DM_GEMM_F16X2 = 4 };
@@ -235,6 +237,10 @@ int dm_set_gemm_timing(dm_session* s, int enable);
 int dm_worker_seed(dm_session* s, int worker, uint64_t* out); /* session.hpp:103 */
 /* The session's resolved split-product scheme: DM_GEMM_MIXED, DM_GEMM_TF32X3 or DM_GEMM_AUTO. */
 int dm_session_gemm_mode(dm_session* s, int* out);
+/* Host-only: the scheme (DM_GEMM_MIXED, DM_GEMM_TF32X3 or DM_GEMM_F16X2) a
+ * product over `k` with `work` = 2 m n k flops per worker (< 0: unknown) runs
+ * in under `gemm_mode` (DM_GEMM_DEFAULT reads DM_GEMM_MODE; auto's rule). */
+int dm_split_mode_for(int gemm_mode, int64_t k, double work, int* out);
 /* trace() (session.hpp:94; TraceLog, transport.hpp:56-71): the block transfers
  * this process's workers pulled, oldest first; fills up to cap records and
  * returns the total count (negative status on error). */

@@ -530,6 +530,21 @@ int dm_session_gemm_mode(dm_session* s, int* out) {
   });
 }
 
+int dm_split_mode_for(int gemm_mode, int64_t k, double work, int* out) {
+  return guarded([&] {
+    if (out == nullptr) throw dm::UsageError("split_mode_for: null output");
+    int mode;
+    if (gemm_mode == DM_GEMM_TF32X3) mode = dm::kModeTf32x3;
+    else if (gemm_mode == DM_GEMM_MIXED) mode = dm::kModeMixed;
+    else if (gemm_mode == DM_GEMM_AUTO) mode = dm::kModeAuto;
+    else if (gemm_mode == DM_GEMM_F16X2) mode = dm::kModeF16x2;
+    else if (gemm_mode == DM_GEMM_DEFAULT) mode = dm::env_gemm_mode();
+    else throw dm::UsageError("unknown gemm_mode");
+    const int m = dm::resolve_split_mode(mode, k, work);
+    *out = m == dm::kModeTf32x3 ? DM_GEMM_TF32X3 : m == dm::kModeMixed ? DM_GEMM_MIXED : DM_GEMM_F16X2;
+  });
+}
+
 int dm_worker_count(dm_session* s, int* out) {
   return guarded([&] { *out = S(s).worker_count(); });
 }

@@ -858,7 +858,7 @@ cudaError_t launch(const Tf32x3Args& a, cudaStream_t stream) {
   EpiParams ep{a.c, a.c_half, a.ldc, static_cast<int>(a.m), static_cast<int>(a.n), a.alpha, a.beta,
                a.read_c, a.group_m > 0 ? a.group_m : 8, a.l2_policy, a.lockstep, nullptr, ksplit, a.ws,
                a.a_mn, a.b_mn, amn16 ? 1 : 0, bmn16 ? 1 : 0, a.a_max, a.b_max,
-               a.c_prefetch >= 0 ? a.c_prefetch : 1};
+               a.c_prefetch >= 0 ? a.c_prefetch : 0};
   // lockstep keeps the CTAs of a wave together; with a single wave there is
   // nothing to align (and no counters to clear)
   if (a.lockstep > 0 && a.sync != nullptr && ksplit == 1 && tiles > units) {

@@ -124,7 +124,7 @@ struct Tf32x3Args {
   int ksplit = 0;         // split-K: 0 auto (tiles cannot fill the SMs), 1 off, >1 forced
   float* ws = nullptr;    // split-K partials (>= tf32x3_splitk_bytes); no workspace = no split
   size_t ws_bytes = 0;
-  int c_prefetch = -1;    // beta != 0: L2 prefetch of C this many TMEM chunks ahead (0 off, -1 default 1)
+  int c_prefetch = -1;    // beta != 0: L2 prefetch of C this many TMEM chunks ahead (0 / -1: off; measured no gain)
 };
 
 cudaError_t tf32x3_gemm(const Tf32x3Args& args, cudaStream_t stream);

@@ -8,7 +8,6 @@ tests.  Every call goes through libdmath_b200.so; nothing here computes.
 from __future__ import annotations
 
 import ctypes as C
-import os
 import enum
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -199,13 +198,13 @@ GEMM_MODES = {"default": 0, "mixed": 1, "3xtf32": 2, "auto": 3, "f16x2": 4}  # d
 
 def split_mode_for(mode: str, k: int, work: float = -1.0) -> str:
     """The scheme a product over K with `work` = 2 m n k flops per worker
-    (< 0: large) runs in under `mode` (auto's rule, tf32x3_gemm.h
-    resolve_split_mode: f16x2, except 3xTF32 below DM_F16X2_MIN_GFLOP)."""
-    if mode in ("mixed", "3xtf32", "f16x2"):
-        return mode
-    if work >= 0 and work < float(os.environ.get("DM_F16X2_MIN_GFLOP") or 64) * 1e9:
-        return "3xtf32"
-    return "f16x2"
+    (< 0: large) runs in under `mode` -- the library's own rule
+    (dm_split_mode_for; auto: f16x2, 3xTF32 below DM_F16X2_MIN_GFLOP)."""
+    if mode not in GEMM_MODES:
+        raise UsageError(f"unknown gemm_mode {mode!r}")
+    out = C.c_int()
+    _check(lib.dm_split_mode_for(GEMM_MODES[mode], int(k), float(work), C.byref(out)))
+    return {1: "mixed", 2: "3xtf32", 4: "f16x2"}[out.value]
 
 
 def nccl_unique_id() -> bytes:

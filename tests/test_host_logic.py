@@ -141,3 +141,30 @@ def test_ctypes_signatures_match_header():
         assert fn.argtypes is not None and len(fn.argtypes) == n, (name, n, fn.argtypes)
         want = ret_map.get(ret.strip(), None)
         assert want is None or fn.restype is want, (name, ret, fn.restype)
+
+
+def test_split_mode_rule(monkeypatch):
+    """The split-product scheme a product runs in (tf32x3_gemm.h
+    resolve_split_mode): explicit modes as given; auto = the scaled fp16 pair,
+    except latency-bound products (< DM_F16X2_MIN_GFLOP per worker, default 64)
+    which take 3xTF32's one-pass split; DM_GEMM_MODE steers "default"."""
+    monkeypatch.delenv("DM_F16X2_MIN_GFLOP", raising=False)
+    monkeypatch.delenv("DM_GEMM_MODE", raising=False)
+    for m in ("mixed", "3xtf32", "f16x2"):
+        for work in (-1.0, 1.0, 1e15):
+            assert dm.split_mode_for(m, 4096, work) == m
+    assert dm.split_mode_for("auto", 32768) == "f16x2"                  # unknown work: large
+    assert dm.split_mode_for("auto", 32768, 2.0 * 32768 ** 3) == "f16x2"
+    assert dm.split_mode_for("auto", 2048, 2.0 * 1024 * 1024 * 2048) == "3xtf32"   # config 1 per worker
+    assert dm.split_mode_for("auto", 9216, 2.0 * 64 * 4096 * 9216) == "3xtf32"     # FC forward per worker
+    assert dm.split_mode_for("auto", 16384, 63.9e9) == "3xtf32"
+    assert dm.split_mode_for("auto", 16384, 64.0e9) == "f16x2"
+    assert dm.split_mode_for("default", 2048, 1e15) == "f16x2"
+    monkeypatch.setenv("DM_F16X2_MIN_GFLOP", "0")
+    assert dm.split_mode_for("auto", 2048, 1.0) == "f16x2"
+    monkeypatch.setenv("DM_GEMM_MODE", "0")
+    assert dm.split_mode_for("default", 2048, 1e15) == "3xtf32"
+    monkeypatch.setenv("DM_GEMM_MODE", "1")
+    assert dm.split_mode_for("default", 2048, 1e15) == "mixed"
+    with pytest.raises(dm.UsageError):
+        dm.split_mode_for("fp64", 16)
