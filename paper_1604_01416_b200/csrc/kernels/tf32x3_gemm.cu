@@ -146,28 +146,38 @@ __device__ __noinline__ void run_absmax_jobs(const SplitJobs& sj, int st, uint32
       const int64_t tiles_k = (jb.kcols + 127) / 128;
       const int64_t k = (lt % tiles_k) * 128 + lane * 4;
       const int64_t r0 = (lt / tiles_k) * 32 + wy;
+      // all 16 rows' loads in flight before any reduction (a peer source
+      // costs an NVLink round trip per dependent load)
+      float m[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int64_t r = r0 + 2 * i;
+        m[i] = 0.0f;
+        if (r < jb.rows && k + 4 <= jb.kcols) {
+          const float4 v = __ldcs(reinterpret_cast<const float4*>(jb.src + r * jb.lds + k));
+          m[i] = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+        } else if (r < jb.rows) {
+          for (int64_t kk = k; kk < jb.kcols; ++kk) m[i] = fmaxf(m[i], fabsf(__ldcs(jb.src + r * jb.lds + kk)));
+        }
+      }
+#pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int64_t r = r0 + 2 * i;
         if (r >= jb.rows) break;  // warp-uniform
-        float m = 0.0f;
-        if (k + 4 <= jb.kcols) {
-          const float4 v = __ldcs(reinterpret_cast<const float4*>(jb.src + r * jb.lds + k));
-          m = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
-        } else {
-          for (int64_t kk = k; kk < jb.kcols; ++kk) m = fmaxf(m, fabsf(__ldcs(jb.src + r * jb.lds + kk)));
-        }
+        float mi = m[i];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0 && m > 0.0f) atomicMax(jb.rmax + r, __float_as_uint(m));
+        for (int o = 16; o > 0; o >>= 1) mi = fmaxf(mi, __shfl_xor_sync(0xffffffffu, mi, o));
+        if (lane == 0 && mi > 0.0f) atomicMax(jb.rmax + r, __float_as_uint(mi));
       }
     } else {
       const int64_t tiles_k = (jb.kcols + 31) / 32;
       const int64_t k0 = (lt % tiles_k) * 32;
       const int64_t r = (lt / tiles_k) * 128 + lane * 4;
       float m[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int64_t k = k0 + wy + 2 * i;
-        if (k >= jb.kcols) break;
+        if (k >= jb.kcols) continue;
         if (r + 4 <= jb.rows) {
           const float4 v = __ldcs(reinterpret_cast<const float4*>(jb.src + k * jb.lds + r));
           m[0] = fmaxf(m[0], fabsf(v.x));
