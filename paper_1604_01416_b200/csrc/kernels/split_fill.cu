@@ -164,6 +164,72 @@ __global__ void __launch_bounds__(32 * WY, 24 / WY) split_trans_vec4_kernel(cons
   }
 }
 
+// f16x2 planes from a transposed source, out[r][k] = src[k][r] (the op(B)^T
+// rows of a non-transposed B): 64 k x 128 r per block through a 32 KB smem
+// tile whose 16-B column groups are XOR-swizzled by k / 8.  The write phase
+// gives each output row 8 threads of 8 consecutive k (16 B of h0 and of h1
+// per thread), so one warp store fills four 128-B row segments -- where the
+// tf32-shaped kernel above writes 16 rows x 16 B per store -- and its smem
+// reads (8 k of one r per thread) hit 32 distinct banks.
+__global__ void __launch_bounds__(256, 4) split_trans_f16x2_kernel(const float* __restrict__ src, int64_t lds,
+                                                                   int64_t rows, int64_t kcols, Planes p) {
+  __shared__ __align__(16) float tile[64][128];
+  const int64_t k0 = static_cast<int64_t>(blockIdx.x) * 64;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 128;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t r = r0 + tx * 4;
+  // load: warp ty takes k rows ty, ty + 8, ..., all eight float4 in flight
+  float4 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t k = k0 + ty + 8 * i;
+    v[i] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    if (k < kcols) {
+      if (r + 4 <= rows) {
+        v[i] = __ldcs(reinterpret_cast<const float4*>(src + k * lds + r));
+      } else {
+        float* f = reinterpret_cast<float*>(&v[i]);
+        for (int u = 0; u < 4; ++u)
+          if (r + u < rows) f[u] = __ldcs(src + k * lds + r + u);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)  // row kl = ty + 8 i, column group tx ^ i (kl >> 3 == i)
+    *reinterpret_cast<float4*>(&tile[ty + 8 * i][4 * (tx ^ i)]) = v[i];
+  __syncthreads();
+  // write: lane = 4 c + s -> k chunk c (8 k), row s of a group of four rows
+  const int c = tx >> 2, s = tx & 3;
+  const int64_t kk = k0 + 8 * c;
+  if (kk >= kcols) return;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    const int rl = 4 * (8 * pass + ty) + s;
+    const int64_t ro = r0 + rl;
+    if (ro >= rows) break;
+    const int e = splitdev::row_exp(p, ro);
+    float x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = tile[8 * c + u][rl ^ (4 * c)];
+    if (kk + 8 <= kcols) {
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = splitdev::scale_pow2(x[2 * u], e), b = splitdev::scale_pow2(x[2 * u + 1], e);
+        __half2 hh = __floats2half2_rn(a, b);
+        const float2 hf = __half22float2(hh);
+        __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+        h[u] = *reinterpret_cast<uint32_t*>(&hh);
+        l[u] = *reinterpret_cast<uint32_t*>(&ll);
+      }
+      __stcs(reinterpret_cast<uint4*>(p.h0 + ro * p.ldo16 + kk), make_uint4(h[0], h[1], h[2], h[3]));
+      __stcs(reinterpret_cast<uint4*>(p.h1 + ro * p.ldo16 + kk), make_uint4(l[0], l[1], l[2], l[3]));
+    } else {
+      for (int u = 0; kk + u < kcols; ++u) splitdev::split_store(x[u], p, ro, kk + u, e);
+    }
+  }
+}
+
 template <int WY>
 void launch_split_vec4(const float* s32, int64_t lds, int trans, int64_t rows, int64_t kcols, const Planes& p,
                        cudaStream_t stream) {
@@ -329,6 +395,14 @@ cudaError_t split_f16x2(const float* src, int64_t lds, int trans, int64_t rows, 
   p.rmax = rmax;
   auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   auto a8 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; };
+  const char* t16 = std::getenv("DM_SPLIT_TRANS16");  // 0: the tf32-shaped transposing kernel (A/B, tests)
+  const bool trans16 = t16 == nullptr || std::atoi(t16) != 0;
+  if (trans && trans16 && a16(src) && (lds & 3) == 0 && a16(h0) && a16(h1) && (ldo16 & 7) == 0) {
+    const dim3 g(static_cast<unsigned>((kcols + 63) / 64), static_cast<unsigned>((rows + 127) / 128));
+    if (g.y > 65535u) return cudaErrorInvalidConfiguration;
+    split_trans_f16x2_kernel<<<g, 256, 0, stream>>>(src, lds, rows, kcols, p);
+    return cudaGetLastError();
+  }
   if (a16(src) && (lds & 3) == 0 && a8(h0) && a8(h1) && (ldo16 & 3) == 0) {
     if ((rows + 7) / 8 > 65535) return cudaErrorInvalidConfiguration;
     switch (split_warps()) {

@@ -186,3 +186,28 @@ def test_cuda_graph_capture_with_workspace(cuda):
         torch.cuda.synchronize()
         want = 1.5 * (A.double().T @ B.double()) - 0.5 * C0.double()
         assert _relfro(C, want) <= 3e-6
+
+
+@pytest.mark.parametrize("shape", [(4096, 1024, 2048), (1000, 744, 1304), (384, 520, 4104)])
+def test_f16x2_transposing_split_kernels_agree(cuda, monkeypatch, shape):
+    """The f16x2 transposing split (split_trans_f16x2_kernel, swizzled smem
+    tile, 16-B plane stores) writes the same planes as the tf32-shaped
+    transposing kernel: a GEMM whose op(B) needs the transpose (B not
+    transposed) and whose op(A) too (A transposed) is bit-identical either way."""
+    import numpy as np
+    import torch
+    from paper_1604_01416_b200 import local_gemm
+    m, n, k = shape
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = torch.rand(k, m, device="cuda", generator=g) * 2 - 1   # op(A) = A^T: transposing split
+    B = torch.rand(k, n, device="cuda", generator=g) * 2 - 1   # op(B)^T rows = columns of B
+    out = {}
+    for t16 in ("1", "0"):
+        monkeypatch.setenv("DM_SPLIT_TRANS16", t16)
+        C = torch.zeros(m, n, device="cuda")
+        local_gemm(1.0, A, True, B, False, 0.0, C, gemm_mode="f16x2")
+        torch.cuda.synchronize()
+        out[t16] = C.cpu().numpy()
+    assert out["1"].tobytes() == out["0"].tobytes()
+    ref = A.double().T.cpu().numpy() @ B.double().cpu().numpy()
+    assert np.linalg.norm(out["1"] - ref) / np.linalg.norm(ref) <= 1e-5
