@@ -12,6 +12,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -334,7 +335,26 @@ __global__ void __launch_bounds__(256) absmax_trans_kernel(const float* __restri
   }
 }
 
+// dst[r] = max over the n sources of src[i][r] (row maxima as float bits;
+// sources may live on peer GPUs).
+__global__ void rowmax_combine_kernel(RowmaxSources srcs, unsigned* __restrict__ dst, int64_t rows) {
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    unsigned m = 0;
+    for (int i = 0; i < srcs.n; ++i) m = max(m, __ldcg(srcs.p[i] + r));
+    dst[r] = m;
+  }
+}
+
 }  // namespace
+
+cudaError_t rowmax_combine(const RowmaxSources& srcs, unsigned* dst, int64_t rows, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (srcs.n < 1 || srcs.n > RowmaxSources::kMax) return cudaErrorInvalidValue;
+  const int blocks = static_cast<int>(std::min<int64_t>((rows + 255) / 256, 148 * 4));
+  rowmax_combine_kernel<<<blocks, 256, 0, stream>>>(srcs, dst, rows);
+  return cudaGetLastError();
+}
 
 cudaError_t split_tf32(const void* src, int src_half, int64_t lds, int trans, int64_t rows,
                        int64_t kcols, float* hi, float* lo, int64_t ldo, void* hi16, void* lo16,

@@ -167,6 +167,14 @@ cudaError_t absmax_rows(const float* src, int64_t lds, int trans, int64_t rows, 
                         cudaStream_t stream);
 cudaError_t split_f16x2(const float* src, int64_t lds, int trans, int64_t rows, int64_t kcols, void* h0, void* h1,
                         int64_t ldo16, const unsigned* rmax, cudaStream_t stream);
+// Row maxima of a whole op(X) row from its blocks' partial maxima:
+// dst[r] = max_i p[i][r] (float bits; p[i] may point into peer memory).
+struct RowmaxSources {
+  static constexpr int kMax = 32;
+  const unsigned* p[kMax];
+  int n = 0;
+};
+cudaError_t rowmax_combine(const RowmaxSources& srcs, unsigned* dst, int64_t rows, cudaStream_t stream);
 
 // Double64 GEMM bit-exact with the reference's gemm_typed<double> (gemm_f64.cu):
 // C[i][j] <- alpha * sum_k A[i][k] B[j][k] (+ beta C[i][j] when read_c), A and B

@@ -118,7 +118,7 @@ Session::~Session() {
     w->replicas.clear();
     w->arena = DeviceBuffer();
     w->plane_arena = DeviceBuffer();
-    for (cudaEvent_t e : {w->plane_reads, w->presplit_done, w->presplit_order})
+    for (cudaEvent_t e : {w->plane_reads, w->presplit_done, w->presplit_order, w->maxima_done})
       if (e) cudaEventDestroy(e);
     w->pull_flag = DeviceBuffer();
     w->inflight.clear();
@@ -287,6 +287,7 @@ void Session::bound_inflight(Worker& w) {
 // Complete every outstanding asynchronous command on every rank.
 void Session::drain() {
   sync_local();
+  remote_read_.clear();  // (every rank drains; the barrier below ends the epoch)
   for (auto& w : workers_) {
     if (!w) continue;
     DeviceGuard g(w->device);
@@ -329,6 +330,7 @@ void Session::end_command() {
   if (async_) return;  // stream-ordered; completed by barrier()/drain()
   HostScope hs("end_command");
   if (!streams_drained_) sync_local();
+  remote_read_.clear();  // synchronous: every rank's reads finished before the digest exchange
   streams_drained_ = false;
   collect_timing();
   if (comm_) {
@@ -491,7 +493,7 @@ void Session::scatter(MatrixId id, const void* host, std::int64_t rows, std::int
       reap_inflight(*w);
       st = w->h2d;
       wait_all(st, id);
-      device_barrier(st, 0);
+      if (remote_read_.count(id)) device_barrier(st, 0);
     }
     for (BlockCoord c : owned_coords(d.layout, w->id)) {
       StoredBlock& blk = w->owned.at({id, c});
@@ -507,6 +509,7 @@ void Session::scatter(MatrixId id, const void* host, std::int64_t rows, std::int
     }
     if (async_) mark_write(*w, st, id);
   }
+  remote_read_.erase(id);
   bump_version(id);  // runtime_types.hpp:289-292
   end_command();
 }
@@ -743,10 +746,11 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
           }
   }
   if (presplit) {
-    // Panels never straddle a K-block boundary of A or B: every piece then
-    // covers its panel's full width, so each plane row of a panel comes from
-    // one owner block, whose split (and row scale) the owner made once.
-    // Segments wider than DM_PRESPLIT_PANEL are cut evenly (256-aligned).
+    // Panels start at K-block edges of A or B where they can (a panel inside
+    // one block whose range is one local piece is read in place from the
+    // owner's arena): the segments between edges are merged up to
+    // DM_PRESPLIT_PANEL wide, wider ones cut evenly (256-aligned).  Every
+    // plane row carries its whole op row's scale, so a panel may span blocks.
     std::vector<std::int64_t> cuts = {0, K};
     auto add_cuts = [&](const BlockGrid& gr, bool k_on_rows) {
       const std::int64_t step = k_on_rows ? gr.block_rows : gr.block_cols;
@@ -761,11 +765,14 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     // 8192-wide 1575 TFLOP/s; 2 GPUs: 855 vs 798).
     const std::int64_t maxw = std::max<std::int64_t>(256, env_int("DM_PRESPLIT_PANEL", 16384));
     plan.k0.clear();
-    for (std::size_t i = 0; i + 1 < cuts.size(); ++i) {
-      const std::int64_t len = cuts[i + 1] - cuts[i];
+    for (std::size_t i = 0; i + 1 < cuts.size();) {
+      std::size_t j = i + 1;  // merge [cuts[i], cuts[j]) while it stays within maxw
+      while (j + 1 < cuts.size() && cuts[j + 1] - cuts[i] <= maxw) ++j;
+      const std::int64_t len = cuts[j] - cuts[i];
       const std::int64_t n = (len + maxw - 1) / maxw;
       const std::int64_t width = ((len + n - 1) / n + 255) / 256 * 256;
-      for (std::int64_t k = cuts[i]; k < cuts[i + 1]; k += width) plan.k0.push_back(k);
+      for (std::int64_t k = cuts[i]; k < cuts[j]; k += width) plan.k0.push_back(k);
+      i = j;
     }
     plan.k0.push_back(K);
     for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
@@ -954,6 +961,7 @@ void Session::flush_trace(const char* op) {
 
 void Session::cache_foreign_a(const GemmArgs& g) {
   const MatrixDescriptor& da = table_.at(g.a);
+  remote_read_.insert(g.a);
   bool copied = false;
   for (auto& wp : workers_) {
     if (!wp) continue;

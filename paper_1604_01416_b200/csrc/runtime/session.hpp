@@ -143,6 +143,7 @@ struct Worker {
   DeviceBuffer plane_arena;
   cudaEvent_t plane_reads = nullptr;
   cudaEvent_t presplit_done = nullptr;  // this command's owner split (+ barrier) finished
+  cudaEvent_t maxima_done = nullptr;    // this command's partial row maxima (+ barrier) finished
   cudaEvent_t presplit_order = nullptr;  // sync commands: the owner split after the compute stream
   std::uint64_t seed = 0;
   dm_worker_stats stats{};
@@ -277,7 +278,9 @@ class Session {
   // Decided from replicated state only (every rank agrees: it adds a barrier).
   bool presplit_eligible(const GemmArgs& g, SourcePolicy pol) const;
   struct ArenaBlock {  // one owned block's planes in its owner's plane arena
-    std::size_t h0 = 0, h1 = 0, rmax = 0;  // byte offsets
+    // byte offsets: fp16 planes, this block's row maxima, the whole op row's
+    // maxima (max over the blocks of its band -- the scale the planes carry)
+    std::size_t h0 = 0, h1 = 0, rmax = 0, grmax = 0;
     std::int64_t oprows = 0, kext = 0, ld = 0;
     int trans = 0;
   };
@@ -321,6 +324,14 @@ class Session {
   std::vector<std::unique_ptr<Worker>> workers_;  // index = worker id; null if not local
   std::map<MatrixId, MatrixDescriptor> table_;
   std::map<MatrixId, std::uint64_t> cache_meta_;
+  // Asynchronous mode: matrices whose blocks a peer GPU may have read since
+  // their last write (operands of GEMMs whose consumers pull fp32 pieces,
+  // cache fills).  Replicated -- every rank issues the same commands.  A
+  // scatter needs the cross-rank barrier only for these; presplit GEMMs read
+  // A / B only on their owners (peers pull the plane arenas), so a resident
+  // operand refreshed every step is overwritten without waiting for a
+  // barrier that could only run after the GEMM freed the SMs.
+  std::set<MatrixId> remote_read_;
   std::uint64_t nondet_counter_ = 0;
   // trace() (transport.hpp:56-71): this process's pulls, the newest
   // DM_TRACE_CAP (default 2^20) records -- bounded so long runs do not grow it

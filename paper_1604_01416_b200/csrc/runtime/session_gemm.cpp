@@ -539,7 +539,7 @@ struct Session::GemmRun {
             const std::int64_t off = (L.o * L.ab->ld + L.q) * 2;
             char* base = const_cast<char*>(L.base);
             sp[i] = Planes{nullptr, nullptr, base + L.ab->h0 + off, base + L.ab->h1 + off, false, L.ab->ld,
-                           reinterpret_cast<unsigned*>(base + L.ab->rmax) + L.o};
+                           reinterpret_cast<unsigned*>(base + L.ab->grmax) + L.o};
             w.stats.local_bytes_read += pc.bytes();
             continue;
           }
@@ -561,9 +561,10 @@ struct Session::GemmRun {
                                          w.pull),
                        "cudaMemcpy2DAsync(planes)");
           }
-          cuda_check(cudaMemcpyAsync(dst.rmax + pc.dst_row, L.base + L.ab->rmax + L.o * 4, pc.rows * 4,
-                                     cudaMemcpyDefault, w.pull),
-                     "cudaMemcpyAsync(row maxima)");
+          if (pc.dst_k == 0)  // the row scales: once per row (every piece of a row carries the same)
+            cuda_check(cudaMemcpyAsync(dst.rmax + pc.dst_row, L.base + L.ab->grmax + L.o * 4, pc.rows * 4,
+                                       cudaMemcpyDefault, w.pull),
+                       "cudaMemcpyAsync(row maxima)");
           if (L.owner != w.id) {
             w.stats.peer_bytes_read += pc.bytes();
             pulled_blocks[{pc.matrix, pc.coord}] += pc.bytes();
@@ -996,6 +997,10 @@ void Session::run_gemm(const GemmArgs& g, SourcePolicy pol) {
   // first -- after the asynchronous preamble, which then runs for every
   // worker here instead of in the loop below.
   const bool presplit = presplit_eligible(g, pol);
+  if (!presplit && P_ > 1) {  // consumers read the operands' blocks on their owners' GPUs
+    remote_read_.insert(g.a);
+    remote_read_.insert(g.b);
+  }
   if (presplit) {
     for (auto& wp : workers_) {
       if (!wp) continue;

@@ -14,9 +14,11 @@
 // At P = 4 (2x2) that halves the split work, at P = 8 (2x4) it is a third.
 //
 // The row scale of a plane row is the power of two of its |x| maximum over
-// the owner block's K extent (not the panel's): panels never straddle a
-// K-block boundary (plan_worker), so every plane row of a panel comes from
-// one block and carries that block's scale, which the GEMM epilogue undoes.
+// the WHOLE op(X) row, as in a one-GPU split: the owners first write their
+// blocks' partial row maxima, then (after a barrier) each combines the
+// partials of its row band -- the blocks sharing its op rows, on any GPU --
+// and splits with that.  Every piece of a plane row therefore carries the
+// same scale, so K panels may span several owners' blocks.
 #include <algorithm>
 
 #include "../kernels/tf32x3_gemm.h"
@@ -52,6 +54,10 @@ bool Session::presplit_eligible(const GemmArgs& g, SourcePolicy pol) const {
   const std::int64_t ka = g.trans_a ? da.layout.grid.block_rows : da.layout.grid.block_cols;
   const std::int64_t kb = g.trans_b ? db.layout.grid.block_cols : db.layout.grid.block_rows;
   if (ka % 8 != 0 || kb % 8 != 0) return false;
+  // a row band's partial maxima are combined in one launch
+  const int band_a = g.trans_a ? da.layout.grid.n_block_rows() : da.layout.grid.n_block_cols();
+  const int band_b = g.trans_b ? db.layout.grid.n_block_cols() : db.layout.grid.n_block_rows();
+  if (band_a > RowmaxSources::kMax || band_b > RowmaxSources::kMax) return false;
   // only pipelined commands (enough math per worker to hide the pulls)
   const double min_work = static_cast<double>(env_int("DM_PIPELINE_MIN_GFLOP", 200)) * 1e9;
   bool any = false;
@@ -88,6 +94,7 @@ std::map<std::pair<int, BlockKey>, Session::ArenaBlock> Session::plane_arena_map
       ab.h0 = off;
       ab.h1 = off = align_up(off + plane);
       ab.rmax = off = align_up(off + plane);
+      ab.grmax = off = align_up(off + static_cast<std::size_t>(ab.oprows) * 4);
       off = align_up(off + static_cast<std::size_t>(ab.oprows) * 4);
       out[{role, BlockKey{d.matrix_id, c}}] = ab;
     }
@@ -125,37 +132,71 @@ void Session::ensure_plane_arenas(std::size_t bytes) {
 }
 
 // Every local worker splits its own A / B blocks into its plane arena on its
-// split stream, then (SPMD) a device barrier on that stream: pulls ordered
-// after `presplit_done` see every owner's planes.  The caller has ordered the
-// split stream after the operands' writes and after every earlier reader of
-// the arenas (Worker::plane_reads, plus the async preamble's barrier).
+// split stream, in two barrier-separated phases: (1) partial row maxima of
+// each owned block; (2) the whole-row maxima of each owned block's row band
+// (read from every band member's arena, peers included), then the split.
+// Pulls ordered after `presplit_done` (phase 2's barrier) see every owner's
+// planes.  The caller has ordered the split stream after the operands' writes
+// and after every earlier reader of the arenas (Worker::plane_reads, plus the
+// async preamble's barrier).
 void Session::presplit_owners(const GemmArgs& g) {
+  std::map<int, std::map<std::pair<int, BlockKey>, ArenaBlock>> maps;
   std::size_t need = kAlign;
   for (int w = 0; w < P_; ++w) {
     std::size_t t = 0;
-    plane_arena_map(g, w, &t);
+    maps[w] = plane_arena_map(g, w, &t);
     need = std::max(need, t);
   }
   ensure_plane_arenas(need);
-  for (auto& wp : workers_) {
+  for (auto& wp : workers_) {  // phase 1: partial maxima
     if (!wp) continue;
     Worker& w = *wp;
     DeviceGuard guard(w.device);
     for (auto& o : workers_)
       if (o && o->plane_reads) cuda_check(cudaStreamWaitEvent(w.side, o->plane_reads, 0), "wait plane readers");
-    cudaEvent_t ta = (tracing() && !async_) ? trace_event(w.side) : nullptr;
-    std::size_t total = 0;
-    std::uint64_t bytes = 0;
     char* base = plane_arena_ptrs_.at(w.id);
-    for (const auto& [key, ab] : plane_arena_map(g, w.id, &total)) {
+    for (const auto& [key, ab] : maps.at(w.id)) {
       if (ab.oprows <= 0 || ab.kext <= 0) continue;
       const StoredBlock& blk = w.owned.at(key.second);
-      const float* src = blk.mem.f32();
       unsigned* rmax = reinterpret_cast<unsigned*>(base + ab.rmax);
       cuda_check(cudaMemsetAsync(rmax, 0, static_cast<std::size_t>(ab.oprows) * 4, w.side), "memset row maxima");
-      cuda_check(absmax_rows(src, blk.cols, ab.trans, ab.oprows, ab.kext, rmax, w.side), "absmax_rows");
-      cuda_check(split_f16x2(src, blk.cols, ab.trans, ab.oprows, ab.kext, base + ab.h0, base + ab.h1, ab.ld, rmax,
-                             w.side),
+      cuda_check(absmax_rows(blk.mem.f32(), blk.cols, ab.trans, ab.oprows, ab.kext, rmax, w.side), "absmax_rows");
+      w.stats.split_launches += 1;
+    }
+    device_barrier(w.side, 1);  // every owner's partial maxima exist
+    if (!w.maxima_done) cuda_check(cudaEventCreateWithFlags(&w.maxima_done, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventRecord(w.maxima_done, w.side), "event");
+  }
+  for (auto& wp : workers_) {  // phase 2: whole-row maxima, split
+    if (!wp) continue;
+    Worker& w = *wp;
+    DeviceGuard guard(w.device);
+    for (auto& o : workers_)  // (LOCAL mode: the other workers' phase 1)
+      if (o && o.get() != &w) cuda_check(cudaStreamWaitEvent(w.side, o->maxima_done, 0), "wait maxima");
+    cudaEvent_t ta = (tracing() && !async_) ? trace_event(w.side) : nullptr;
+    std::uint64_t bytes = 0;
+    char* base = plane_arena_ptrs_.at(w.id);
+    for (const auto& [key, ab] : maps.at(w.id)) {
+      if (ab.oprows <= 0 || ab.kext <= 0) continue;
+      const int role = key.first;
+      const MatrixDescriptor& d = table_.at(key.second.matrix);
+      const BlockCoord c = key.second.coord;
+      // the band: blocks sharing this block's op rows (same block row when
+      // op rows are stored rows, same block column otherwise)
+      RowmaxSources src;
+      const int nb = ab.trans ? d.layout.grid.n_block_rows() : d.layout.grid.n_block_cols();
+      for (int i = 0; i < nb; ++i) {
+        const BlockCoord y = ab.trans ? BlockCoord{i, c.col} : BlockCoord{c.row, i};
+        const int oy = d.layout.owner(y);
+        const ArenaBlock& aby = maps.at(oy).at({role, BlockKey{d.matrix_id, y}});
+        if (aby.kext <= 0) continue;
+        src.p[src.n++] = reinterpret_cast<const unsigned*>(plane_arena_ptrs_.at(oy) + aby.rmax);
+      }
+      unsigned* grmax = reinterpret_cast<unsigned*>(base + ab.grmax);
+      cuda_check(rowmax_combine(src, grmax, ab.oprows, w.side), "rowmax_combine");
+      const StoredBlock& blk = w.owned.at(key.second);
+      cuda_check(split_f16x2(blk.mem.f32(), blk.cols, ab.trans, ab.oprows, ab.kext, base + ab.h0, base + ab.h1, ab.ld,
+                             grmax, w.side),
                  "split_f16x2");
       w.stats.split_launches += 2;
       bytes += static_cast<std::uint64_t>(ab.oprows * ab.kext) * 4;

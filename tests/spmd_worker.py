@@ -193,6 +193,23 @@ def main():
             want_e = c1 @ D.astype(np.float64)
             results[f"async_chain_{tag}e"] = float(np.linalg.norm(Eg - want_e) / np.linalg.norm(want_e))
             results[f"async_chain_{tag}c"] = float(np.linalg.norm(Cg + c1) / np.linalg.norm(c1))
+        # scatter right after a GEMM that read the operand: the overwrite must
+        # not reach a peer still pulling the old blocks (consumer split) -- and
+        # needs no cross-rank barrier when only the owner read them (presplit)
+        rng = np.random.default_rng(7)
+        A2 = (rng.random((n, n), dtype=np.float32) * 2 - 1).astype(np.float32)
+        s.set_async(True)
+        s.general_gemm(1.0, a, b, 0.0, c)      # reads A
+        s.scatter(a, A2)                       # overwrites A
+        s.general_gemm(1.0, a, b, 0.0, e)      # reads the new A
+        s.barrier()
+        s.set_async(False)
+        Cg, Eg = s.gather(c), s.gather(e)
+        if rank == 0:
+            c1 = A.astype(np.float64) @ B.astype(np.float64)
+            e1 = A2.astype(np.float64) @ B.astype(np.float64)
+            results[f"async_scatter_{tag}c"] = float(np.linalg.norm(Cg - c1) / np.linalg.norm(c1))
+            results[f"async_scatter_{tag}e"] = float(np.linalg.norm(Eg - e1) / np.linalg.norm(e1))
         s.close()
         for k in env:
             del os.environ[k]

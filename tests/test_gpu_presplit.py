@@ -62,8 +62,8 @@ def test_presplit_2x2_transposes(cuda, monkeypatch, trans, panel):
     n = 1536
     err, st = run_case(4, n, n, n, (768, 768), (768, 768), (768, 768), trans)
     assert err <= TOL, err
-    # owner split only: absmax + split per owned A block and B block
-    assert all(x.split_launches == 4 for x in st), [x.split_launches for x in st]
+    # owner split only: partial maxima, whole-row maxima + split per owned A block and B block
+    assert all(x.split_launches == 6 for x in st), [x.split_launches for x in st]
 
 
 @pytest.mark.parametrize("trans", [0, 3])
@@ -102,7 +102,7 @@ def test_presplit_eight_workers_2x4(cuda, monkeypatch):
         for trans in (0, 3):
             err, st = run_case(8, n, n, n, (n // 2, n // 4), (n // 2, n // 4), (n // 2, n // 4), trans)
             assert err <= TOL, (panel, trans, err)
-            assert all(x.split_launches == 4 for x in st)
+            assert all(x.split_launches == 6 for x in st)
 
 
 def test_presplit_unaligned_blocks_fall_back(cuda, monkeypatch):
@@ -142,7 +142,7 @@ def test_presplit_across_gpus(cuda, monkeypatch):
             for trans in (0, 3):
                 err, st = run_case(P, n, n, n, blk, blk, blk, trans, devices=[w % ndev for w in range(P)])
                 assert err <= TOL, (P, panel, trans, err)
-                assert all(x.split_launches == 4 for x in st)
+                assert all(x.split_launches == 6 for x in st)
 
 
 @pytest.mark.parametrize("devices", [[0] * 4, "all"])
@@ -175,19 +175,35 @@ def test_presplit_async_chain(cuda, monkeypatch, devices):
         assert relfro(s.gather(c), -c1) <= TOL
 
 
-def test_presplit_matches_consumer_split_bitwise_when_scales_agree(cuda, monkeypatch):
-    """One K block per panel and one panel per block: the owner's block-wide
-    row scale equals the consumer's panel-wide one, the planes are the same
-    bytes and the GEMMs the same launches -- results bit-identical."""
+def test_presplit_matches_consumer_split_bitwise(cuda, monkeypatch):
+    """The owner splits scale every plane row by its WHOLE op row's maximum
+    (partial maxima combined across the row band's owners), as a one-panel
+    consumer split does: with both schedules in one K panel the planes are the
+    same bytes and the GEMM the same launch -- results bit-identical."""
     n = 1024
     out = {}
     for ps in ("1", "0"):
         monkeypatch.setenv("DM_PRESPLIT", ps)
-        monkeypatch.setenv("DM_PANEL_K", "512")
-        monkeypatch.setenv("DM_FUSE_SPLIT", "0")
+        monkeypatch.setenv("DM_PANEL_K", "0")  # consumer split: one panel
         with Session(Config(worker_count=4, root_seed=5, devices=[0] * 4, gemm_mode="f16x2")) as s:
             lay = make_layout(LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, 4)
             a, b, c = (s.create_matrix(lay, fill=FillKind.SeededRandom) for _ in range(3))
+            s.reset_worker_stats()
             s.general_gemm(1.0, a, b, 0.0, c)
-            out[ps] = s.gather(c)
-    assert out["1"].tobytes() == out["0"].tobytes()
+            out[ps] = (s.gather(c), [s.worker_stats(w).split_launches for w in range(4)])
+    assert out["1"][1] == [6] * 4  # the presplit schedule ran
+    assert out["1"][0].tobytes() == out["0"][0].tobytes()
+
+
+def test_presplit_panels_span_blocks(cuda, monkeypatch):
+    """K blocks of 256 (A) and 512 (B) under 1024-wide panels: every panel
+    assembles its planes from several owners' blocks, whose rows share the
+    whole-row scale."""
+    monkeypatch.setenv("DM_PRESPLIT_PANEL", "1024")
+    m = n = 1024
+    k = 2048
+    for trans in (0, 3):
+        ba = (512, 256) if not (trans & 1) else (256, 512)
+        bb = (512, 512)
+        err, st = run_case(4, m, n, k, ba, bb, (512, 512), trans)
+        assert err <= TOL, (trans, err)

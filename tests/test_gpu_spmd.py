@@ -58,3 +58,5 @@ def test_spmd_parity(cuda):
     # async chained GEMMs with the pipeline forced (cross-rank write-after-read)
     assert res["async_chain_e"] <= 1e-5 and res["async_chain_c"] <= 1e-5
     assert res["async_chain_ps_e"] <= 1e-5 and res["async_chain_ps_c"] <= 1e-5
+    for tag in ("", "ps_"):  # scatter right after a GEMM that read the operand
+        assert res[f"async_scatter_{tag}c"] <= 1e-5 and res[f"async_scatter_{tag}e"] <= 1e-5
