@@ -763,7 +763,11 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     // Wide panels: every panel after the first re-reads C (beta = 1), and
     // fewer, longer launches measured faster (4 GPUs: 16384-wide 1615 vs
     // 8192-wide 1575 TFLOP/s; 2 GPUs: 855 vs 798).
-    const std::int64_t maxw = std::max<std::int64_t>(256, env_int("DM_PRESPLIT_PANEL", 16384));
+    // At least two panels, so the first one's GEMM can hide the next one's
+    // pulls (config 5, N=16384 on 2x2: one 16384-wide panel would expose
+    // every pull; 15.8 vs 11.7 ms per chain).
+    const std::int64_t maxw = std::max<std::int64_t>(
+        256, std::min(env_int("DM_PRESPLIT_PANEL", 16384), (K / 2 + 255) / 256 * 256));
     plan.k0.clear();
     for (std::size_t i = 0; i + 1 < cuts.size();) {
       std::size_t j = i + 1;  // merge [cuts[i], cuts[j]) while it stays within maxw
