@@ -6,12 +6,15 @@
 // worker is a GPU:
 //   * owned / cached blocks live in HBM, allocated from a per-worker caching
 //     DevicePool (pool.hpp);
-//   * a GEMM is executed by every worker as a pipeline of K panels: operand
-//     pieces are PULLED straight from the owning worker's HBM (same device,
-//     CUDA peer access, or CUDA-IPC mapped across processes over NVLink) by
-//     the split kernel, which writes the tf32 hi/lo K-major panels the
-//     tcgen05 GEMM consumes; panel p+1 is pulled on a side stream while
-//     panel p multiplies (double-buffered);
+//   * a GEMM is executed by every worker (owner of C blocks) as a pipeline
+//     of K panels over split operand planes (scaled fp16 pair by default,
+//     tf32/bf16 or 3xTF32 selectable) the tcgen05 GEMM consumes.  Large
+//     f16x2 commands are "presplit": every owner splits its own A / B blocks
+//     once into an IPC-exported plane arena and the consumers pull plane
+//     rectangles on the copy engines while the previous panel multiplies
+//     (session_presplit.cpp); otherwise each worker pulls the fp32 pieces
+//     (copy engines into landing buffers, or the split kernel's own peer
+//     loads) and splits them itself (session_gemm.cpp);
 //   * LOCAL mode: one process drives all P workers (tests, 1-GPU parity at
 //     any P);  SPMD mode: one process per GPU (torchrun), every rank issues
 //     the same calls in the same order, NCCL provides the barrier and the

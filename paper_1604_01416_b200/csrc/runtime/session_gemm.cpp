@@ -4,16 +4,21 @@
 // 336-383, 406-503): the same pieces, pulled panel by panel and overlapped
 // with the tcgen05 GEMM.
 //
-// Per panel step s (panels in `order`, the least-remote first):
+// Consumer-split schedule, per panel step s (panels in `order`, the
+// least-remote first):
 //   pull   (stream `pull`, copy engines): pieces on another GPU land in a
 //          double-buffered local buffer; a stream memory op then publishes
 //          the step's sequence number in the worker's flag word;
-//   split  (stream `side` for step 0 and whenever fusing does not pay; else
-//          the split warps of step s-1's GEMM launches): transpose/assemble
-//          into K-major planes, fp32 -> tf32 hi + bf16 hi/lo;
+//   split  (stream `side`, or -- tf32 / mixed planes, when it pays -- the
+//          split warps of step s-1's GEMM launches): transpose/assemble into
+//          K-major planes (scaled fp16 pair, or tf32 hi + tf32 lo / bf16 hi, lo);
 //   GEMM   (stream `stream`): C += op(A)_s op(B)_s over double-buffered planes.
 // Buffer reuse is event-ordered: landing[s % 2] waits until step s-2's split
 // consumed it, planes[s % 2] until step s-2's GEMM read them.
+// Presplit schedule (run_presplit): no split here -- the owners split their
+// blocks (session_presplit.cpp); per step the pull stream copies plane
+// rectangles and row maxima from the owners' arenas into planes[s % 2] (or
+// the step reads a wholly-local panel in place), then the GEMM.
 #include <algorithm>
 #include <array>
 #include <cstring>
