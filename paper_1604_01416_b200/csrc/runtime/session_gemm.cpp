@@ -316,7 +316,8 @@ struct Session::GemmRun {
     put(static_cast<std::uint64_t>(gemm_mode));
     put(static_cast<std::uint64_t>(np));
     static const char* knobs[] = {"DM_FUSE_SPLIT", "DM_CTA_GROUP", "DM_FLUSH_K", "DM_GROUP_M", "DM_L2_POLICY",
-                                  "DM_LOCKSTEP", "DM_MN_REUSE", "DM_PULL_CE", "DM_SPLIT_WARPS", "DM_C_PREFETCH"};
+                                  "DM_LOCKSTEP", "DM_MN_REUSE", "DM_PULL_CE", "DM_SPLIT_WARPS", "DM_C_PREFETCH",
+                                  "DM_KSPLIT"};
     for (const char* k : knobs) {
       const char* v = std::getenv(k);
       put(v ? std::hash<std::string>()(v) : 0);
@@ -828,6 +829,7 @@ struct Session::GemmRun {
       a.group_m = static_cast<int>(env_int("DM_GROUP_M", 0));
       a.l2_policy = static_cast<int>(env_int("DM_L2_POLICY", 1));
       a.c_prefetch = static_cast<int>(env_int("DM_C_PREFETCH", -1));
+      a.ksplit = static_cast<int>(env_int("DM_KSPLIT", 0));  // 0 auto, 1 off, >1 forced
       a.lockstep = lockstep;
       if (lockstep > 0) {
         const std::size_t need = tf32x3_sync_bytes(a);

@@ -430,3 +430,15 @@ def test_fc_plane_cache_follows_weight_versions(cuda):
             assert relfro(s.gather(dx), ref_gemm(1.0, Wh, False, dY, False, 0.0, None)) <= TOL
             if step % 2 == 1:  # same W as the previous step: only X's pieces are split
                 assert fwd_splits == P
+
+
+def test_graft_smoke(cuda):
+    """__graft_entry__.smoke(): the reference KAT case and the headline
+    (f16x2, presplit) schedule at small sizes against the oracle."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "graft_entry", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "__graft_entry__.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.smoke()
