@@ -12,8 +12,10 @@ import numpy as np  # noqa: E402
 import paper_1604_01416_b200 as dm  # noqa: E402
 
 n = int(os.environ.get("P4_N", "32768"))
-with dm.Session(dm.Config(worker_count=4, root_seed=42, devices=[0, 1, 2, 3])) as s:
-    lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // 2, n // 2, 4)
+P = int(os.environ.get("P4_WORKERS", "4"))  # 2: the 1x2 grid of the 2-GPU bench
+pr, pc = dm.checkerboard_dims(P)
+with dm.Session(dm.Config(worker_count=P, root_seed=42, devices=list(range(P)))) as s:
+    lay = dm.make_layout(dm.LayoutKind.Checkerboard2D, n, n, n // pr, n // pc, P)
     a, b, c = (s.create_matrix(lay, fill=dm.FillKind.SeededRandom) for _ in range(3))
     s.reset_worker_stats()
     for _ in range(2):
