@@ -165,6 +165,57 @@ __global__ void __launch_bounds__(32 * WY, 24 / WY) split_trans_vec4_kernel(cons
   }
 }
 
+// f16x2 planes from a direct source (op(X) rows stored as rows): each
+// thread splits 8 consecutive k of 4 rows -- two float4 loads per row, all
+// eight in flight -- and stores 16 B of h0 and of h1 per row, so a warp store
+// covers 512 contiguous bytes of a plane row; 32 rows x 256 k per block.
+__global__ void __launch_bounds__(256, 4) split_direct_f16x2_kernel(const float* __restrict__ src, int64_t lds,
+                                                                    int64_t rows, int64_t kcols, Planes p) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t k = static_cast<int64_t>(blockIdx.x) * 256 + tx * 8;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32 + ty;
+  if (k >= kcols) return;
+  const bool full = k + 8 <= kcols;
+  float4 v[4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + 8 * i;
+    if (r < rows && full) {
+      const float4* q = reinterpret_cast<const float4*>(src + r * lds + k);
+      v[i][0] = __ldcs(q);
+      v[i][1] = __ldcs(q + 1);
+    }
+  }
+  int e[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + 8 * i;
+    e[i] = r < rows ? splitdev::row_exp(p, r) : 0;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = r0 + 8 * i;
+    if (r >= rows) break;
+    if (full) {
+      const float x[8] = {v[i][0].x, v[i][0].y, v[i][0].z, v[i][0].w, v[i][1].x, v[i][1].y, v[i][1].z, v[i][1].w};
+      uint32_t h[4], l[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = splitdev::scale_pow2(x[2 * u], e[i]), b = splitdev::scale_pow2(x[2 * u + 1], e[i]);
+        __half2 hh = __floats2half2_rn(a, b);
+        const float2 hf = __half22float2(hh);
+        __half2 ll = __floats2half2_rn(a - hf.x, b - hf.y);
+        h[u] = *reinterpret_cast<uint32_t*>(&hh);
+        l[u] = *reinterpret_cast<uint32_t*>(&ll);
+      }
+      __stcs(reinterpret_cast<uint4*>(p.h0 + r * p.ldo16 + k), make_uint4(h[0], h[1], h[2], h[3]));
+      __stcs(reinterpret_cast<uint4*>(p.h1 + r * p.ldo16 + k), make_uint4(l[0], l[1], l[2], l[3]));
+    } else {
+      for (int64_t kk = k; kk < kcols; ++kk) splitdev::split_store(__ldcs(src + r * lds + kk), p, r, kk, e[i]);
+    }
+  }
+}
+
 // f16x2 planes from a transposed source, out[r][k] = src[k][r] (the op(B)^T
 // rows of a non-transposed B): 64 k x 128 r per block through a 32 KB smem
 // tile whose 16-B column groups are XOR-swizzled by k / 8.  The write phase
@@ -417,6 +468,14 @@ cudaError_t split_f16x2(const float* src, int64_t lds, int trans, int64_t rows, 
   auto a8 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 7) == 0; };
   const char* t16 = std::getenv("DM_SPLIT_TRANS16");  // 0: the tf32-shaped transposing kernel (A/B, tests)
   const bool trans16 = t16 == nullptr || std::atoi(t16) != 0;
+  const char* d16 = std::getenv("DM_SPLIT_DIRECT16");  // 0: the tf32-shaped direct kernel (A/B, tests)
+  const bool direct16 = d16 == nullptr || std::atoi(d16) != 0;
+  if (!trans && direct16 && a16(src) && (lds & 3) == 0 && a16(h0) && a16(h1) && (ldo16 & 7) == 0) {
+    const dim3 g(static_cast<unsigned>((kcols + 255) / 256), static_cast<unsigned>((rows + 31) / 32));
+    if (g.y > 65535u) return cudaErrorInvalidConfiguration;
+    split_direct_f16x2_kernel<<<g, 256, 0, stream>>>(src, lds, rows, kcols, p);
+    return cudaGetLastError();
+  }
   if (trans && trans16 && a16(src) && (lds & 3) == 0 && a16(h0) && a16(h1) && (ldo16 & 7) == 0) {
     const dim3 g(static_cast<unsigned>((kcols + 63) / 64), static_cast<unsigned>((rows + 127) / 128));
     if (g.y > 65535u) return cudaErrorInvalidConfiguration;

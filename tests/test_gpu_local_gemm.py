@@ -189,7 +189,7 @@ def test_cuda_graph_capture_with_workspace(cuda):
 
 
 @pytest.mark.parametrize("shape", [(4096, 1024, 2048), (1000, 744, 1304), (384, 520, 4104)])
-def test_f16x2_transposing_split_kernels_agree(cuda, monkeypatch, shape):
+def test_f16x2_split_kernels_agree(cuda, monkeypatch, shape):
     """The f16x2 transposing split (split_trans_f16x2_kernel, swizzled smem
     tile, 16-B plane stores) writes the same planes as the tf32-shaped
     transposing kernel: a GEMM whose op(B) needs the transpose (B not
@@ -201,13 +201,21 @@ def test_f16x2_transposing_split_kernels_agree(cuda, monkeypatch, shape):
     g = torch.Generator(device="cuda").manual_seed(m + n + k)
     A = torch.rand(k, m, device="cuda", generator=g) * 2 - 1   # op(A) = A^T: transposing split
     B = torch.rand(k, n, device="cuda", generator=g) * 2 - 1   # op(B)^T rows = columns of B
+    # ... and the direct splits: op(A) = A2 (rows), op(B) = B2^T (rows of B2)
+    A2 = torch.rand(m, k, device="cuda", generator=g) * 2 - 1
+    B2 = torch.rand(n, k, device="cuda", generator=g) * 2 - 1
     out = {}
     for t16 in ("1", "0"):
         monkeypatch.setenv("DM_SPLIT_TRANS16", t16)
+        monkeypatch.setenv("DM_SPLIT_DIRECT16", t16)
         C = torch.zeros(m, n, device="cuda")
         local_gemm(1.0, A, True, B, False, 0.0, C, gemm_mode="f16x2")
+        C2 = torch.zeros(m, n, device="cuda")
+        local_gemm(1.0, A2, False, B2, True, 0.0, C2, gemm_mode="f16x2")
         torch.cuda.synchronize()
         out[t16] = C.cpu().numpy()
+        out["d" + t16] = C2.cpu().numpy()
     assert out["1"].tobytes() == out["0"].tobytes()
+    assert out["d1"].tobytes() == out["d0"].tobytes()
     ref = A.double().T.cpu().numpy() @ B.double().cpu().numpy()
     assert np.linalg.norm(out["1"] - ref) / np.linalg.norm(ref) <= 1e-5
