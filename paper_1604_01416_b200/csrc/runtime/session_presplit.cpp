@@ -75,7 +75,7 @@ bool Session::presplit_eligible(const GemmArgs& g, SourcePolicy pol) const {
 }
 
 // Planes of `owner`'s A blocks (role 0, op(A) rows, K-major) then B blocks
-// (role 1, op(B)^T rows), block-row-major; per block h0 | h1 | rmax.
+// (role 1, op(B)^T rows), block-row-major; per block h0 | h1 | rmax | grmax.
 std::map<std::pair<int, BlockKey>, Session::ArenaBlock> Session::plane_arena_map(const GemmArgs& g, int owner,
                                                                                  std::size_t* total) const {
   std::map<std::pair<int, BlockKey>, ArenaBlock> out;
