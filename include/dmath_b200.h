@@ -164,6 +164,12 @@ uint64_t dm_pool_size_class(uint64_t bytes);
 int dm_plan_general_gemm(const dm_layout* a, int trans_a, const dm_layout* b, int trans_b,
                          const dm_layout* c, int worker, int64_t* peer_blocks,
                          int64_t* peer_bytes);
+/* K panels of a presplit (owner-split) GEMM over K with A's / B's K-block
+ * widths a_kblock / b_kblock and the widest panel `max_width`
+ * (DM_PRESPLIT_PANEL): panel starts then K in out[0..*n-1] (at most cap
+ * entries).  Pure host logic (before a worker's own lead-panel cut). */
+int dm_presplit_panels(int64_t k, int64_t a_kblock, int64_t b_kblock, int64_t max_width, int64_t* out,
+                       int cap, int* n);
 
 /* ---- session (Session, session.hpp:53-485) ---- */
 /* Session::Session (session.hpp:64-76).  SPMD: collective over all ranks. */

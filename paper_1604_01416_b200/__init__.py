@@ -7,6 +7,6 @@ from .session import (  # noqa: F401
     Axis, CacheMissError, Config, ConfigError, CudaError, DeadlockError, Error, FillKind, IntegrityError,
     LayoutKind, LayoutSpec, MatrixDescriptor, NcclError, PlanError, Precision, ProtocolError,
     Session, ShapeError, UnsupportedError, UsageError, checkerboard_dims, fill_seeded, local_gemm,
-    local_gemm_workspace_size, split_mode_for,
+    local_gemm_workspace_size, split_mode_for, presplit_panels,
     make_custom_layout, make_layout, nccl_unique_id, plan_general_gemm, pool_size_class,
 )

@@ -110,6 +110,7 @@ def _load() -> C.CDLL:
                                            i64, i64, i64, C.c_int, C.c_int, vp, C.c_size_t, vp]),
         "dm_session_gemm_mode": (C.c_int, [vp, P(C.c_int)]),
         "dm_split_mode_for": (C.c_int, [C.c_int, i64, C.c_double, P(C.c_int)]),
+        "dm_presplit_panels": (C.c_int, [i64, i64, i64, i64, P(C.c_int64), C.c_int, P(C.c_int)]),
         "dm_fill_seeded_f32": (C.c_int, [vp, i64, u64, C.c_int, C.c_int, vp]),
     }
     for name, (res, args) in sigs.items():
@@ -134,5 +135,5 @@ EXPORTED = [
     "dm_set_gemm_timing", "dm_worker_seed", "dm_seed_workers", "dm_root_seed", "dm_transfer_log", "dm_descriptor_digest", "dm_block_device_ptr",
     "dm_barrier", "dm_set_async", "dm_marker_record", "dm_marker_elapsed", "dm_local_gemm_f32", "dm_local_gemm_f32_ex", "dm_fill_seeded_f32",
     "dm_local_gemm_f32_workspace_size", "dm_local_gemm_f32_ws", "dm_session_gemm_mode",
-    "dm_split_mode_for",
+    "dm_split_mode_for", "dm_presplit_panels",
 ]

@@ -530,6 +530,18 @@ int dm_session_gemm_mode(dm_session* s, int* out) {
   });
 }
 
+int dm_presplit_panels(int64_t k, int64_t a_kblock, int64_t b_kblock, int64_t max_width, int64_t* out, int cap,
+                       int* n) {
+  return guarded([&] {
+    if (out == nullptr || n == nullptr) throw dm::UsageError("presplit_panels: null output");
+    if (k <= 0 || a_kblock <= 0 || b_kblock <= 0) throw dm::ShapeError("presplit_panels: non-positive extent");
+    const std::vector<int64_t> k0 = dm::presplit_panels(k, a_kblock, b_kblock, max_width);
+    if (static_cast<int64_t>(k0.size()) > cap) throw dm::UsageError("presplit_panels: output too small");
+    std::copy(k0.begin(), k0.end(), out);
+    *n = static_cast<int>(k0.size());
+  });
+}
+
 int dm_split_mode_for(int gemm_mode, int64_t k, double work, int* out) {
   return guarded([&] {
     if (out == nullptr) throw dm::UsageError("split_mode_for: null output");

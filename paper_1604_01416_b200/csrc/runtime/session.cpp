@@ -751,34 +751,14 @@ Session::WorkerPlan Session::plan_worker(const GemmArgs& g, int w, SourcePolicy 
     // owner's arena): the segments between edges are merged up to
     // DM_PRESPLIT_PANEL wide, wider ones cut evenly (256-aligned).  Every
     // plane row carries its whole op row's scale, so a panel may span blocks.
-    std::vector<std::int64_t> cuts = {0, K};
-    auto add_cuts = [&](const BlockGrid& gr, bool k_on_rows) {
-      const std::int64_t step = k_on_rows ? gr.block_rows : gr.block_cols;
-      for (std::int64_t k = step; step > 0 && k < K; k += step) cuts.push_back(k);
-    };
-    add_cuts(da.layout.grid, g.trans_a);
-    add_cuts(db.layout.grid, !g.trans_b);
-    std::sort(cuts.begin(), cuts.end());
-    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
     // Wide panels: every panel after the first re-reads C (beta = 1), and
     // fewer, longer launches measured faster (4 GPUs: 16384-wide 1615 vs
-    // 8192-wide 1575 TFLOP/s; 2 GPUs: 855 vs 798).
-    // At least two panels, so the first one's GEMM can hide the next one's
-    // pulls (config 5, N=16384 on 2x2: one 16384-wide panel would expose
-    // every pull; 15.8 vs 11.7 ms per chain).
-    const std::int64_t maxw = std::max<std::int64_t>(
-        256, std::min(env_int("DM_PRESPLIT_PANEL", 16384), (K / 2 + 255) / 256 * 256));
-    plan.k0.clear();
-    for (std::size_t i = 0; i + 1 < cuts.size();) {
-      std::size_t j = i + 1;  // merge [cuts[i], cuts[j]) while it stays within maxw
-      while (j + 1 < cuts.size() && cuts[j + 1] - cuts[i] <= maxw) ++j;
-      const std::int64_t len = cuts[j] - cuts[i];
-      const std::int64_t n = (len + maxw - 1) / maxw;
-      const std::int64_t width = ((len + n - 1) / n + 255) / 256 * 256;
-      for (std::int64_t k = cuts[i]; k < cuts[j]; k += width) plan.k0.push_back(k);
-      i = j;
-    }
-    plan.k0.push_back(K);
+    // 8192-wide 1575 TFLOP/s; 2 GPUs: 855 vs 798); at least two (config 5,
+    // N=16384 on 2x2: one 16384-wide panel exposes every pull, 15.8 vs
+    // 11.7 ms per chain).
+    plan.k0 = presplit_panels(K, g.trans_a ? da.layout.grid.block_rows : da.layout.grid.block_cols,
+                              g.trans_b ? db.layout.grid.block_cols : db.layout.grid.block_rows,
+                              env_int("DM_PRESPLIT_PANEL", 16384));
     for (auto& r : plan.ar) add_range_pieces(r, da, g.trans_a, true, plan.k0);
     for (auto& r : plan.br) add_range_pieces(r, db, g.trans_b, false, plan.k0);
     // A worker whose every panel needs a pull waits for the first one before

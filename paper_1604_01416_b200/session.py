@@ -169,6 +169,15 @@ def plan_general_gemm(la: LayoutSpec, ta: bool, lb: LayoutSpec, tb: bool, lc: La
     return nb.value, by.value
 
 
+def presplit_panels(k: int, a_kblock: int, b_kblock: int, max_width: int = 16384) -> list:
+    """K-panel starts (then K) of a presplit GEMM (dm_presplit_panels)."""
+    cap = 4 * (k // 256 + 4) + 8
+    out = (C.c_int64 * cap)()
+    n = C.c_int()
+    _check(lib.dm_presplit_panels(int(k), int(a_kblock), int(b_kblock), int(max_width), out, cap, C.byref(n)))
+    return list(out[:n.value])
+
+
 # --------------------------------------------------------------- session
 @dataclass
 class Config:

@@ -168,3 +168,23 @@ def test_split_mode_rule(monkeypatch):
     assert dm.split_mode_for("default", 2048, 1e15) == "mixed"
     with pytest.raises(dm.UsageError):
         dm.split_mode_for("fp64", 16)
+
+
+def test_presplit_panel_rule():
+    """K panels of a presplit GEMM (layout.hpp presplit_panels): start at A's
+    and B's K-block edges, merge up to the widest panel, never fewer than two
+    (the first panel's GEMM hides the next one's pulls), 256-aligned cuts."""
+    P = dm.presplit_panels
+    assert P(32768, 16384, 16384) == [0, 16384, 32768]          # 2x2 grid
+    assert P(32768, 16384, 32768) == [0, 16384, 32768]          # 1x2 grid (B's K unblocked)
+    assert P(32768, 8192, 16384) == [0, 16384, 32768]           # 2x4: two of A's K blocks per panel
+    assert P(32768, 8192, 16384, 8192) == [0, 8192, 16384, 24576, 32768]
+    assert P(16384, 8192, 8192) == [0, 8192, 16384]             # config 5: at least two panels
+    assert P(1024, 512, 512) == [0, 512, 1024]
+    assert P(1536, 768, 768, 256) == [0, 256, 512, 768, 1024, 1280, 1536]
+    assert P(1304, 448, 448, 512) == [0, 448, 896, 1304]        # ragged edge blocks
+    assert P(2048, 256, 512, 1024) == [0, 1024, 2048]
+    k0 = P(32768, 8192, 16384)
+    assert all(b > a for a, b in zip(k0, k0[1:])) and k0[0] == 0 and k0[-1] == 32768
+    with pytest.raises(dm.ShapeError):
+        P(0, 1, 1)
