@@ -33,7 +33,7 @@ for _ in range(4):
     h = np.empty((N, N), np.float32)
     band = h[r_lo:r_hi]
     assert int(cudart.cudaHostRegister(band.ctypes.data, band.nbytes, 0)) == 0
-    band[:] = 1.0
+    band[:] = np.random.default_rng(len(hosts)).random(band.shape, dtype=np.float32)
     hosts.append(h)
 hA, hB, hC0, hC1 = hosts
 root = -1 if world > 1 else 0
@@ -72,7 +72,33 @@ def astep():
 
 s.set_async(True)
 t_async = timed(astep, reps=4)
+extra = ""
+if os.environ.get("E2E_VARIANTS", "0") == "1":
+    def step_no_gather():
+        i = it[0]
+        it[0] += 1
+        ea, eb, ec = sets[i % 2]
+        s.scatter(ea, hA)
+        s.scatter(eb, hB)
+        s.general_gemm(1.0, ea, eb, 0.0, ec)
+
+    def step_no_scatter():
+        i = it[0]
+        it[0] += 1
+        ea, eb, ec = sets[i % 2]
+        s.general_gemm(1.0, ea, eb, 0.0, ec)
+        s.gather(ec, outs[i % 2], root=root)
+
+    def step_copies_only():
+        i = it[0]
+        it[0] += 1
+        ea, eb, ec = sets[i % 2]
+        s.scatter(ea, hA)
+        s.scatter(eb, hB)
+        s.gather(ec, outs[i % 2], root=root)
+    extra = (f" async(no gather)={timed(step_no_gather, reps=4):.1f} async(no scatter)={timed(step_no_scatter, reps=4):.1f}"
+             f" async(copies only)={timed(step_copies_only, reps=4):.1f}")
 s.set_async(False)
 print(f"rank {rank}/{world} N={N}: h2d(A,B)={t_h2d:.1f} gemm={t_gemm:.1f} d2h(C)={t_d2h:.1f} "
-      f"sync_step={t_sync:.1f} async_step={t_async:.1f} ms", flush=True)
+      f"sync_step={t_sync:.1f} async_step={t_async:.1f}{extra} ms", flush=True)
 s.close()
