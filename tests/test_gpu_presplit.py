@@ -229,3 +229,21 @@ def test_presplit_same_matrix_both_operands(cuda, monkeypatch, tb):
         got = s.gather(c)
         assert all(s.worker_stats(w).split_launches == 6 for w in range(4))
     assert relfro(got, ref_gemm(0.75, A, False, A, tb, 0.25, C0)) <= TOL
+
+
+def test_presplit_panels_and_lead(cuda, monkeypatch):
+    """The K panels the workers run (dm_presplit_panels: block edges, at least
+    two) and the lead panel cut off the first panel of a worker whose every
+    panel needs a pull (2x2: the off-diagonal workers) -- GEMM launch counts."""
+    import paper_1604_01416_b200 as dm
+    n = 4096
+    assert dm.presplit_panels(n, n // 2, n // 2) == [0, 2048, 4096]
+    monkeypatch.setenv("DM_PRESPLIT_LEAD", "512")
+    err, st = run_case(4, n, n, n, (n // 2, n // 2), (n // 2, n // 2), (n // 2, n // 2), 0)
+    assert err <= TOL
+    # workers 0 and 3 own a whole local panel; 1 and 2 pull for every panel
+    assert [x.gemm_launches for x in st] == [2, 3, 3, 2], [x.gemm_launches for x in st]
+    monkeypatch.setenv("DM_PRESPLIT_LEAD", "0")
+    err, st = run_case(4, n, n, n, (n // 2, n // 2), (n // 2, n // 2), (n // 2, n // 2), 0)
+    assert err <= TOL
+    assert [x.gemm_launches for x in st] == [2, 2, 2, 2]
