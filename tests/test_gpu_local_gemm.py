@@ -188,7 +188,8 @@ def test_cuda_graph_capture_with_workspace(cuda):
         assert _relfro(C, want) <= 3e-6
 
 
-@pytest.mark.parametrize("shape", [(4096, 1024, 2048), (1000, 744, 1304), (384, 520, 4104)])
+@pytest.mark.parametrize("shape", [(4096, 1024, 2048), (1000, 744, 1304), (384, 520, 4104), (77, 96, 1004),
+                                   (130, 33, 260)])
 def test_f16x2_split_kernels_agree(cuda, monkeypatch, shape):
     """The f16x2 transposing split (split_trans_f16x2_kernel, swizzled smem
     tile, 16-B plane stores) writes the same planes as the tf32-shaped
